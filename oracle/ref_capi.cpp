@@ -1,0 +1,304 @@
+// C-ABI shim over the UNMODIFIED reference library (compiled from
+// /root/reference/proj/src by oracle/Makefile into oracle/_ref/).
+//
+// TEST INFRASTRUCTURE ONLY: loaded by tests/ (as the parity checker) and by
+// bench.py's cpu_baseline / --impl reference legs (as the timed reference
+// CPU path). Nothing in paper_2409_10516_b200/ links or loads this.
+//
+// Every entry point returns 0 on success or -1 with ref_last_error() set to
+// the reference exception's what() — the same messages the reference tests
+// assert (e.g. test_index_oodgraph.cpp:384-400).
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "attnindex/attention.hpp"
+#include "attnindex/engine.hpp"
+#include "attnindex/index_flat.hpp"
+#include "attnindex/index_oodgraph.hpp"
+#include "attnindex/util.hpp"
+#include "attnindex/workload.hpp"
+
+using namespace attnindex;
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = std::string("invalid_argument: ") + e.what();
+  } catch (const std::runtime_error& e) {
+    g_err = std::string("runtime_error: ") + e.what();
+  } catch (const std::exception& e) {
+    g_err = std::string("exception: ") + e.what();
+  }
+  return -1;
+}
+
+std::shared_ptr<const VectorSet> make_set(Role role, const float* p, uint64_t n,
+                                          uint32_t d) {
+  auto s = std::make_shared<VectorSet>(role, n, d);
+  if (n) std::memcpy(s->data.data(), p, sizeof(float) * n * d);
+  return s;
+}
+
+struct RefGraph {
+  std::shared_ptr<const VectorSet> keys;
+  std::unique_ptr<OODGraph> g;
+};
+
+void copy_result(const SearchResult& r, uint32_t* ids, float* scores,
+                 uint64_t* n_out, uint64_t* scanned, uint8_t* truncated) {
+  std::copy(r.ids.begin(), r.ids.end(), ids);
+  std::copy(r.scores.begin(), r.scores.end(), scores);
+  *n_out = r.ids.size();
+  *scanned = r.scanned;
+  *truncated = r.truncated ? 1 : 0;
+}
+
+// Decode-step harness for the CPU baseline: engine_init's per-head state,
+// but with graphs loaded from OODG blobs (index_oodgraph.hpp:40) so 128K
+// graphs need not be rebuilt on the CPU.
+struct RefEngine {
+  EngineState st;
+};
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+uint64_t ref_splitmix64(uint64_t* state) { return splitmix64(*state); }
+
+// generate_workload (workload.cpp:102-203). Outputs, all f32 row-major:
+// prefill_q[n_heads][n_ctx][d_head], decode_q[n_heads][n_decode][d_head],
+// keys[n_kv_groups][n_ctx][d_head], values[n_kv_groups][n_ctx][d_head].
+int ref_generate_workload(uint64_t n_ctx, uint32_t d_model, uint32_t d_head,
+                          uint32_t n_heads, uint32_t n_kv_groups, uint64_t seed,
+                          double ood_strength, double concentration, uint64_t n_decode,
+                          int n_threads, float* prefill_q, float* decode_q, float* keys,
+                          float* values) {
+  return guard([&] {
+    WorkloadSpec s;
+    s.n_ctx = n_ctx;
+    s.d_model = d_model;
+    s.d_head = d_head;
+    s.n_heads = n_heads;
+    s.n_kv_groups = n_kv_groups;
+    s.seed = seed;
+    s.ood_strength = ood_strength;
+    s.concentration = concentration;
+    s.n_decode = n_decode;
+    auto heads = generate_workload(s, n_threads);
+    const size_t per_ctx = size_t(n_ctx) * d_head, per_dec = size_t(n_decode) * d_head;
+    for (uint32_t h = 0; h < n_heads; ++h) {
+      std::memcpy(prefill_q + h * per_ctx, heads[h].prefill_queries.data.data(),
+                  per_ctx * sizeof(float));
+      std::memcpy(decode_q + h * per_dec, heads[h].decode_queries.data.data(),
+                  per_dec * sizeof(float));
+      const uint32_t g = heads[h].kv_group_id;
+      std::memcpy(keys + g * per_ctx, heads[h].keys->data.data(), per_ctx * sizeof(float));
+      std::memcpy(values + g * per_ctx, heads[h].values->data.data(),
+                  per_ctx * sizeof(float));
+    }
+  });
+}
+
+int ref_graph_build(const float* keys, uint64_t n, uint32_t d, const float* train_q,
+                    uint64_t nq, uint32_t k_train, uint32_t max_degree,
+                    uint32_t ef_construction, uint32_t edge_window, int entry_maxnorm,
+                    int prune_inner_product, uint32_t default_ef, int n_threads,
+                    void** out) {
+  return guard([&] {
+    auto h = std::make_unique<RefGraph>();
+    h->keys = make_set(Role::Key, keys, n, d);
+    VectorSet tq(Role::Query, nq, d);
+    if (nq) std::memcpy(tq.data.data(), train_q, sizeof(float) * nq * d);
+    OODGraphBuildParams p;
+    p.k_train = k_train;
+    p.max_degree = max_degree;
+    p.ef_construction = ef_construction;
+    p.edge_window = edge_window;
+    p.entry_strategy = entry_maxnorm ? EntryStrategy::MaxNorm : EntryStrategy::Medoid;
+    p.prune_rule = prune_inner_product ? PruneRule::InnerProduct : PruneRule::Euclidean;
+    p.default_ef = default_ef;
+    h->g = ood_build(h->keys, tq, p, n_threads);
+    *out = h.release();
+  });
+}
+
+int ref_graph_from_blob(const float* keys, uint64_t n, uint32_t d, const char* blob,
+                        uint64_t size, void** out) {
+  return guard([&] {
+    auto h = std::make_unique<RefGraph>();
+    h->keys = make_set(Role::Key, keys, n, d);
+    h->g = std::make_unique<OODGraph>(h->keys, std::string(blob, size));
+    *out = h.release();
+  });
+}
+
+void ref_graph_free(void* g) { delete static_cast<RefGraph*>(g); }
+
+// Writes the OODG v1 blob (index_oodgraph.cpp:435-449) when cap suffices;
+// always reports the size.
+int ref_graph_serialize(void* g, char* buf, uint64_t cap, uint64_t* size) {
+  return guard([&] {
+    const std::string b = static_cast<RefGraph*>(g)->g->serialize();
+    *size = b.size();
+    if (buf && cap >= b.size()) std::memcpy(buf, b.data(), b.size());
+  });
+}
+
+uint64_t ref_graph_entry(void* g) { return static_cast<RefGraph*>(g)->g->entry_point(); }
+
+int ref_graph_search(void* g, const float* q, uint32_t d, uint64_t k,
+                     const uint32_t* mask, uint64_t mask_n, int64_t ef, uint32_t* ids,
+                     float* scores, uint64_t* n_out, uint64_t* scanned,
+                     uint8_t* truncated) {
+  return guard([&] {
+    const auto& G = *static_cast<RefGraph*>(g)->g;
+    std::optional<uint32_t> ef_opt;
+    if (ef >= 0) ef_opt = uint32_t(ef);
+    auto r = G.search(std::span<const float>(q, d), k,
+                      Mask{std::span<const uint32_t>(mask, mask_n)}, ef_opt);
+    copy_result(r, ids, scores, n_out, scanned, truncated);
+  });
+}
+
+int ref_flat_search(const float* keys, uint64_t n, uint32_t d, const float* q, uint64_t k,
+                    const uint32_t* mask, uint64_t mask_n, uint32_t* ids, float* scores,
+                    uint64_t* n_out, uint64_t* scanned) {
+  return guard([&] {
+    auto ks = make_set(Role::Key, keys, n, d);
+    FlatIndex f(ks);
+    auto r = f.search(std::span<const float>(q, d), k,
+                      Mask{std::span<const uint32_t>(mask, mask_n)});
+    uint8_t t;
+    copy_result(r, ids, scores, n_out, scanned, &t);
+  });
+}
+
+// partial_attention (attention.cpp:102-128); out has d doubles.
+int ref_partial_attention(const float* q, const float* keys, const float* values,
+                          uint64_t n, uint32_t d, const uint32_t* idx, uint64_t m,
+                          double* out, double* zmax, double* expsum) {
+  return guard([&] {
+    VectorSet K(Role::Key, n, d), V(Role::Value, n, d);
+    std::memcpy(K.data.data(), keys, sizeof(float) * n * d);
+    std::memcpy(V.data.data(), values, sizeof(float) * n * d);
+    auto p = partial_attention(std::span<const float>(q, d), K, V,
+                               std::span<const uint32_t>(idx, m));
+    std::copy(p.out.begin(), p.out.end(), out);
+    *zmax = p.zmax;
+    *expsum = p.expsum;
+  });
+}
+
+// merge (attention.cpp:149-157); a side with empty != 0 is empty_partial(d).
+int ref_merge(uint32_t d, const double* ow, double zw, double sw, int w_empty,
+              const double* oo, double zo, double so, int o_empty, double* out,
+              double* gw, double* go) {
+  return guard([&] {
+    PartialAttention pw, po;
+    pw.out.assign(ow, ow + d);
+    pw.zmax = zw;
+    pw.expsum = sw;
+    pw.empty = w_empty != 0;
+    po.out.assign(oo, oo + d);
+    po.zmax = zo;
+    po.expsum = so;
+    po.empty = o_empty != 0;
+    if (pw.empty) pw = empty_partial(d);
+    if (po.empty) po = empty_partial(d);
+    auto [a, b] = merge_gammas(pw, po);
+    *gw = a;
+    *go = b;
+    auto r = merge(pw, po);
+    std::copy(r.begin(), r.end(), out);
+  });
+}
+
+int ref_static_partition(uint64_t t, uint64_t s_init, uint64_t s_local,
+                         uint32_t* static_ids, uint64_t* n_static, uint32_t* pool_ids,
+                         uint64_t* n_pool) {
+  return guard([&] {
+    auto p = static_partition(t, s_init, s_local);
+    if (static_ids) std::copy(p.static_set.begin(), p.static_set.end(), static_ids);
+    if (pool_ids) std::copy(p.dynamic_pool.begin(), p.dynamic_pool.end(), pool_ids);
+    *n_static = p.static_set.size();
+    *n_pool = p.dynamic_pool.size();
+  });
+}
+
+// ---- decode engine over blob-loaded graphs (engine.cpp:69-115) -------------
+// keys/values: [n_groups][t][d]; head h uses group h / (n_heads / n_groups);
+// blobs: concatenated OODG blobs, one per head, sizes in blob_sizes.
+int ref_engine_create(const float* keys, const float* values, uint64_t t, uint32_t d,
+                      uint32_t n_heads, uint32_t n_groups, const char* blobs,
+                      const uint64_t* blob_sizes, uint64_t s_init, uint64_t s_local,
+                      uint32_t top_k, int64_t ef, int n_threads, void** out) {
+  return guard([&] {
+    auto e = std::make_unique<RefEngine>();
+    EngineConfig& c = e->st.config;
+    c.s_init = s_init;
+    c.s_local = s_local;
+    c.top_k = top_k;
+    c.index_kind = IndexKind::OODGraph;
+    if (ef >= 0) c.search_param = uint32_t(ef);
+    c.n_threads = n_threads;
+    e->st.t = t;
+    std::vector<std::shared_ptr<const VectorSet>> K(n_groups), V(n_groups);
+    for (uint32_t g = 0; g < n_groups; ++g) {
+      K[g] = make_set(Role::Key, keys + size_t(g) * t * d, t, d);
+      V[g] = make_set(Role::Value, values + size_t(g) * t * d, t, d);
+    }
+    const uint32_t per = n_heads / n_groups;
+    size_t off = 0;
+    e->st.heads.resize(n_heads);
+    for (uint32_t h = 0; h < n_heads; ++h) {
+      HeadState& hs = e->st.heads[h];
+      hs.head_id = h;
+      hs.kv_group_id = h / per;
+      hs.partition = static_partition(t, s_init, s_local);
+      hs.keys = K[h / per];
+      hs.values = V[h / per];
+      hs.index = std::make_unique<OODGraph>(hs.keys, std::string(blobs + off, blob_sizes[h]));
+      off += blob_sizes[h];
+    }
+    *out = e.release();
+  });
+}
+
+void ref_engine_free(void* e) { delete static_cast<RefEngine*>(e); }
+
+// One decode_step over all heads: q [n_heads][d] -> out [n_heads][d] f64,
+// omega ids [n_heads][top_k] (UINT32_MAX padded), scanned [n_heads].
+int ref_engine_step(void* e, const float* q, uint64_t step, double* out, uint32_t* omega,
+                    uint64_t* scanned) {
+  return guard([&] {
+    const auto& st = static_cast<RefEngine*>(e)->st;
+    const uint32_t d = st.heads[0].keys->d;
+    std::vector<std::span<const float>> qs(st.heads.size());
+    for (size_t h = 0; h < qs.size(); ++h) qs[h] = std::span<const float>(q + h * d, d);
+    auto entries = decode_step(st, qs, step);
+    const uint32_t k = st.config.top_k;
+    for (size_t h = 0; h < entries.size(); ++h) {
+      if (out) std::copy(entries[h].out.begin(), entries[h].out.end(), out + h * d);
+      if (omega) {
+        for (uint32_t i = 0; i < k; ++i)
+          omega[h * k + i] = i < entries[h].omega.size() ? entries[h].omega[i] : UINT32_MAX;
+      }
+      if (scanned) scanned[h] = entries[h].scanned;
+    }
+  });
+}
+
+}  // extern "C"
