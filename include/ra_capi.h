@@ -1,0 +1,195 @@
+/* ra_capi.h — C ABI of the B200-native RetrievalAttention decode hot path.
+ *
+ * One shared library (paper_2409_10516_b200/libra_b200.so), sm_100a only.
+ * Plain pointers, sizes and an opaque stream (cudaStream_t passed as void*);
+ * no C++ or torch types cross this boundary. Every call returns ra_status;
+ * on failure ra_last_error() (thread-local) holds the message, which for
+ * argument errors is the reference's exact exception text, so an adapter can
+ * rethrow the same std::invalid_argument / std::runtime_error.
+ *
+ * Reference interfaces replaced (paths under /root/reference/proj):
+ *   ra_graph_build          <- ood_build / OODGraph::OODGraph     include/attnindex/index_oodgraph.hpp:35-36,78-81
+ *   ra_graph_deserialize    <- OODGraph(keys, blob) / load        include/attnindex/index_oodgraph.hpp:40,63-64
+ *   ra_graph_serialize      <- OODGraph::serialize / save         include/attnindex/index_oodgraph.hpp:61-62
+ *   ra_graph_* accessors    <- entry_point/degree/neighbors/...    include/attnindex/index_oodgraph.hpp:49-59
+ *   ra_graph_search_batch   <- SearchIndex::search (OODGraph)      include/attnindex/index.hpp:41-42
+ *   ra_flat_search_batch    <- FlatIndex::search                   include/attnindex/index_flat.hpp:14-15
+ *   ra_partial_attention    <- partial_attention                   include/attnindex/attention.hpp:47-50
+ *   ra_merge                <- merge_gammas + merge                include/attnindex/attention.hpp:52-60
+ *   ra_static_partition     <- static_partition                    include/attnindex/attention.hpp:44-45
+ *   ra_engine_* / decode    <- engine_init / decode_step           include/attnindex/engine.hpp:103-111
+ *
+ * Memory: "host" pointers are ordinary CPU memory (pinned recommended);
+ * "device" pointers are CUDA global memory on the context's device. Each
+ * function documents which it takes. Handles are immutable after creation
+ * and may be used from several threads; an ra_ctx (stream + scratch) must
+ * not be shared between threads concurrently.
+ */
+#ifndef RA_CAPI_H
+#define RA_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RA_OK = 0,
+  RA_ERR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+  RA_ERR_RUNTIME = 2,          /* reference: std::runtime_error (blob errors) */
+  RA_ERR_CUDA = 3,             /* CUDA failure, no usable device, or missing sm_100a */
+  RA_ERR_CAPACITY = 4          /* internal capacity exceeded (never silent) */
+} ra_status;
+
+typedef struct ra_ctx ra_ctx;     /* device + stream + scratch arena */
+typedef struct ra_kv ra_kv;       /* one KV group resident in HBM (refcounted) */
+typedef struct ra_graph ra_graph; /* one query head's OODGraph on the device */
+typedef struct ra_engine ra_engine;
+
+/* OODGraphBuildParams (index_oodgraph.hpp:17-27); ra_build_params_default
+ * fills the reference defaults 32/32/128/8, Medoid, Euclidean, ef 128. */
+typedef struct {
+  uint32_t k_train;
+  uint32_t max_degree;
+  uint32_t ef_construction;
+  uint32_t edge_window;
+  int32_t entry_maxnorm;       /* 0 = EntryStrategy::Medoid, 1 = MaxNorm */
+  int32_t prune_inner_product; /* 0 = PruneRule::Euclidean, 1 = InnerProduct */
+  uint32_t default_ef;
+} ra_build_params;
+
+/* Per-build diagnostics (not part of the reference API). */
+typedef struct {
+  uint64_t knn_rows;          /* training queries processed in phase 1 */
+  uint64_t knn_rows_widened;  /* rows whose approximate top-k had to be rescanned */
+  uint64_t candidate_edges;   /* unique (src,dst) proposals after phase 2 */
+  uint64_t repair_rounds;     /* phase-4 iterations */
+  uint64_t repaired_nodes;    /* nodes attached by phase 4 */
+  double ms_knn, ms_edges, ms_prune, ms_entry, ms_repair;
+} ra_build_stats;
+
+const char* ra_last_error(void);
+const char* ra_version(void);
+
+/* ---- context ------------------------------------------------------------ */
+ra_status ra_ctx_create(int device, ra_ctx** out);
+void ra_ctx_destroy(ra_ctx* ctx);
+/* stream: a cudaStream_t (NULL = legacy default). Kernels of this ctx are
+ * enqueued on it; calls taking host buffers synchronize it before returning. */
+ra_status ra_ctx_set_stream(ra_ctx* ctx, void* stream);
+ra_status ra_ctx_synchronize(ra_ctx* ctx);
+
+/* ---- KV groups (types.hpp:18-35, 54-61) ------------------------------------
+ * keys/values: n x d f32 row-major; values may be NULL (search-only).
+ * on_device = 0: host pointers, copied in; 1: device pointers, copied too
+ * (the ra_kv owns its HBM). The handle is shared by all query heads of the
+ * GQA group (refcount), mirroring the shared_ptr<const VectorSet>. */
+ra_status ra_kv_create(ra_ctx* ctx, const float* keys, const float* values, uint64_t n,
+                       uint32_t d, int on_device, ra_kv** out);
+void ra_kv_retain(ra_kv* kv);
+void ra_kv_release(ra_kv* kv);
+uint64_t ra_kv_size(const ra_kv* kv);
+uint32_t ra_kv_dim(const ra_kv* kv);
+const float* ra_kv_keys_device(const ra_kv* kv);
+const float* ra_kv_values_device(const ra_kv* kv);
+
+/* ---- graph index ------------------------------------------------------------ */
+void ra_build_params_default(ra_build_params* p);
+/* ood_build: train_q nq x d f32, host (on_device = 0) or device (1). Not
+ * stored. stats may be NULL. Errors: "empty keys", "too many keys",
+ * "k_train must be >= 1", "max_degree must be >= 1",
+ * "ef_construction must be >= 1", "query dimension mismatch". */
+ra_status ra_graph_build(ra_ctx* ctx, ra_kv* keys, const float* train_q, uint64_t nq,
+                         uint32_t q_dim, int on_device, const ra_build_params* params,
+                         ra_build_stats* stats, ra_graph** out);
+/* OODG v1 blob (host bytes). Errors are the reference's runtime_error texts. */
+ra_status ra_graph_deserialize(ra_ctx* ctx, ra_kv* keys, const char* blob, uint64_t size,
+                               ra_graph** out);
+/* Writes when buf != NULL and cap >= size; always sets *size. */
+ra_status ra_graph_serialize(const ra_graph* g, char* buf, uint64_t cap, uint64_t* size);
+void ra_graph_free(ra_graph* g);
+uint64_t ra_graph_size(const ra_graph* g);
+uint64_t ra_graph_entry_point(const ra_graph* g);
+uint32_t ra_graph_max_degree_bound(const ra_graph* g);
+uint32_t ra_graph_default_ef(const ra_graph* g);
+uint32_t ra_graph_degree(const ra_graph* g, uint64_t u);
+/* copies neighbors(u) (at most cap) into out (host); returns the degree */
+uint32_t ra_graph_neighbors(const ra_graph* g, uint64_t u, uint32_t* out, uint32_t cap);
+uint64_t ra_graph_reachable_count(const ra_graph* g);
+/* OODGraph::memory_bytes (index_oodgraph.cpp:413-415): CSR u64 offsets + u32 adjacency */
+uint64_t ra_graph_memory_bytes(const ra_graph* g);
+/* HBM actually held by the device-side adjacency */
+uint64_t ra_graph_device_bytes(const ra_graph* g);
+
+/* ---- search (OODGraph::search, index_oodgraph.cpp:357-411) -----------------
+ * B queries; query b searches graphs[b] (graphs may repeat) with q + b*d.
+ * All array arguments are DEVICE pointers: q [B][d] f32; mask: sorted,
+ * duplicate-free excluded ids shared by the batch (mask_n may be 0).
+ * ef < 0 selects each graph's default_ef. Outputs: ids/scores [B][k]
+ * (slots past n_out padded with UINT32_MAX / NaN), n_out, scanned, truncated
+ * [B]; expanded [B] (optional, NULL ok) counts frontier pops.
+ * Errors: "k must be >= 1", "ef must be >= k", "query dimension mismatch". */
+ra_status ra_graph_search_batch(ra_ctx* ctx, const ra_graph* const* graphs, uint32_t B,
+                                const float* q, uint32_t q_dim, uint32_t k, int64_t ef,
+                                const uint32_t* mask, uint64_t mask_n, uint32_t* ids,
+                                float* scores, uint32_t* n_out, uint64_t* scanned,
+                                uint8_t* truncated, uint32_t* expanded);
+
+/* FlatIndex::search (index_flat.cpp:22-43): exact top-k by f64 inner product
+ * with the same (score desc, id asc) order. Device pointers as above. */
+ra_status ra_flat_search_batch(ra_ctx* ctx, ra_kv* keys, uint32_t B, const float* q,
+                               uint32_t k, const uint32_t* mask, uint64_t mask_n,
+                               uint32_t* ids, float* scores, uint64_t* scanned);
+
+/* ---- attention (attention.cpp:87-157) ------------------------------------- */
+/* static_partition into host arrays (either may be NULL to just count). */
+ra_status ra_static_partition(uint64_t t, uint64_t s_init, uint64_t s_local,
+                              uint32_t* static_ids, uint64_t* n_static, uint32_t* pool_ids,
+                              uint64_t* n_pool);
+/* partial_attention for B queries against one KV group. Device pointers:
+ * q [B][d], idx [B][m_stride] (row b uses its first m[b] entries; m[b] = 0
+ * yields an empty partial), out [B][d] f64, zmax/expsum [B] f64. Errors:
+ * "keys and values must have equal n" (values missing), "index out of range". */
+ra_status ra_partial_attention(ra_ctx* ctx, ra_kv* kv, uint32_t B, const float* q,
+                               const uint32_t* idx, uint32_t m_stride, const uint32_t* m,
+                               double* out, double* zmax, double* expsum);
+/* merge of B partial pairs (device arrays; *_empty [B] u8 flags). Error
+ * "empty attention support" if both sides of any row are empty. */
+ra_status ra_merge(ra_ctx* ctx, uint32_t B, uint32_t d, const double* ow, const double* zw,
+                   const double* sw, const uint8_t* w_empty, const double* oo,
+                   const double* zo, const double* so, const uint8_t* o_empty, double* out,
+                   double* gw, double* go);
+
+/* ---- decode engine (engine.cpp:23-115) ------------------------------------------
+ * n_heads query heads over n_groups KV groups (head h -> group
+ * h / (n_heads / n_groups)), one graph per head, frozen static partition at
+ * t = kv size. ef < 0 selects default_ef. */
+typedef struct {
+  uint64_t s_init;   /* 128 */
+  uint64_t s_local;  /* 512 */
+  uint32_t top_k;    /* 100 */
+  int64_t ef;        /* search_param; < 0 = index default */
+} ra_engine_config;
+
+ra_status ra_engine_create(ra_ctx* ctx, ra_kv* const* groups, uint32_t n_groups,
+                           ra_graph* const* head_graphs, uint32_t n_heads,
+                           const ra_engine_config* cfg, ra_engine** out);
+void ra_engine_destroy(ra_engine* e);
+/* decode_step on DEVICE buffers: q [H][d] f32 -> out [H][d] f64; omega
+ * [H][top_k] u32 (UINT32_MAX padded) and scanned [H] u64 may be NULL. */
+ra_status ra_engine_step_device(ra_engine* e, const float* q, double* out, uint32_t* omega,
+                                uint64_t* scanned);
+/* decode_step on HOST buffers: H2D of q, the step, D2H of out/omega/scanned,
+ * synchronized. This is the drop-in call a CPU-side engine makes. */
+ra_status ra_engine_step_host(ra_engine* e, const float* q, double* out, uint32_t* omega,
+                              uint64_t* scanned);
+/* device-side counters of the last step (for roofline accounting) */
+ra_status ra_engine_last_stats(ra_engine* e, uint64_t* total_scanned,
+                               uint64_t* total_expanded);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RA_CAPI_H */

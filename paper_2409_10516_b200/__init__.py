@@ -1,0 +1,15 @@
+"""B200-native RetrievalAttention decode hot path (arXiv 2409.10516).
+
+Drop-in for the reference attnindex library's graph build, graph search,
+sparse attention and partial-softmax merge; compute runs in the sm_100a
+library libra_b200.so (C ABI: include/ra_capi.h). Importing this package
+loads (building if necessary) that library; there is no CPU fallback.
+"""
+from ._capi import EXPORTED, lib  # noqa: F401  (loads libra_b200.so, loudly)
+from .api import (  # noqa: F401
+    BatchResult, BuildStats, Context, CudaError, Engine, EngineConfig, GraphError,
+    InvalidArgument, KVGroup, KVPartition, OODGraph, OODGraphBuildParams, PartialAttention,
+    SearchResult, default_context, empty_partial, merge, merge_gammas, ood_build,
+    partial_attention, search_batch, static_partition)
+
+__version__ = lib.ra_version().decode()

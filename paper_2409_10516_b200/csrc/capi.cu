@@ -1,0 +1,589 @@
+// C ABI of libra_b200.so (include/ra_capi.h): handles, validation with the
+// reference's error texts, OODG v1 (de)serialization, and the decode engine
+// that strings K6 (search) and K7 (partials + merge) together per step.
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <numeric>
+
+#include "common.cuh"
+
+namespace ra {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+void graph_upload(ra_ctx* ctx, ra_graph* g) {
+  const uint64_t n = g->n;
+  const uint32_t M = g->max_degree;
+  std::vector<uint32_t> rows(size_t(n) * M, kSentinel);
+  for (uint64_t u = 0; u < n; ++u)
+    std::copy(g->adjacency.begin() + g->offsets[u], g->adjacency.begin() + g->offsets[u + 1],
+              rows.begin() + u * M);
+  g->adj.alloc(rows.size());
+  RA_CUDA(cudaMemcpyAsync(g->adj.p, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice,
+                          ctx->stream));
+  RA_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+static void check_ctx(ra_ctx* ctx) {
+  if (!ctx) invalid("null context");
+}
+
+}  // namespace ra
+
+using namespace ra;
+
+extern "C" {
+
+const char* ra_last_error(void) { return g_last_error.c_str(); }
+const char* ra_version(void) { return "ra_b200 0.1 (sm_100a)"; }
+
+// ---- context ----------------------------------------------------------------
+ra_status ra_ctx_create(int device, ra_ctx** out) {
+  return guard([&] {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+      throw Error(RA_ERR_CUDA, "no CUDA device available (libra_b200 has no CPU fallback)");
+    if (device < 0 || device >= count) invalid("device index out of range");
+    cudaDeviceProp prop{};
+    RA_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      throw Error(RA_ERR_CUDA, std::string("libra_b200 is built for sm_100a; device is ") +
+                                   prop.name);
+    auto c = std::make_unique<ra_ctx>();
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    c->smem_optin = prop.sharedMemPerBlockOptin;
+    *out = c.release();
+  });
+}
+
+void ra_ctx_destroy(ra_ctx* ctx) {
+  if (!ctx) return;
+  DeviceGuard dg(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  delete ctx;
+}
+
+ra_status ra_ctx_set_stream(ra_ctx* ctx, void* stream) {
+  return guard([&] {
+    check_ctx(ctx);
+    ctx->stream = static_cast<cudaStream_t>(stream);
+  });
+}
+
+ra_status ra_ctx_synchronize(ra_ctx* ctx) {
+  return guard([&] {
+    check_ctx(ctx);
+    DeviceGuard dg(ctx->device);
+    RA_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+// ---- KV groups ------------------------------------------------------------------
+ra_status ra_kv_create(ra_ctx* ctx, const float* keys, const float* values, uint64_t n,
+                       uint32_t d, int on_device, ra_kv** out) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (d < 1) invalid("VectorSet.d must be >= 1");
+    DeviceGuard dg(ctx->device);
+    auto kv = std::make_unique<ra_kv>();
+    kv->device = ctx->device;
+    kv->n = n;
+    kv->d = d;
+    const auto kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    kv->keys.alloc(size_t(n) * d);
+    if (n) RA_CUDA(cudaMemcpyAsync(kv->keys.p, keys, size_t(n) * d * 4, kind, ctx->stream));
+    if (values) {
+      kv->values.alloc(size_t(n) * d);
+      if (n)
+        RA_CUDA(cudaMemcpyAsync(kv->values.p, values, size_t(n) * d * 4, kind, ctx->stream));
+    }
+    RA_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = kv.release();
+  });
+}
+
+void ra_kv_retain(ra_kv* kv) {
+  if (kv) kv->refs.fetch_add(1);
+}
+void ra_kv_release(ra_kv* kv) {
+  if (kv && kv->refs.fetch_sub(1) == 1) {
+    DeviceGuard dg(kv->device);
+    delete kv;
+  }
+}
+uint64_t ra_kv_size(const ra_kv* kv) { return kv ? kv->n : 0; }
+uint32_t ra_kv_dim(const ra_kv* kv) { return kv ? kv->d : 0; }
+const float* ra_kv_keys_device(const ra_kv* kv) { return kv ? kv->keys.p : nullptr; }
+const float* ra_kv_values_device(const ra_kv* kv) { return kv ? kv->values.p : nullptr; }
+
+// ---- graphs -------------------------------------------------------------------------
+void ra_build_params_default(ra_build_params* p) {
+  p->k_train = 32;
+  p->max_degree = 32;
+  p->ef_construction = 128;
+  p->edge_window = 8;
+  p->entry_maxnorm = 0;
+  p->prune_inner_product = 0;
+  p->default_ef = 128;
+}
+
+// OODGraph::from_blob (index_oodgraph.cpp:468-495), same checks and messages
+ra_status ra_graph_deserialize(ra_ctx* ctx, ra_kv* keys, const char* blob, uint64_t size,
+                               ra_graph** out) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (!keys || keys->n == 0) invalid("empty keys");
+    if (size < 4 || std::memcmp(blob, "OODG", 4) != 0) runtime("bad graph magic");
+    uint64_t pos = 4;
+    auto rd = [&](void* dst, size_t bytes) {
+      if (pos + bytes > size) runtime("truncated graph blob");
+      std::memcpy(dst, blob + pos, bytes);
+      pos += bytes;
+    };
+    uint32_t version;
+    rd(&version, 4);
+    if (version != 1) runtime("unsupported graph version");
+    uint64_t n;
+    rd(&n, 8);
+    if (n != keys->n) runtime("graph/key count mismatch");
+    auto g = std::make_unique<ra_graph>();
+    rd(&g->max_degree, 4);
+    if (g->max_degree < 1) runtime("bad degree bound");
+    rd(&g->entry, 8);
+    if (g->entry >= n) runtime("entry point out of range");
+    g->n = n;
+    g->offsets.assign(n + 1, 0);
+    for (uint64_t u = 0; u < n; ++u) {
+      uint32_t deg;
+      rd(&deg, 4);
+      if (deg > g->max_degree) runtime("degree exceeds bound");
+      g->offsets[u + 1] = g->offsets[u] + deg;
+      for (uint32_t j = 0; j < deg; ++j) {
+        uint64_t v;
+        rd(&v, 8);
+        if (v >= n) runtime("neighbor id out of range");
+        if (v == u) runtime("self loop");
+        g->adjacency.push_back(uint32_t(v));
+      }
+    }
+    if (pos != size) runtime("trailing bytes in graph blob");
+    DeviceGuard dg(ctx->device);
+    graph_upload(ctx, g.get());
+    ra_kv_retain(keys);
+    g->kv = keys;
+    *out = g.release();
+  });
+}
+
+// OODGraph::serialize (index_oodgraph.cpp:435-449)
+ra_status ra_graph_serialize(const ra_graph* g, char* buf, uint64_t cap, uint64_t* size) {
+  return guard([&] {
+    if (!g) invalid("null graph");
+    const uint64_t n = g->n;
+    const uint64_t total = 28 + 4 * n + 8 * uint64_t(g->adjacency.size());
+    *size = total;
+    if (!buf || cap < total) return;
+    char* p = buf;
+    auto put = [&](const void* v, size_t b) {
+      std::memcpy(p, v, b);
+      p += b;
+    };
+    const uint32_t ver = 1;
+    put("OODG", 4);
+    put(&ver, 4);
+    put(&n, 8);
+    put(&g->max_degree, 4);
+    put(&g->entry, 8);
+    for (uint64_t u = 0; u < n; ++u) {
+      const uint32_t deg = uint32_t(g->offsets[u + 1] - g->offsets[u]);
+      put(&deg, 4);
+      for (uint64_t j = g->offsets[u]; j < g->offsets[u + 1]; ++j) {
+        const uint64_t v = g->adjacency[j];
+        put(&v, 8);
+      }
+    }
+  });
+}
+
+void ra_graph_free(ra_graph* g) {
+  if (!g) return;
+  {
+    DeviceGuard dg(g->kv ? g->kv->device : 0);
+    g->adj.reset();
+  }
+  ra_kv_release(g->kv);
+  delete g;
+}
+
+uint64_t ra_graph_size(const ra_graph* g) { return g->n; }
+uint64_t ra_graph_entry_point(const ra_graph* g) { return g->entry; }
+uint32_t ra_graph_max_degree_bound(const ra_graph* g) { return g->max_degree; }
+uint32_t ra_graph_default_ef(const ra_graph* g) { return g->default_ef; }
+uint32_t ra_graph_degree(const ra_graph* g, uint64_t u) {
+  return uint32_t(g->offsets[u + 1] - g->offsets[u]);
+}
+uint32_t ra_graph_neighbors(const ra_graph* g, uint64_t u, uint32_t* out, uint32_t cap) {
+  const uint32_t deg = ra_graph_degree(g, u);
+  std::copy_n(g->adjacency.begin() + g->offsets[u], std::min(deg, cap), out);
+  return deg;
+}
+// reachable_count (index_oodgraph.cpp:417-433)
+uint64_t ra_graph_reachable_count(const ra_graph* g) {
+  std::vector<uint8_t> seen(g->n, 0);
+  std::vector<uint32_t> stack{uint32_t(g->entry)};
+  seen[g->entry] = 1;
+  uint64_t count = 1;
+  while (!stack.empty()) {
+    const uint32_t u = stack.back();
+    stack.pop_back();
+    for (uint64_t j = g->offsets[u]; j < g->offsets[u + 1]; ++j) {
+      const uint32_t v = g->adjacency[j];
+      if (!seen[v]) {
+        seen[v] = 1;
+        ++count;
+        stack.push_back(v);
+      }
+    }
+  }
+  return count;
+}
+uint64_t ra_graph_memory_bytes(const ra_graph* g) {
+  return g->offsets.size() * 8 + g->adjacency.size() * 4;
+}
+uint64_t ra_graph_device_bytes(const ra_graph* g) { return g->adj.bytes(); }
+
+// ---- search ------------------------------------------------------------------------------
+ra_status ra_graph_search_batch(ra_ctx* ctx, const ra_graph* const* graphs, uint32_t B,
+                                const float* q, uint32_t q_dim, uint32_t k, int64_t ef,
+                                const uint32_t* mask, uint64_t mask_n, uint32_t* ids,
+                                float* scores, uint32_t* n_out, uint64_t* scanned,
+                                uint8_t* truncated, uint32_t* expanded) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (B == 0) return;
+    uint32_t max_n = 0;
+    std::vector<GraphDesc> desc(B);
+    for (uint32_t b = 0; b < B; ++b) {
+      const ra_graph* g = graphs[b];
+      if (!g) invalid("null graph");
+      if (q_dim != g->kv->d) invalid("query dimension mismatch");  // :359
+      if (k < 1) invalid("k must be >= 1");                         // :360
+      const uint64_t e = ef >= 0 ? uint64_t(ef) : g->default_ef;
+      if (e < k) invalid("ef must be >= k");                        // :362
+      desc[b] = GraphDesc{g->adj.p, g->kv->keys.p, g->entry, uint32_t(g->n), g->max_degree,
+                          uint32_t(std::min<uint64_t>(e, 0xFFFFFFFFu)), 0};
+      max_n = std::max<uint32_t>(max_n, uint32_t(g->n));
+    }
+    DeviceGuard dg(ctx->device);
+    const uint64_t words = (uint64_t(max_n) + 31) / 32;
+    const size_t desc_bytes = (B * sizeof(GraphDesc) + 255) & ~size_t(255);
+    uint8_t* a = arena<uint8_t>(ctx->scratch_a, desc_bytes + words * 4 + 256);
+    GraphDesc* d_desc = reinterpret_cast<GraphDesc*>(a);
+    uint32_t* bits = reinterpret_cast<uint32_t*>(a + desc_bytes);
+    RA_CUDA(cudaMemcpyAsync(d_desc, desc.data(), B * sizeof(GraphDesc), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    if (mask_n) launch_mask_bitset(ctx->stream, mask, mask_n, bits, words);
+    SearchArgs sa{};
+    sa.desc = d_desc;
+    sa.q = q;
+    sa.mask_bits = mask_n ? bits : nullptr;
+    sa.B = B;
+    sa.d = q_dim;
+    sa.k = k;
+    sa.ids = ids;
+    sa.scores = scores;
+    sa.scores64 = nullptr;
+    sa.n_out = n_out;
+    sa.scanned = scanned;
+    sa.truncated = truncated;
+    sa.expanded = expanded;
+    const size_t sbytes = search_scratch_bytes(ctx, B, max_n, q_dim);
+    uint8_t* scr = sbytes ? arena<uint8_t>(ctx->scratch_b, sbytes) : nullptr;
+    launch_graph_search(ctx, sa, max_n, scr);
+  });
+}
+
+ra_status ra_flat_search_batch(ra_ctx*, ra_kv*, uint32_t, const float*, uint32_t,
+                               const uint32_t*, uint64_t, uint32_t*, float*, uint64_t*) {
+  return guard([&] { runtime("flat search is not part of this build yet"); });
+}
+
+// ---- attention ------------------------------------------------------------------------------
+ra_status ra_static_partition(uint64_t t, uint64_t s_init, uint64_t s_local,
+                              uint32_t* static_ids, uint64_t* n_static, uint32_t* pool_ids,
+                              uint64_t* n_pool) {
+  return guard([&] {
+    if (t > 0xFFFFFFFFull) invalid("context length exceeds id width");
+    const uint64_t head_end = std::min(s_init, t);
+    const uint64_t tail_begin = t > s_local ? std::max(t - s_local, head_end) : head_end;
+    uint64_t ns = 0, np = 0;
+    for (uint64_t i = 0; i < head_end; ++i, ++ns)
+      if (static_ids) static_ids[ns] = uint32_t(i);
+    for (uint64_t i = tail_begin; i < t; ++i, ++ns)
+      if (static_ids) static_ids[ns] = uint32_t(i);
+    for (uint64_t i = head_end; i < tail_begin; ++i, ++np)
+      if (pool_ids) pool_ids[np] = uint32_t(i);
+    *n_static = ns;
+    *n_pool = np;
+  });
+}
+
+static uint32_t read_flag(ra_ctx* ctx, uint32_t* d_flag) {
+  uint32_t f = 0;
+  RA_CUDA(cudaMemcpyAsync(&f, d_flag, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  RA_CUDA(cudaStreamSynchronize(ctx->stream));
+  return f;
+}
+
+ra_status ra_partial_attention(ra_ctx* ctx, ra_kv* kv, uint32_t B, const float* q,
+                               const uint32_t* idx, uint32_t m_stride, const uint32_t* m,
+                               double* out, double* zmax, double* expsum) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (!kv) invalid("null kv");
+    if (kv->values.n != kv->keys.n || !kv->values.p)
+      invalid("keys and values must have equal n");
+    if (B == 0) return;
+    DeviceGuard dg(ctx->device);
+    const size_t refs_bytes = (B * sizeof(KVRef) + 255) & ~size_t(255);
+    uint8_t* a = arena<uint8_t>(ctx->scratch_a, refs_bytes + 256);
+    KVRef* refs = reinterpret_cast<KVRef*>(a);
+    uint32_t* flag = reinterpret_cast<uint32_t*>(a + refs_bytes);
+    std::vector<KVRef> h(B, KVRef{kv->keys.p, kv->values.p, kv->n});
+    RA_CUDA(cudaMemcpyAsync(refs, h.data(), B * sizeof(KVRef), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    RA_CUDA(cudaMemsetAsync(flag, 0, 4, ctx->stream));
+    const size_t zd = partial_scratch_doubles(B, m_stride ? m_stride : 1u << 30);
+    double* z = nullptr;
+    if (m_stride > 8192) z = arena<double>(ctx->scratch_c, zd);
+    launch_partial_attention_ex(ctx->stream, refs, kv->d, B, q, idx, m_stride, m, nullptr, 0,
+                                out, zmax, expsum, z, m_stride, nullptr, flag);
+    if (read_flag(ctx, flag) & 1u) invalid("index out of range");
+  });
+}
+
+ra_status ra_merge(ra_ctx* ctx, uint32_t B, uint32_t d, const double* ow, const double* zw,
+                   const double* sw, const uint8_t* w_empty, const double* oo,
+                   const double* zo, const double* so, const uint8_t* o_empty, double* out,
+                   double* gw, double* go) {
+  return guard([&] {
+    check_ctx(ctx);
+    DeviceGuard dg(ctx->device);
+    uint32_t* flag = arena<uint32_t>(ctx->scratch_a, 1);
+    RA_CUDA(cudaMemsetAsync(flag, 0, 4, ctx->stream));
+    launch_merge(ctx->stream, B, d, ow, zw, sw, w_empty, oo, zo, so, o_empty, out, gw, go, flag);
+    if (read_flag(ctx, flag) & 2u) invalid("empty attention support");  // :138-139
+  });
+}
+
+}  // extern "C"
+
+// ---- decode engine (engine.cpp:23-115) -----------------------------------------------
+struct ra_engine {
+  ra_ctx* ctx = nullptr;
+  uint32_t H = 0, G = 0, d = 0, k = 0;
+  uint64_t t = 0, n_pool = 0, n_static = 0;
+  ra_engine_config cfg{};
+  std::vector<ra_kv*> groups;     // retained
+  std::vector<ra_graph*> graphs;  // borrowed (caller keeps them alive)
+  std::string step_error;         // deferred "ef must be >= k" (raised per step)
+  DevBuf<GraphDesc> desc;
+  DevBuf<KVRef> kvrefs;
+  DevBuf<uint32_t> w_ids, w_bits, w_m, o_m;
+  DevBuf<uint8_t> w_empty, o_empty;
+  DevBuf<float> q;
+  DevBuf<uint32_t> ids, n_out, expanded, flag;
+  DevBuf<float> scores;
+  DevBuf<double> scores64, ow, zw, sw, oo, zo, so, out;
+  DevBuf<uint64_t> scanned;
+  DevBuf<uint8_t> truncated;
+  DevBuf<uint8_t> search_scratch;
+  uint32_t max_n = 0;
+};
+
+extern "C" {
+
+ra_status ra_engine_create(ra_ctx* ctx, ra_kv* const* groups, uint32_t n_groups,
+                           ra_graph* const* head_graphs, uint32_t n_heads,
+                           const ra_engine_config* cfg, ra_engine** out) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (n_heads == 0) invalid("no heads");
+    if (cfg->top_k < 1) invalid("top_k must be >= 1");
+    if (n_groups == 0 || n_heads % n_groups) invalid("n_heads must be divisible by n_kv_groups");
+    const uint64_t t = groups[0]->n;
+    if (t == 0) invalid("empty context");
+    for (uint32_t gi = 0; gi < n_groups; ++gi)
+      if (groups[gi]->n != t || groups[gi]->values.n != groups[gi]->keys.n)
+        invalid("context length mismatch across heads");
+    const uint32_t per = n_heads / n_groups;
+    for (uint32_t h = 0; h < n_heads; ++h)
+      if (!head_graphs[h] || head_graphs[h]->kv != groups[h / per])
+        invalid("head graph is not built over its group's keys");
+    DeviceGuard dg(ctx->device);
+    auto e = std::make_unique<ra_engine>();
+    e->ctx = ctx;
+    e->H = n_heads;
+    e->G = n_groups;
+    e->d = groups[0]->d;
+    e->t = t;
+    e->cfg = *cfg;
+    for (uint32_t gi = 0; gi < n_groups; ++gi) {
+      ra_kv_retain(groups[gi]);
+      e->groups.push_back(groups[gi]);
+    }
+    e->graphs.assign(head_graphs, head_graphs + n_heads);
+    uint64_t ns, np;
+    if (ra_static_partition(t, cfg->s_init, cfg->s_local, nullptr, &ns, nullptr, &np))
+      invalid(ra_last_error());
+    std::vector<uint32_t> w(ns), pool(np);
+    ra_static_partition(t, cfg->s_init, cfg->s_local, w.data(), &ns, pool.data(), &np);
+    e->n_static = ns;
+    e->n_pool = np;
+    e->k = uint32_t(std::min<uint64_t>(cfg->top_k, np));
+    const uint32_t H = n_heads, d = e->d, kk = std::max<uint32_t>(e->k, 1);
+    std::vector<GraphDesc> desc(H);
+    std::vector<KVRef> refs(H);
+    for (uint32_t h = 0; h < H; ++h) {
+      const ra_graph* g = head_graphs[h];
+      const uint64_t ef = cfg->ef >= 0 ? uint64_t(cfg->ef) : g->default_ef;
+      if (np > 0 && ef < e->k) e->step_error = "ef must be >= k";
+      desc[h] = GraphDesc{g->adj.p, g->kv->keys.p, g->entry, uint32_t(g->n), g->max_degree,
+                          uint32_t(std::min<uint64_t>(ef, 0xFFFFFFFFu)), 0};
+      refs[h] = KVRef{g->kv->keys.p, g->kv->values.p, g->kv->n};
+      e->max_n = std::max<uint32_t>(e->max_n, uint32_t(g->n));
+    }
+    auto up = [&](auto& buf, const auto& vec) {
+      buf.alloc(std::max<size_t>(vec.size(), 1));
+      if (!vec.empty())
+        RA_CUDA(cudaMemcpy(buf.p, vec.data(), vec.size() * sizeof(vec[0]),
+                           cudaMemcpyHostToDevice));
+    };
+    up(e->desc, desc);
+    up(e->kvrefs, refs);
+    up(e->w_ids, w);
+    up(e->w_m, std::vector<uint32_t>(H, uint32_t(ns)));
+    up(e->w_empty, std::vector<uint8_t>(H, ns == 0));
+    const uint64_t words = (t + 31) / 32;
+    e->w_bits.alloc(words);
+    launch_mask_bitset(ctx->stream, e->w_ids.p, ns, e->w_bits.p, words);
+    e->q.alloc(size_t(H) * d);
+    e->ids.alloc(size_t(H) * kk);
+    e->scores.alloc(size_t(H) * kk);
+    e->scores64.alloc(size_t(H) * kk);
+    e->n_out.alloc(H);
+    e->scanned.alloc(H);
+    e->truncated.alloc(H);
+    e->expanded.alloc(H);
+    e->o_empty.alloc(H);
+    e->flag.alloc(1);
+    for (auto* b : {&e->ow, &e->oo, &e->out}) b->alloc(size_t(H) * d);
+    for (auto* b : {&e->zw, &e->sw, &e->zo, &e->so}) b->alloc(H);
+    const size_t sb = search_scratch_bytes(ctx, H, e->max_n, d);
+    e->search_scratch.alloc(sb);
+    RA_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = e.release();
+  });
+}
+
+void ra_engine_destroy(ra_engine* e) {
+  if (!e) return;
+  {
+    DeviceGuard dg(e->ctx->device);
+    cudaStreamSynchronize(e->ctx->stream);
+    for (ra_kv* g : e->groups) ra_kv_release(g);
+  }
+  delete e;
+}
+
+namespace {
+// run_head for every head (engine.cpp:69-101): search with Mask{W} ->
+// partial over W -> partial over Omega (scores reused) -> merge.
+void engine_enqueue(ra_engine* e, const float* q_dev) {
+  ra_ctx* ctx = e->ctx;
+  cudaStream_t s = ctx->stream;
+  const uint32_t H = e->H, d = e->d;
+  if (e->n_pool > 0) {
+    SearchArgs sa{};
+    sa.desc = e->desc.p;
+    sa.q = q_dev;
+    sa.mask_bits = e->n_static ? e->w_bits.p : nullptr;
+    sa.B = H;
+    sa.d = d;
+    sa.k = e->k;
+    sa.ids = e->ids.p;
+    sa.scores = e->scores.p;
+    sa.scores64 = e->scores64.p;
+    sa.n_out = e->n_out.p;
+    sa.scanned = e->scanned.p;
+    sa.truncated = e->truncated.p;
+    sa.expanded = e->expanded.p;
+    launch_graph_search(ctx, sa, e->max_n, e->search_scratch.p);
+  } else {
+    RA_CUDA(cudaMemsetAsync(e->n_out.p, 0, H * 4, s));
+    RA_CUDA(cudaMemsetAsync(e->scanned.p, 0, H * 8, s));
+    RA_CUDA(cudaMemsetAsync(e->expanded.p, 0, H * 4, s));
+  }
+  launch_partial_attention_ex(s, e->kvrefs.p, d, H, q_dev, e->w_ids.p, 0, e->w_m.p, nullptr, 0,
+                              e->ow.p, e->zw.p, e->sw.p, nullptr, 0, e->w_empty.p, e->flag.p);
+  launch_partial_attention_ex(s, e->kvrefs.p, d, H, q_dev, e->ids.p, e->k, e->n_out.p,
+                              e->scores64.p, e->k, e->oo.p, e->zo.p, e->so.p, nullptr, 0,
+                              e->o_empty.p, e->flag.p);
+  launch_merge(s, H, d, e->ow.p, e->zw.p, e->sw.p, e->w_empty.p, e->oo.p, e->zo.p, e->so.p,
+               e->o_empty.p, e->out.p, nullptr, nullptr, e->flag.p);
+}
+}  // namespace
+
+ra_status ra_engine_step_device(ra_engine* e, const float* q, double* out, uint32_t* omega,
+                                uint64_t* scanned) {
+  return guard([&] {
+    if (!e) invalid("null engine");
+    if (!e->step_error.empty()) invalid(e->step_error);
+    DeviceGuard dg(e->ctx->device);
+    cudaStream_t s = e->ctx->stream;
+    engine_enqueue(e, q);
+    if (out)
+      RA_CUDA(cudaMemcpyAsync(out, e->out.p, size_t(e->H) * e->d * 8, cudaMemcpyDeviceToDevice, s));
+    if (omega && e->k)
+      RA_CUDA(cudaMemcpyAsync(omega, e->ids.p, size_t(e->H) * e->k * 4, cudaMemcpyDeviceToDevice, s));
+    if (scanned)
+      RA_CUDA(cudaMemcpyAsync(scanned, e->scanned.p, size_t(e->H) * 8, cudaMemcpyDeviceToDevice, s));
+  });
+}
+
+ra_status ra_engine_step_host(ra_engine* e, const float* q, double* out, uint32_t* omega,
+                              uint64_t* scanned) {
+  return guard([&] {
+    if (!e) invalid("null engine");
+    if (!e->step_error.empty()) invalid(e->step_error);
+    DeviceGuard dg(e->ctx->device);
+    cudaStream_t s = e->ctx->stream;
+    RA_CUDA(cudaMemcpyAsync(e->q.p, q, size_t(e->H) * e->d * 4, cudaMemcpyHostToDevice, s));
+    engine_enqueue(e, e->q.p);
+    if (out) RA_CUDA(cudaMemcpyAsync(out, e->out.p, size_t(e->H) * e->d * 8, cudaMemcpyDeviceToHost, s));
+    if (omega && e->k)
+      RA_CUDA(cudaMemcpyAsync(omega, e->ids.p, size_t(e->H) * e->k * 4, cudaMemcpyDeviceToHost, s));
+    if (scanned)
+      RA_CUDA(cudaMemcpyAsync(scanned, e->scanned.p, size_t(e->H) * 8, cudaMemcpyDeviceToHost, s));
+    RA_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+ra_status ra_engine_last_stats(ra_engine* e, uint64_t* total_scanned, uint64_t* total_expanded) {
+  return guard([&] {
+    if (!e) invalid("null engine");
+    DeviceGuard dg(e->ctx->device);
+    std::vector<uint64_t> sc(e->H);
+    std::vector<uint32_t> ex(e->H);
+    RA_CUDA(cudaMemcpyAsync(sc.data(), e->scanned.p, e->H * 8, cudaMemcpyDeviceToHost, e->ctx->stream));
+    RA_CUDA(cudaMemcpyAsync(ex.data(), e->expanded.p, e->H * 4, cudaMemcpyDeviceToHost, e->ctx->stream));
+    RA_CUDA(cudaStreamSynchronize(e->ctx->stream));
+    if (total_scanned) *total_scanned = std::accumulate(sc.begin(), sc.end(), uint64_t(0));
+    if (total_expanded) *total_expanded = std::accumulate(ex.begin(), ex.end(), uint64_t(0));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,203 @@
+// Shared internals of libra_b200.so (sm_100a). Not part of the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ra_capi.h"
+
+namespace ra {
+
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+constexpr uint32_t kSentinel = 0xFFFFFFFFu;  // padded adjacency slot / "no id"
+
+// ---- error plumbing: exceptions inside, ra_status at the ABI --------------
+struct Error : std::runtime_error {
+  ra_status code;
+  Error(ra_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void invalid(const std::string& m) {
+  throw Error(RA_ERR_INVALID_ARGUMENT, m);
+}
+[[noreturn]] inline void runtime(const std::string& m) { throw Error(RA_ERR_RUNTIME, m); }
+
+void set_last_error(const std::string& m);
+
+template <typename F>
+ra_status guard(F&& f) {
+  try {
+    f();
+    return RA_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("out of host memory");
+    return RA_ERR_RUNTIME;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return RA_ERR_RUNTIME;
+  }
+}
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess)
+    throw Error(RA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e) + " (" + file +
+                                 ":" + std::to_string(line) + ")");
+}
+#define RA_CUDA(x) ::ra::cuda_check((x), #x, __FILE__, __LINE__)
+#define RA_LAUNCH_CHECK() ::ra::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// ---- device buffers ------------------------------------------------------------
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    return *this;
+  }
+  ~DevBuf() { reset(); }
+  void alloc(size_t count) {
+    reset();
+    if (count) RA_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  // grow-only reallocation (contents not preserved)
+  void ensure(size_t count) {
+    if (count > n) alloc(count);
+  }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// Device-side view of one query head's graph (what the search kernel reads).
+struct GraphDesc {
+  const uint32_t* adj;  // [n][M], kSentinel-padded rows
+  const float* keys;    // [n][d]
+  uint64_t entry;
+  uint32_t n, M;
+  uint32_t ef;          // resolved ef for this query
+  uint32_t pad;
+};
+
+}  // namespace ra
+
+// ---- handles -----------------------------------------------------------------
+struct ra_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  size_t smem_optin = 0;
+  // grow-only scratch arenas reused across calls (one call at a time per ctx)
+  ra::DevBuf<uint8_t> scratch_a;
+  ra::DevBuf<uint8_t> scratch_b;
+  ra::DevBuf<uint8_t> scratch_c;
+};
+
+struct ra_kv {
+  std::atomic<int> refs{1};
+  int device = 0;
+  uint64_t n = 0;
+  uint32_t d = 0;
+  ra::DevBuf<float> keys;    // n x d row-major (f32, the reference's VectorSet layout)
+  ra::DevBuf<float> values;  // n x d row-major (may be empty)
+};
+
+struct ra_graph {
+  ra_kv* kv = nullptr;  // retained
+  uint64_t n = 0;
+  uint32_t max_degree = 0;
+  uint32_t default_ef = 128;
+  uint64_t entry = 0;
+  // device: fixed-stride adjacency, row u = adj[u*max_degree ...], padded
+  // with kSentinel past degree(u): one coalesced load per expansion, no
+  // offsets hop.
+  ra::DevBuf<uint32_t> adj;
+  // host mirror (reference CSR) for accessors and OODG serialization
+  std::vector<uint64_t> offsets;
+  std::vector<uint32_t> adjacency;
+};
+
+namespace ra {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) RA_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (cudaGetDevice(&cur) == cudaSuccess && prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// grow-only typed carve-outs from a ctx arena
+template <typename T>
+T* arena(DevBuf<uint8_t>& a, size_t count) {
+  a.ensure(count * sizeof(T) + 256);
+  return reinterpret_cast<T*>(a.p);
+}
+
+// ---- search (search.cu) --------------------------------------------------------
+struct SearchArgs {
+  const GraphDesc* desc;      // [B] device
+  const float* q;             // [B][d]
+  const uint32_t* mask_bits;  // bitset over ids, nullptr = no mask (shared by batch)
+  uint32_t B, d, k;
+  uint32_t* ids;              // [B][k]
+  float* scores;              // [B][k]
+  double* scores64;           // optional [B][k] exact f64 scores
+  uint32_t* n_out;            // [B]
+  uint64_t* scanned;          // [B]
+  uint8_t* truncated;         // [B]
+  uint32_t* expanded;         // optional [B]
+  // HBM spill area used when a query outgrows its shared-memory list
+  // (per query: max_n entries of f64 + u32 + u8) and the visited bitset
+  // when it does not fit shared memory (per query: ceil(max_n/32) words).
+  uint8_t* spill;
+  uint32_t* vis_global;
+};
+
+// Returns bytes of scratch needed for (B, max_n, d); then launches.
+size_t search_scratch_bytes(const ra_ctx* ctx, uint32_t B, uint32_t max_n, uint32_t d);
+void launch_graph_search(ra_ctx* ctx, SearchArgs a, uint32_t max_n, uint8_t* scratch);
+
+void launch_mask_bitset(cudaStream_t s, const uint32_t* mask, uint64_t mask_n, uint32_t* bits,
+                        uint64_t words);
+
+// ---- attention (attention.cu) --------------------------------------------------
+size_t partial_scratch_doubles(uint32_t B, uint32_t max_m);
+struct KVRef {
+  const float* keys;
+  const float* values;
+  uint64_t n;
+};
+void launch_partial_attention_ex(cudaStream_t s, const KVRef* kvs, uint32_t d, uint32_t B, const float* q,
+                                 const uint32_t* idx, uint32_t m_stride, const uint32_t* m,
+                                 const double* scores64, uint32_t s_stride, double* out,
+                                 double* zmax, double* expsum, double* zscratch,
+                                 uint64_t z_stride, uint8_t* empty_out, uint32_t* err_flag);
+void launch_merge(cudaStream_t s, uint32_t B, uint32_t d, const double* ow, const double* zw,
+                  const double* sw, const uint8_t* w_empty, const double* oo,
+                  const double* zo, const double* so, const uint8_t* o_empty, double* out,
+                  double* gw, double* go, uint32_t* err_flag);
+
+}  // namespace ra
