@@ -1,0 +1,394 @@
+#!/usr/bin/env python3
+"""Decode-attention benchmark: RetrievalAttention hot path at Llama-3-8B shape.
+
+Workload (BASELINE.json configs[1]): one layer, 32 query heads over 8 KV
+groups, d_head 128, 128K context, static set = first 128 + last 512 tokens,
+top-100 retrieval per head through the head's OODGraph (k_train 128, M 24,
+efc 256, window 8; README/acceptance parameters), ef 128. Inputs are the
+reference generator's synthetic OOD K/Q/V (seed 7), synthesized on the GPU
+(paper_2409_10516_b200.workload); graphs are built on the GPU (untimed).
+
+One step = ra_engine decode step for all local heads: graph search ->
+partial attention over W -> partial over Omega -> LSE merge (+ NCCL
+all_gather of per-head outputs when N > 1, heads sharded by KV group).
+Metric: ms per decode step (token) for the layer, lower is better.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode attention ms/token @128K (Llama-3-8B shape); search recall@100; HBM GB/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n-ctx", type=int, default=131072)
+    ap.add_argument("--heads", type=int, default=32)
+    ap.add_argument("--groups", type=int, default=8)
+    ap.add_argument("--ef", type=int, default=128)
+    ap.add_argument("--top-k", type=int, default=100)
+    ap.add_argument("--k-train", type=int, default=128)
+    ap.add_argument("--max-degree", type=int, default=24)
+    ap.add_argument("--ef-construction", type=int, default=256)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--flush-mb", type=int, default=512)
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.stop = device, [], threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the search kernel from the committed ncu
+    --set full capture (profiles/ncu_search_summary.json), if present."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_search_summary.json")) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference" and rank != 0:
+        return  # the reference CPU arm runs on rank 0 only
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1 and a.impl == "ours":
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2409_10516_b200 as ra
+    from paper_2409_10516_b200.workload import WorkloadSpec, generate_group
+
+    H, G = a.heads, a.groups
+    hpg = H // G
+    n_world = world if a.impl == "ours" else 1
+    my_groups = list(range(rank * G // n_world, (rank + 1) * G // n_world))
+    n_dec = a.warmup + 2 * a.steps + 2
+    spec = WorkloadSpec(n_ctx=a.n_ctx, d_model=256, d_head=128, n_heads=H, n_kv_groups=G,
+                        seed=7, n_decode=n_dec)
+    dev = torch.device("cuda", local)
+    t0 = time.time()
+    kvs, graphs, dq, keys_host, vals_host = [], [], [], [], []
+    bp = ra.OODGraphBuildParams(a.k_train, a.max_degree, a.ef_construction, 8)
+    build_ms = []
+    for g in my_groups:
+        w = generate_group(spec, g, dev)
+        kv = ra.KVGroup(w["keys"], w["values"])
+        kvs.append(kv)
+        for m in range(hpg):
+            torch.cuda.synchronize()
+            tb = time.time()
+            graphs.append(ra.ood_build(kv, w["prefill_q"][m], bp))
+            build_ms.append((time.time() - tb) * 1e3)
+            dq.append(w["decode_q"][m])
+        if a.impl == "reference" or rank == 0:
+            keys_host.append(w["keys"].cpu().numpy())
+            vals_host.append(w["values"].cpu().numpy())
+        del w
+    setup_s = time.time() - t0
+    Hl = len(graphs)
+    Q = torch.stack(dq)  # [Hl, n_dec, d]
+    del dq
+    cfg = ra.EngineConfig(128, 512, a.top_k, a.ef)
+
+    if a.impl == "reference":
+        run_reference(a, keys_host, vals_host, graphs, Q, cfg, H, G, setup_s)
+        return
+
+    eng = ra.Engine(kvs, graphs, cfg)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(a.flush_mb * (1 << 20) // 4, dtype=torch.float32, device=dev)
+    gather_out = None
+    if dist is not None:
+        gather_out = [torch.empty((Hl, 128), dtype=torch.float64, device=dev)
+                      for _ in range(world)]
+
+    def step(i):
+        out, om, sc = eng.decode_step_device(Q[:, i])
+        if dist is not None:
+            dist.all_gather(gather_out, out)
+        return out
+
+    for i in range(a.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    times, search_ms, attn_ms, scanned, expanded = [], [], [], [], []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        for i in range(a.warmup, a.warmup + a.steps):
+            flush.zero_()  # evict L2 between timed steps (outside the events)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step(i)
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+            s_ms, a_ms = eng.last_timing()
+            search_ms.append(s_ms)
+            attn_ms.append(a_ms)
+            s, e = eng.last_stats()
+            scanned.append(s)
+            expanded.append(e)
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+
+    # ---- end-to-end through the host API (H2D q, D2H out/omega/scanned) ----
+    qh = torch.empty((Hl, 128), dtype=torch.float32, pin_memory=True)
+    out_h = torch.empty((Hl, 128), dtype=torch.float64, pin_memory=True)
+    om_h = torch.empty((Hl, max(eng.k, 1)), dtype=torch.int32, pin_memory=True)
+    sc_h = torch.empty(Hl, dtype=torch.int64, pin_memory=True)
+    Qh = Q.cpu()
+    e2e = []
+    for i in range(a.warmup + a.steps, a.warmup + 2 * a.steps):
+        qh.copy_(Qh[:, i])
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.ctx.bind_stream()
+        ra.api._check(ra.lib.ra_engine_step_host(eng.h, qh.data_ptr(), out_h.data_ptr(),
+                                                 om_h.data_ptr(), sc_h.data_ptr()))
+        e1.record(stream)
+        e1.synchronize()
+        e2e.append(e0.elapsed_time(e1))
+
+    ms = statistics.mean(times)
+    ms_search = statistics.mean(search_ms)
+    ms_e2e = statistics.mean(e2e)
+    if dist is not None:
+        t = torch.tensor([ms, ms_e2e, ms_search], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, ms_e2e, ms_search = (float(x) for x in t)
+    d, M = 128, a.max_degree
+    bytes_search = statistics.mean([s * d * 4 + e * M * 4 + 0.0 for s, e in zip(scanned, expanded)])
+    peak, peak_kind = measured_peaks()
+    achieved = bytes_search / (statistics.mean(search_ms) * 1e-3) / 1e9
+    res = {
+        "metric": METRIC, "value": round(ms, 4), "unit": "ms/token", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference OOD generator algorithm, seed 7, GPU-synthesized)",
+        "config": {"workload": "configs[1]: Llama-3-8B shape single layer, 32 Q heads / 8 KV "
+                               "groups, d=128, 128K ctx, top-100 + 640 static, ef 128",
+                   "n_ctx": a.n_ctx, "heads": H, "kv_groups": G, "top_k": a.top_k, "ef": a.ef,
+                   "graph": {"k_train": a.k_train, "max_degree": M,
+                             "ef_construction": a.ef_construction, "edge_window": 8},
+                   "l2": f"flushed between timed steps ({a.flush_mb} MiB write)",
+                   "parallelism": f"heads sharded by KV group over {world} GPU(s)"},
+        "e2e": {"value": round(ms_e2e, 4), "unit": "ms/token",
+                "h2d_bytes_per_step": Hl * 128 * 4,
+                "d2h_bytes_per_step": Hl * 128 * 8 + Hl * max(eng.k, 1) * 4 + Hl * 8},
+        "gpu_launches": 4 * a.steps,
+        "roofline": {"bound": "hbm", "kernel": "k_graph_search",
+                     "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 5), "peak_source": peak_kind,
+                     "traffic": ncu_traffic(),
+                     "algorithmic_bytes_per_launch": int(bytes_search),
+                     "search_ms": round(ms_search, 4),
+                     "attention_ms": round(statistics.mean(attn_ms), 4)},
+        "search": {"mean_scanned_per_head": statistics.mean(scanned) / Hl,
+                   "mean_expanded_per_head": statistics.mean(expanded) / Hl,
+                   "scan_fraction": statistics.mean(scanned) / Hl / (a.n_ctx - 640)},
+        "clocks": clk.summary(),
+        "setup_s": round(setup_s, 1),
+        "build_ms_per_head": round(statistics.mean(build_ms), 1),
+    }
+    if rank == 0:
+        res["recall"] = recall(eng, graphs, kvs, Q, a, ra)
+        if world == 1 and not a.no_cpu_baseline:
+            res["cpu_baseline"], res["parity"] = cpu_baseline(a, keys_host, vals_host, graphs,
+                                                              Q, cfg, eng)
+        print(json.dumps(res))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def recall(eng, graphs, kvs, Q, a, ra):
+    """recall@100 on a sample: engine-level (masked, vs exact pool top-100,
+    acceptance.cpp:207-212) and unmasked vs FlatIndex (diagnostics.cpp:150-164)."""
+    import torch
+    hpg = a.heads // a.groups
+    W = ra.static_partition(a.n_ctx, 128, 512).static_set
+    mask = torch.zeros(a.n_ctx, dtype=torch.bool, device=Q.device)
+    mask[torch.from_numpy(W.astype(np.int64)).to(Q.device)] = True
+    rec_m, rec_u = [], []
+    for i in range(min(4, a.steps)):
+        q = Q[:, a.warmup + i]
+        out, om, sc = eng.decode_step_device(q)
+        omega = om.cpu().numpy().view(np.uint32)
+        un = ra.search_batch(graphs, q, 100, None, a.ef).host()
+        for h in range(len(graphs)):
+            K = kvs[h // hpg].keys_tensor().double()
+            s = K @ q[h].double()
+            top_u = torch.topk(s, 100).indices.cpu().numpy()
+            s[mask] = -float("inf")
+            top_m = torch.topk(s, 100).indices.cpu().numpy()
+            rec_m.append(len(set(top_m.tolist()) & set(omega[h].tolist())) / 100)
+            rec_u.append(len(set(top_u.tolist()) & set(un[h].ids.tolist())) / 100)
+    return {"masked_engine": round(float(np.mean(rec_m)), 4),
+            "unmasked_flat": round(float(np.mean(rec_u)), 4), "samples": len(rec_m),
+            "ef": a.ef}
+
+
+def _ref_engine(keys_host, vals_host, graphs, cfg, threads):
+    from oracle.ffi import Oracle, available
+    if not available("ref"):
+        return None, None
+    o = Oracle("ref")
+    blobs = [g.serialize() for g in graphs]
+    eng = o.engine(np.stack(keys_host), np.stack(vals_host), blobs, cfg.s_init, cfg.s_local,
+                   cfg.top_k, cfg.search_param, threads)
+    return o, eng
+
+
+def cpu_baseline(a, keys_host, vals_host, graphs, Q, cfg, eng):
+    """The reference's own decode_step (oracle/_ref, unmodified sources) on the
+    host cores over the same graphs (loaded through OODGraph(keys, blob)),
+    bounded to ~cpu_seconds; doubles as a full-size parity check."""
+    threads = os.cpu_count() or 1
+    o, reng = _ref_engine(keys_host, vals_host, graphs, cfg, threads)
+    if reng is None:
+        return {"value": None, "unavailable": "oracle/_ref not built"}, None
+    Qh = Q.cpu().numpy()
+    times, same_om, same_sc, max_rel, n = [], 0, 0, 0.0, 0
+    t_end = time.time() + a.cpu_seconds
+    i = a.warmup
+    while (time.time() < t_end or not times) and i < Q.shape[1]:
+        q = np.ascontiguousarray(Qh[:, i])
+        t0 = time.perf_counter()
+        rout, rom, rsc = reng.step(q, i)
+        times.append((time.perf_counter() - t0) * 1e3)
+        if not a.no_parity:
+            out, om, sc = eng.decode_step(q)
+            same_om += int((om == rom[:, : om.shape[1]]).all(axis=1).sum())
+            same_sc += int((sc == rsc).sum())
+            rel = np.linalg.norm(out - rout, axis=1) / np.linalg.norm(rout, axis=1)
+            max_rel = max(max_rel, float(rel.max()))
+            n += q.shape[0]
+        i += 1
+    base = {"value": round(statistics.mean(times), 3), "unit": "ms/token", "cores": threads,
+            "kind": "reference",
+            "sample": f"{len(times)} decode steps x {Qh.shape[0]} heads at n_ctx {a.n_ctx} "
+                      f"(reference decode_step, n_threads={threads}, GPU-built graphs via OODG)"}
+    parity = None if a.no_parity else {
+        "heads_checked": n, "omega_identical": same_om, "scanned_identical": same_sc,
+        "max_out_rel_err": max_rel}
+    return base, parity
+
+
+def run_reference(a, keys_host, vals_host, graphs, Q, cfg, H, G, setup_s):
+    threads = os.cpu_count() or 1
+    o, reng = _ref_engine(keys_host, vals_host, graphs, cfg, threads)
+    if reng is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    Qh = Q.cpu().numpy()
+    for i in range(a.warmup):
+        reng.step(np.ascontiguousarray(Qh[:, i]), i)
+    times = []
+    t_start = time.perf_counter()
+    for i in range(a.warmup, a.warmup + a.steps):
+        t0 = time.perf_counter()
+        reng.step(np.ascontiguousarray(Qh[:, i]), i)
+        times.append((time.perf_counter() - t0) * 1e3)
+    ms = statistics.mean(times)
+    sample = (f"{a.steps} reference decode_steps x {H} heads at n_ctx {a.n_ctx} "
+              f"(n_threads={threads}; graphs built on GPU, loaded via OODG blobs)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(ms, 3), "unit": "ms/token",
+        "n_gpus": 1, "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference OOD generator algorithm, seed 7)",
+        "config": {"workload": "configs[1]", "n_ctx": a.n_ctx, "heads": H, "kv_groups": G,
+                   "top_k": a.top_k, "ef": a.ef},
+        "cpu_baseline": {"value": round(ms, 3), "unit": "ms/token", "cores": threads,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": round(ms, 3), "unit": "ms/token", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": round(time.perf_counter() - t_start, 2), "setup_s": round(setup_s, 1)}))
+
+
+if __name__ == "__main__":
+    main()

@@ -188,6 +188,9 @@ ra_status ra_engine_step_host(ra_engine* e, const float* q, double* out, uint32_
 /* device-side counters of the last step (for roofline accounting) */
 ra_status ra_engine_last_stats(ra_engine* e, uint64_t* total_scanned,
                                uint64_t* total_expanded);
+/* CUDA-event durations of the last step's search kernel and of its
+ * attention + merge kernels (recorded on the ctx stream). Synchronizes. */
+ra_status ra_engine_last_timing(ra_engine* e, float* search_ms, float* attention_ms);
 
 #ifdef __cplusplus
 }

@@ -514,6 +514,12 @@ class Engine:
                                        sc.ctypes.data))
         return out, om[:, : self.k], sc
 
+    def last_timing(self):
+        """(search_ms, attention_ms) of the last step, CUDA events on the ctx stream."""
+        a, b = C.c_float(), C.c_float()
+        _check(lib.ra_engine_last_timing(self.h, C.byref(a), C.byref(b)))
+        return float(a.value), float(b.value)
+
     def last_stats(self):
         s, e = C.c_uint64(), C.c_uint64()
         _check(lib.ra_engine_last_stats(self.h, C.byref(s), C.byref(e)))

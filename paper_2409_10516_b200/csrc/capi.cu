@@ -402,6 +402,9 @@ struct ra_engine {
   DevBuf<uint8_t> truncated;
   DevBuf<uint8_t> search_scratch;
   uint32_t max_n = 0;
+  // events bracketing the search kernel and the attention kernels of the
+  // last step, recorded on the ctx stream (ra_engine_last_timing)
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
 };
 
 extern "C" {
@@ -484,6 +487,7 @@ ra_status ra_engine_create(ra_ctx* ctx, ra_kv* const* groups, uint32_t n_groups,
     for (auto* b : {&e->zw, &e->sw, &e->zo, &e->so}) b->alloc(H);
     const size_t sb = search_scratch_bytes(ctx, H, e->max_n, d);
     e->search_scratch.alloc(sb);
+    for (auto& ev : e->ev) RA_CUDA(cudaEventCreate(&ev));
     RA_CUDA(cudaStreamSynchronize(ctx->stream));
     *out = e.release();
   });
@@ -495,6 +499,8 @@ void ra_engine_destroy(ra_engine* e) {
     DeviceGuard dg(e->ctx->device);
     cudaStreamSynchronize(e->ctx->stream);
     for (ra_kv* g : e->groups) ra_kv_release(g);
+    for (auto& ev : e->ev)
+      if (ev) cudaEventDestroy(ev);
   }
   delete e;
 }
@@ -506,6 +512,7 @@ void engine_enqueue(ra_engine* e, const float* q_dev) {
   ra_ctx* ctx = e->ctx;
   cudaStream_t s = ctx->stream;
   const uint32_t H = e->H, d = e->d;
+  RA_CUDA(cudaEventRecord(e->ev[0], s));
   if (e->n_pool > 0) {
     SearchArgs sa{};
     sa.desc = e->desc.p;
@@ -527,6 +534,7 @@ void engine_enqueue(ra_engine* e, const float* q_dev) {
     RA_CUDA(cudaMemsetAsync(e->scanned.p, 0, H * 8, s));
     RA_CUDA(cudaMemsetAsync(e->expanded.p, 0, H * 4, s));
   }
+  RA_CUDA(cudaEventRecord(e->ev[1], s));
   launch_partial_attention_ex(s, e->kvrefs.p, d, H, q_dev, e->w_ids.p, 0, e->w_m.p, nullptr, 0,
                               e->ow.p, e->zw.p, e->sw.p, nullptr, 0, e->w_empty.p, e->flag.p);
   launch_partial_attention_ex(s, e->kvrefs.p, d, H, q_dev, e->ids.p, e->k, e->n_out.p,
@@ -534,6 +542,7 @@ void engine_enqueue(ra_engine* e, const float* q_dev) {
                               e->o_empty.p, e->flag.p);
   launch_merge(s, H, d, e->ow.p, e->zw.p, e->sw.p, e->w_empty.p, e->oo.p, e->zo.p, e->so.p,
                e->o_empty.p, e->out.p, nullptr, nullptr, e->flag.p);
+  RA_CUDA(cudaEventRecord(e->ev[2], s));
 }
 }  // namespace
 
@@ -583,6 +592,16 @@ ra_status ra_engine_last_stats(ra_engine* e, uint64_t* total_scanned, uint64_t* 
     RA_CUDA(cudaStreamSynchronize(e->ctx->stream));
     if (total_scanned) *total_scanned = std::accumulate(sc.begin(), sc.end(), uint64_t(0));
     if (total_expanded) *total_expanded = std::accumulate(ex.begin(), ex.end(), uint64_t(0));
+  });
+}
+
+ra_status ra_engine_last_timing(ra_engine* e, float* search_ms, float* attention_ms) {
+  return guard([&] {
+    if (!e) invalid("null engine");
+    DeviceGuard dg(e->ctx->device);
+    RA_CUDA(cudaEventSynchronize(e->ev[2]));
+    if (search_ms) RA_CUDA(cudaEventElapsedTime(search_ms, e->ev[0], e->ev[1]));
+    if (attention_ms) RA_CUDA(cudaEventElapsedTime(attention_ms, e->ev[1], e->ev[2]));
   });
 }
 

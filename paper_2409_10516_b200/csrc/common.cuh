@@ -149,6 +149,9 @@ struct DeviceGuard {
   }
 };
 
+// Host CSR mirror -> fixed-stride device adjacency (capi.cu).
+void graph_upload(ra_ctx* ctx, ra_graph* g);
+
 // grow-only typed carve-outs from a ctx arena
 template <typename T>
 T* arena(DevBuf<uint8_t>& a, size_t count) {

@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(256) k_graph_search(SearchArgs a, uint32_t wpb
       // capacity: migrate L to its HBM spill slot (sized for every key)
       if (len + nnew > lcap) {
         if (spilled || a.spill == nullptr) __trap();  // unreachable: spill_cap >= n
-        uint8_t* sb = a.spill + size_t(b) * spill_cap * 13;
+        uint8_t* sb = a.spill + size_t(b) * ((size_t(spill_cap) * 13 + 15) & ~size_t(15));
         ListRef G{reinterpret_cast<double*>(sb), nullptr, nullptr};
         G.id = reinterpret_cast<uint32_t*>(G.s + spill_cap);
         G.fl = reinterpret_cast<uint8_t*>(G.id + spill_cap);
@@ -384,7 +384,7 @@ void launch_d(ra_ctx* ctx, const SearchArgs& a, const Plan& p, uint32_t spill_ca
 size_t search_scratch_bytes(const ra_ctx* ctx, uint32_t B, uint32_t max_n, uint32_t d) {
   const Plan p = plan(ctx, B, max_n, d);
   size_t bytes = 0;
-  if (p.cap < max_n) bytes += size_t(B) * max_n * 13 + 256;
+  if (p.cap < max_n) bytes += size_t(B) * ((size_t(max_n) * 13 + 15) & ~size_t(15)) + 256;
   if (!p.vis_smem) bytes += size_t(B) * p.vis_words * 4 + 256;
   return bytes;
 }
@@ -397,7 +397,7 @@ void launch_graph_search(ra_ctx* ctx, SearchArgs a, uint32_t max_n, uint8_t* scr
   a.vis_global = nullptr;
   if (p.cap < max_n) {
     a.spill = cur;
-    cur += (size_t(a.B) * max_n * 13 + 255) & ~size_t(255);
+    cur += (size_t(a.B) * ((size_t(max_n) * 13 + 15) & ~size_t(15)) + 255) & ~size_t(255);
   }
   if (!p.vis_smem) a.vis_global = reinterpret_cast<uint32_t*>(cur);
   switch (a.d) {

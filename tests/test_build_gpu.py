@@ -1,0 +1,144 @@
+"""GPU graph build (K1-K5) vs the reference build.
+
+Bar: the OODG v1 blob (adjacency order, degrees, entry point) is
+byte-identical to the oracle's, which is itself pinned byte-for-byte to the
+unmodified reference (tests/test_oracle.py, tests/golden/graph_*.oodg).
+Cases mirror test_index_oodgraph.cpp plus the acceptance parameter sets."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_golden
+from oracle.ffi import BuildParams
+
+pytestmark = pytest.mark.gpu
+
+
+def _ra():
+    import paper_2409_10516_b200 as ra
+    return ra
+
+
+def to_ra(bp: BuildParams):
+    ra = _ra()
+    return ra.OODGraphBuildParams(bp.k_train, bp.max_degree, bp.ef_construction, bp.edge_window,
+                                  "maxnorm" if bp.entry_maxnorm else "medoid",
+                                  "inner_product" if bp.prune_inner_product else "euclidean",
+                                  bp.default_ef)
+
+
+def check_structure(g):
+    # test_index_oodgraph.cpp:55-67
+    n = g.size()
+    assert g.reachable_count() == n
+    assert g.entry_point() < n
+    for u in range(n):
+        nb = g.neighbors(u)
+        assert len(nb) <= g.max_degree_bound()
+        assert len(set(nb.tolist())) == len(nb)
+        assert u not in set(nb.tolist())
+
+
+@pytest.mark.parametrize("name,h", [("d32", 0), ("d32", 1), ("d128", 0)])
+def test_build_matches_golden_blob(name, h):
+    ra = _ra()
+    w = load_golden(f"workload_{name}.npz")
+    H, G = int(w["spec"][3]), int(w["spec"][4])
+    params = {"d32": BuildParams(k_train=32, max_degree=16, ef_construction=64),
+              "d128": BuildParams(k_train=128, max_degree=24, ef_construction=256,
+                                  edge_window=8)}[name]
+    kv = ra.KVGroup(w["keys"][h // (H // G)])
+    g = ra.ood_build(kv, w["prefill_q"][h], to_ra(params))
+    with open(os.path.join(GOLDEN, f"graph_{name}_h{h}.oodg"), "rb") as f:
+        assert g.serialize() == f.read()
+
+
+CASES = [
+    # (n, d, nq, params)  — test_index_oodgraph.cpp:163-229 and edge cases
+    (257, 8, 64, BuildParams(k_train=8, max_degree=4, ef_construction=8)),
+    (1000, 16, 200, BuildParams(k_train=16, max_degree=8, ef_construction=16)),
+    (2048, 32, 512, BuildParams(k_train=32, max_degree=16, ef_construction=32)),
+    (500, 16, 100, BuildParams(k_train=16, max_degree=8, prune_inner_product=True)),
+    (600, 16, 150, BuildParams(k_train=16, max_degree=8)),
+    (300, 12, 40, BuildParams(k_train=20, max_degree=1)),
+    (100, 4, 0, BuildParams(max_degree=3)),
+    (64, 8, 4, BuildParams(k_train=8, edge_window=0, max_degree=32)),
+    (1, 4, 1, BuildParams()),
+    (700, 20, 90, BuildParams(k_train=40, max_degree=12, ef_construction=30, entry_maxnorm=True)),
+    (3000, 128, 700, BuildParams(k_train=128, max_degree=24, ef_construction=256)),
+    (2500, 64, 2500, BuildParams(k_train=64, max_degree=40, ef_construction=80, edge_window=3)),
+]
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_build_matches_oracle(port, case):
+    ra = _ra()
+    n, d, nq, bp = CASES[case]
+    rng = np.random.default_rng(100 + case)
+    keys = rng.standard_normal((n, d)).astype(np.float32)
+    tq = rng.standard_normal((nq, d)).astype(np.float32)
+    g = ra.ood_build(ra.KVGroup(keys), tq, to_ra(bp))
+    assert g.serialize() == port.graph_build(keys, tq, bp)
+    check_structure(g)
+
+
+def test_build_on_ood_workload_hubs(port):
+    """Reference generator (anisotropic, hub-heavy) at 4096 keys: exercises
+    hub nodes with more candidates than shared memory holds."""
+    ra = _ra()
+    w = port.generate_workload(4096, 128, 64, 1, 1, seed=17, n_decode=1)
+    bp = BuildParams(k_train=128, max_degree=24, ef_construction=256, edge_window=8)
+    g = ra.ood_build(ra.KVGroup(w["keys"][0]), w["prefill_q"][0], to_ra(bp))
+    assert g.serialize() == port.graph_build(w["keys"][0], w["prefill_q"][0], bp)
+    assert g.build_stats.candidate_edges > 0
+
+
+def test_hand_built_line_graph():
+    # test_index_oodgraph.cpp:71-111, 207-216
+    ra = _ra()
+    keys = ra.KVGroup(np.array([[10, 0], [9, 0], [8, 0], [0, 5]], np.float32))
+    q = np.array([[1, 0]], np.float32)
+    g = ra.ood_build(keys, q, ra.OODGraphBuildParams(k_train=3))
+    assert g.degree(0) == 0 and list(g.neighbors(1)) == [0]
+    assert list(g.neighbors(2)) == [1, 0, 3] and g.entry_point() == 2
+    g1 = ra.ood_build(keys, q, ra.OODGraphBuildParams(k_train=3, max_degree=1))
+    assert list(g1.neighbors(1)) == [0] and list(g1.neighbors(2)) == [1]
+    assert list(g1.neighbors(0)) == [3] and g1.entry_point() == 2
+    gm = ra.ood_build(keys, q, ra.OODGraphBuildParams(k_train=3, entry_strategy="maxnorm"))
+    assert gm.entry_point() == 1
+    for x in (g, g1, gm):
+        check_structure(x)
+
+
+def test_build_parameter_validation():
+    ra = _ra()
+    kv = ra.KVGroup(np.ones((4, 8), np.float32))
+    q = np.ones((2, 8), np.float32)
+    for bad, msg in [(dict(k_train=0), "k_train must be >= 1"),
+                     (dict(max_degree=0), "max_degree must be >= 1"),
+                     (dict(ef_construction=0), "ef_construction must be >= 1")]:
+        with pytest.raises(ra.InvalidArgument, match="^" + msg + "$"):
+            ra.ood_build(kv, q, ra.OODGraphBuildParams(**bad))
+    with pytest.raises(ra.InvalidArgument, match="^query dimension mismatch$"):
+        ra.ood_build(kv, np.ones((2, 7), np.float32))
+    with pytest.raises(ra.InvalidArgument, match="^empty keys$"):
+        ra.ood_build(ra.KVGroup(np.ones((0, 8), np.float32)), q)
+
+
+def test_recall_grows_with_ef_and_is_exact_at_ef_n(port):
+    # test_index_oodgraph.cpp:231-279 on the GPU build + GPU search
+    ra = _ra()
+    w = port.generate_workload(2048, 64, 32, 1, 1, seed=7, n_decode=64)
+    kv = ra.KVGroup(w["keys"][0])
+    g = ra.ood_build(kv, w["prefill_q"][0], ra.OODGraphBuildParams(32, 16, 64))
+    Q = w["decode_q"][0]
+    truth = [set(port.flat_search(w["keys"][0], q, 10).ids.tolist()) for q in Q]
+    rec, scan = [], []
+    for ef in (10, 20, 40, 80, 2048):
+        res = ra.search_batch([g], Q, 10, None, ef).host()
+        rec.append(np.mean([len(truth[i] & set(r.ids.tolist())) / 10 for i, r in enumerate(res)]))
+        scan.append(np.mean([r.scanned for r in res]))
+    assert rec[-1] == 1.0 and scan[-1] == 2048.0
+    assert rec[3] > 0.9 and scan[0] < 1024
+    assert all(scan[i] >= scan[i - 1] for i in range(1, 5))
