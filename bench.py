@@ -294,14 +294,14 @@ def recall(eng, graphs, kvs, Q, a, ra):
     mask = torch.zeros(a.n_ctx, dtype=torch.bool, device=Q.device)
     mask[torch.from_numpy(W.astype(np.int64)).to(Q.device)] = True
     rec_m, rec_u = [], []
+    K64 = [kv.keys_tensor().double() for kv in kvs]
     for i in range(min(4, a.steps)):
         q = Q[:, a.warmup + i]
         out, om, sc = eng.decode_step_device(q)
         omega = om.cpu().numpy().view(np.uint32)
         un = ra.search_batch(graphs, q, 100, None, a.ef).host()
         for h in range(len(graphs)):
-            K = kvs[h // hpg].keys_tensor().double()
-            s = K @ q[h].double()
+            s = K64[h // hpg] @ q[h].double()
             top_u = torch.topk(s, 100).indices.cpu().numpy()
             s[mask] = -float("inf")
             top_m = torch.topk(s, 100).indices.cpu().numpy()

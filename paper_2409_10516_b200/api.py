@@ -149,7 +149,7 @@ def _view_f32(ptr: int, numel: int, device: int) -> torch.Tensor:
     # borrow device memory owned by the library (valid while the owner lives)
     class _Holder:
         __cuda_array_interface__ = {
-            "shape": (numel,), "typestr": "<f4", "data": (ptr, True), "version": 2,
+            "shape": (numel,), "typestr": "<f4", "data": (ptr, False), "version": 2,
             "strides": None}
     return torch.as_tensor(_Holder(), device=f"cuda:{device}")
 
