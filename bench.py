@@ -164,7 +164,7 @@ def main():
         del w
     setup_s = time.time() - t0
     Hl = len(graphs)
-    Q = torch.stack(dq)  # [Hl, n_dec, d]
+    Q = torch.stack(dq, dim=1).contiguous()  # [n_dec, Hl, d]: Q[i] is one step, contiguous
     del dq
     cfg = ra.EngineConfig(128, 512, a.top_k, a.ef)
 
@@ -181,7 +181,7 @@ def main():
                       for _ in range(world)]
 
     def step(i):
-        out, om, sc = eng.decode_step_device(Q[:, i])
+        out, om, sc = eng.decode_step_device(Q[i])
         if dist is not None:
             dist.all_gather(gather_out, out)
         return out
@@ -221,7 +221,7 @@ def main():
     Qh = Q.cpu()
     e2e = []
     for i in range(a.warmup + a.steps, a.warmup + 2 * a.steps):
-        qh.copy_(Qh[:, i])
+        qh.copy_(Qh[i])
         flush.zero_()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -296,7 +296,7 @@ def recall(eng, graphs, kvs, Q, a, ra):
     rec_m, rec_u = [], []
     K64 = [kv.keys_tensor().double() for kv in kvs]
     for i in range(min(4, a.steps)):
-        q = Q[:, a.warmup + i]
+        q = Q[a.warmup + i]
         out, om, sc = eng.decode_step_device(q)
         omega = om.cpu().numpy().view(np.uint32)
         un = ra.search_batch(graphs, q, 100, None, a.ef).host()
@@ -335,8 +335,8 @@ def cpu_baseline(a, keys_host, vals_host, graphs, Q, cfg, eng):
     times, same_om, same_sc, max_rel, n = [], 0, 0, 0.0, 0
     t_end = time.time() + a.cpu_seconds
     i = a.warmup
-    while (time.time() < t_end or not times) and i < Q.shape[1]:
-        q = np.ascontiguousarray(Qh[:, i])
+    while (time.time() < t_end or not times) and i < Q.shape[0]:
+        q = np.ascontiguousarray(Qh[i])
         t0 = time.perf_counter()
         rout, rom, rsc = reng.step(q, i)
         times.append((time.perf_counter() - t0) * 1e3)
@@ -350,7 +350,7 @@ def cpu_baseline(a, keys_host, vals_host, graphs, Q, cfg, eng):
         i += 1
     base = {"value": round(statistics.mean(times), 3), "unit": "ms/token", "cores": threads,
             "kind": "reference",
-            "sample": f"{len(times)} decode steps x {Qh.shape[0]} heads at n_ctx {a.n_ctx} "
+            "sample": f"{len(times)} decode steps x {Qh.shape[1]} heads at n_ctx {a.n_ctx} "
                       f"(reference decode_step, n_threads={threads}, GPU-built graphs via OODG)"}
     parity = None if a.no_parity else {
         "heads_checked": n, "omega_identical": same_om, "scanned_identical": same_sc,
@@ -366,12 +366,12 @@ def run_reference(a, keys_host, vals_host, graphs, Q, cfg, H, G, setup_s):
         return
     Qh = Q.cpu().numpy()
     for i in range(a.warmup):
-        reng.step(np.ascontiguousarray(Qh[:, i]), i)
+        reng.step(np.ascontiguousarray(Qh[i]), i)
     times = []
     t_start = time.perf_counter()
     for i in range(a.warmup, a.warmup + a.steps):
         t0 = time.perf_counter()
-        reng.step(np.ascontiguousarray(Qh[:, i]), i)
+        reng.step(np.ascontiguousarray(Qh[i]), i)
         times.append((time.perf_counter() - t0) * 1e3)
     ms = statistics.mean(times)
     sample = (f"{a.steps} reference decode_steps x {H} heads at n_ctx {a.n_ctx} "

@@ -495,6 +495,9 @@ class Engine:
 
     def decode_step_device(self, q: torch.Tensor):
         """q: [H, d] f32 CUDA tensor -> (out, omega, scanned) device tensors."""
+        if (q.dtype != torch.float32 or not q.is_cuda or not q.is_contiguous()
+                or tuple(q.shape) != (self.H, self.d)):
+            raise InvalidArgument("q must be a contiguous [H, d] float32 CUDA tensor")
         self.ctx.bind_stream()
         _check(lib.ra_engine_step_device(self.h, _ptr(q), _ptr(self.out), _ptr(self.omega),
                                          _ptr(self.scanned)))

@@ -9,6 +9,7 @@
 #include <cfloat>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace ra {
 namespace {
@@ -151,6 +152,200 @@ __global__ void k_merge(uint32_t B, uint32_t d, const double* ow, const double* 
   }
 }
 
+// ---- engine path: W partial per (KV group, chunk of W) --------------------------
+// The static set W is shared by the hpg query heads of a group, so each W
+// key/value row is read from HBM once per group (TMA bulk copies into shared
+// memory) and scored against all hpg queries. Each chunk emits an
+// unnormalised partial (sum e*v, chunk max, sum e); k_omega_merge folds the
+// chunks with the same log-sum-exp rescaling merge() uses.
+constexpr uint32_t kWC = 64;  // W rows per CTA
+
+template <int D>
+__global__ void __launch_bounds__(256)
+    k_wpartial(const KVRef* __restrict__ gkv, const float* __restrict__ q,
+               const uint32_t* __restrict__ W, uint32_t nW, uint32_t hpg, double inv_sqrt_d,
+               double* __restrict__ part_out, double* __restrict__ part_m,
+               double* __restrict__ part_s) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t c = blockIdx.x, g = blockIdx.y, C = gridDim.x;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t i0 = c * kWC, rows = min(kWC, nW - i0);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  float* Kt = reinterpret_cast<float*>(smem + 16);                 // [kWC][D+4]
+  float* Vt = Kt + kWC * (D + 4);                                   // [kWC][D]
+  double* qs = reinterpret_cast<double*>(Vt + kWC * D);             // [hpg][D]
+  double* z = qs + size_t(hpg) * D;                                 // [hpg][kWC]
+  const float* K = gkv[g].keys;
+  const float* V = gkv[g].values;
+  if (tid == 0) {
+    mbar_init(bar);
+    mbar_arrive_expect_tx(bar, rows * D * 8u);
+  }
+  __syncthreads();
+  if (tid < rows) {
+    const uint32_t id = W[i0 + tid];
+    bulk_g2s(Kt + tid * (D + 4), K + size_t(id) * D, D * 4u, bar);
+    bulk_g2s(Vt + tid * D, V + size_t(id) * D, D * 4u, bar);
+  }
+  for (uint32_t e = tid; e < hpg * D; e += blockDim.x)
+    qs[e] = (double)q[size_t(g) * hpg * D + e];
+  __syncthreads();
+  mbar_wait(bar, 0);
+  for (uint32_t t = tid; t < hpg * kWC; t += blockDim.x) {
+    const uint32_t h = t / kWC, i = t % kWC;
+    double acc = -DBL_MAX;
+    if (i < rows) {
+      acc = 0.0;
+      const float4* r4 = reinterpret_cast<const float4*>(Kt + i * (D + 4));
+      const double* qh = qs + h * D;
+#pragma unroll 8
+      for (int cc = 0; cc < D / 4; ++cc) {
+        const float4 kv = r4[cc];
+        acc = fma(qh[4 * cc + 0], (double)kv.x, acc);
+        acc = fma(qh[4 * cc + 1], (double)kv.y, acc);
+        acc = fma(qh[4 * cc + 2], (double)kv.z, acc);
+        acc = fma(qh[4 * cc + 3], (double)kv.w, acc);
+      }
+      acc *= inv_sqrt_d;
+    }
+    z[h * kWC + i] = acc;
+  }
+  __syncthreads();
+  // per head: chunk max, e = exp(z - max), sum e (warp h handles head h)
+  const uint32_t warp = tid >> 5, lane = tid & 31;
+  for (uint32_t h = warp; h < hpg; h += blockDim.x / 32) {
+    double m = -DBL_MAX;
+    for (uint32_t i = lane; i < rows; i += 32) m = fmax(m, z[h * kWC + i]);
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(kFull, m, o));
+    double s = 0.0;
+    for (uint32_t i = lane; i < rows; i += 32) {
+      const double e = exp(z[h * kWC + i] - m);
+      z[h * kWC + i] = e;
+      s += e;
+    }
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    if (lane == 0) {
+      part_m[(size_t(g) * C + c) * hpg + h] = m;
+      part_s[(size_t(g) * C + c) * hpg + h] = s;
+    }
+  }
+  __syncthreads();
+  for (uint32_t t = tid; t < hpg * D; t += blockDim.x) {
+    const uint32_t h = t / D, j = t % D;
+    double acc = 0.0;
+    for (uint32_t i = 0; i < rows; ++i) acc = fma(z[h * kWC + i], (double)Vt[i * D + j], acc);
+    part_out[((size_t(g) * C + c) * hpg + h) * D + j] = acc;
+  }
+}
+
+// ---- engine path: Omega partial (search scores reused) + merge per head --------
+template <int D>
+__global__ void __launch_bounds__(128)
+    k_omega_merge(const KVRef* __restrict__ hkv, const uint32_t* __restrict__ ids,
+                  const double* __restrict__ s64, const uint32_t* __restrict__ n_out,
+                  uint32_t k, uint32_t hpg, uint32_t C, uint32_t nW, double inv_sqrt_d,
+                  const double* __restrict__ part_out, const double* __restrict__ part_m,
+                  const double* __restrict__ part_s, double* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t h = blockIdx.x, g = h / hpg, hl = h % hpg, tid = threadIdx.x;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  float* Vt = reinterpret_cast<float*>(smem + 16);                  // [kWC][D]
+  double* e = reinterpret_cast<double*>(Vt + kWC * D);              // [kWC]
+  __shared__ double red[4];
+  const uint32_t m = n_out[h];
+  const float* V = hkv[h].values;
+  if (tid == 0) mbar_init(bar);
+  // Omega max (scores are exact f64 search scores; z = s / sqrt(d))
+  double zo = -DBL_MAX;
+  for (uint32_t i = tid; i < m; i += blockDim.x) zo = fmax(zo, s64[size_t(h) * k + i] * inv_sqrt_d);
+  for (int o = 16; o; o >>= 1) zo = fmax(zo, __shfl_xor_sync(kFull, zo, o));
+  if ((tid & 31) == 0) red[tid >> 5] = zo;
+  __syncthreads();
+  zo = fmax(fmax(red[0], red[1]), fmax(red[2], red[3]));
+  double acc[(D + 127) / 128] = {};
+  double so = 0.0;
+  uint32_t phase = 0;
+  for (uint32_t t0 = 0; t0 < m; t0 += kWC) {
+    const uint32_t rows = min(kWC, m - t0);
+    __syncthreads();  // previous tile fully consumed
+    if (tid == 0) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(bar, rows * D * 4u);
+    }
+    __syncthreads();
+    if (tid < rows) {
+      bulk_g2s(Vt + tid * D, V + size_t(ids[size_t(h) * k + t0 + tid]) * D, D * 4u, bar);
+      e[tid] = exp(s64[size_t(h) * k + t0 + tid] * inv_sqrt_d - zo);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    __syncthreads();
+    for (uint32_t i = 0; i < rows; ++i) {
+      const double ei = e[i];
+      so += ei;
+#pragma unroll
+      for (uint32_t r = 0; r < (D + 127) / 128; ++r) {
+        const uint32_t j = tid + r * 128;
+        if (j < D) acc[r] = fma(ei, (double)Vt[i * D + j], acc[r]);
+      }
+    }
+  }
+  // W partial: fold the chunks (log-sum-exp), then merge() with Omega
+  double zw = -DBL_MAX;
+  for (uint32_t c = 0; c < C; ++c) zw = fmax(zw, part_m[(size_t(g) * C + c) * hpg + hl]);
+  double sw = 0.0;
+  for (uint32_t c = 0; c < C; ++c)
+    sw += exp(part_m[(size_t(g) * C + c) * hpg + hl] - zw) * part_s[(size_t(g) * C + c) * hpg + hl];
+  const bool we = nW == 0, oe = m == 0;
+  double gw = 1.0, go = 0.0;
+  if (we) {
+    gw = 0.0, go = 1.0;
+  } else if (!oe) {
+    const double zref = fmax(zw, zo);
+    const double ew = exp(zw - zref) * sw, eo = exp(zo - zref) * so;
+    gw = ew / (ew + eo);
+    go = eo / (ew + eo);
+  }
+#pragma unroll
+  for (uint32_t r = 0; r < (D + 127) / 128; ++r) {
+    const uint32_t j = tid + r * 128;
+    if (j >= D) continue;
+    double ow = 0.0;
+    if (!we) {
+      for (uint32_t c = 0; c < C; ++c)
+        ow += exp(part_m[(size_t(g) * C + c) * hpg + hl] - zw) *
+              part_out[((size_t(g) * C + c) * hpg + hl) * D + j];
+      ow /= sw;
+    }
+    const double oo = oe ? 0.0 : acc[r] / so;
+    out[size_t(h) * D + j] = we ? oo : (oe ? ow : gw * ow + go * oo);
+  }
+}
+
+template <int D>
+void launch_engine_attention_d(cudaStream_t st, const EngineAttn& a, int part) {
+  const uint32_t C = (a.nW + kWC - 1) / kWC;
+  if (part == 0) {
+    if (!C) return;
+    const size_t smem_w = 16 + kWC * (D + 4) * 4 + kWC * D * 4 + size_t(a.hpg) * D * 8 +
+                          size_t(a.hpg) * kWC * 8;
+    RA_CUDA(cudaFuncSetAttribute(k_wpartial<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem_w));
+    k_wpartial<D><<<dim3(C, a.G), 256, smem_w, st>>>(a.gkv, a.q, a.W, a.nW, a.hpg,
+                                                      a.inv_sqrt_d, a.part_out, a.part_m,
+                                                      a.part_s);
+    RA_LAUNCH_CHECK();
+    return;
+  }
+  const size_t smem_o = 16 + kWC * D * 4 + kWC * 8;
+  RA_CUDA(cudaFuncSetAttribute(k_omega_merge<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem_o));
+  k_omega_merge<D><<<a.H, 128, smem_o, st>>>(a.hkv, a.ids, a.s64, a.n_out, a.k, a.hpg, C, a.nW,
+                                             a.inv_sqrt_d, a.part_out, a.part_m, a.part_s,
+                                             a.out);
+  RA_LAUNCH_CHECK();
+}
+
 }  // namespace
 
 size_t partial_scratch_doubles(uint32_t B, uint32_t max_m) {
@@ -188,6 +383,26 @@ void launch_merge(cudaStream_t s, uint32_t B, uint32_t d, const double* ow, cons
   k_merge<<<uint32_t((total + 255) / 256), 256, 0, s>>>(B, d, ow, zw, sw, w_empty, oo, zo, so,
                                                          o_empty, out, gw, go, err_flag);
   RA_LAUNCH_CHECK();
+}
+
+bool engine_attention_supported(uint32_t d) { return d == 128 || d == 64 || d == 32; }
+
+size_t engine_attention_part_doubles(uint32_t G, uint32_t hpg, uint32_t nW, uint32_t d) {
+  const uint32_t C = (nW + kWC - 1) / kWC;
+  return size_t(G) * std::max<uint32_t>(C, 1) * hpg * (d + 2);
+}
+
+static void engine_attention(cudaStream_t st, const EngineAttn& a, int part) {
+  switch (a.d) {
+    case 128: launch_engine_attention_d<128>(st, a, part); break;
+    case 64: launch_engine_attention_d<64>(st, a, part); break;
+    case 32: launch_engine_attention_d<32>(st, a, part); break;
+    default: throw Error(RA_ERR_RUNTIME, "engine attention: unsupported head dim");
+  }
+}
+void launch_engine_wpartial(cudaStream_t st, const EngineAttn& a) { engine_attention(st, a, 0); }
+void launch_engine_omega_merge(cudaStream_t st, const EngineAttn& a) {
+  engine_attention(st, a, 1);
 }
 
 }  // namespace ra

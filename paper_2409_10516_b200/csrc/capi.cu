@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstring>
 #include <memory>
+#include <cmath>
 #include <numeric>
 
 #include "common.cuh"
@@ -405,6 +406,13 @@ struct ra_engine {
   // events bracketing the search kernel and the attention kernels of the
   // last step, recorded on the ctx stream (ra_engine_last_timing)
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  // fast attention path: W partials on a side stream overlapping the search
+  bool fast_attn = false;
+  cudaStream_t aux = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  DevBuf<KVRef> gkv;
+  DevBuf<double> part;
+  uint32_t hpg = 0;
 };
 
 extern "C" {
@@ -467,6 +475,14 @@ ra_status ra_engine_create(ra_ctx* ctx, ra_kv* const* groups, uint32_t n_groups,
     };
     up(e->desc, desc);
     up(e->kvrefs, refs);
+    std::vector<KVRef> grefs(n_groups);
+    for (uint32_t gi = 0; gi < n_groups; ++gi)
+      grefs[gi] = KVRef{groups[gi]->keys.p, groups[gi]->values.p, groups[gi]->n};
+    up(e->gkv, grefs);
+    e->hpg = per;
+    e->fast_attn = engine_attention_supported(d);
+    if (e->fast_attn)
+      e->part.alloc(engine_attention_part_doubles(n_groups, per, uint32_t(ns), d));
     up(e->w_ids, w);
     up(e->w_m, std::vector<uint32_t>(H, uint32_t(ns)));
     up(e->w_empty, std::vector<uint8_t>(H, ns == 0));
@@ -488,6 +504,9 @@ ra_status ra_engine_create(ra_ctx* ctx, ra_kv* const* groups, uint32_t n_groups,
     const size_t sb = search_scratch_bytes(ctx, H, e->max_n, d);
     e->search_scratch.alloc(sb);
     for (auto& ev : e->ev) RA_CUDA(cudaEventCreate(&ev));
+    RA_CUDA(cudaStreamCreateWithFlags(&e->aux, cudaStreamNonBlocking));
+    RA_CUDA(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
+    RA_CUDA(cudaEventCreateWithFlags(&e->join, cudaEventDisableTiming));
     RA_CUDA(cudaStreamSynchronize(ctx->stream));
     *out = e.release();
   });
@@ -501,6 +520,9 @@ void ra_engine_destroy(ra_engine* e) {
     for (ra_kv* g : e->groups) ra_kv_release(g);
     for (auto& ev : e->ev)
       if (ev) cudaEventDestroy(ev);
+    if (e->aux) cudaStreamDestroy(e->aux);
+    if (e->fork) cudaEventDestroy(e->fork);
+    if (e->join) cudaEventDestroy(e->join);
   }
   delete e;
 }
@@ -512,6 +534,19 @@ void engine_enqueue(ra_engine* e, const float* q_dev) {
   ra_ctx* ctx = e->ctx;
   cudaStream_t s = ctx->stream;
   const uint32_t H = e->H, d = e->d;
+  EngineAttn ea{};
+  if (e->fast_attn) {
+    const uint32_t C = uint32_t((e->n_static + 63) / 64);
+    ea = EngineAttn{e->gkv.p, e->kvrefs.p, q_dev, e->w_ids.p, uint32_t(e->n_static), e->G, H,
+                    e->hpg, d, e->k, 1.0 / std::sqrt(double(d)), e->ids.p, e->scores64.p,
+                    e->n_out.p, e->part.p, e->part.p + size_t(e->G) * std::max(C, 1u) * e->hpg * d,
+                    e->part.p + size_t(e->G) * std::max(C, 1u) * e->hpg * (d + 1), e->out.p};
+    // fork: the W partials depend only on q, so they run beside the search
+    RA_CUDA(cudaEventRecord(e->fork, s));
+    RA_CUDA(cudaStreamWaitEvent(e->aux, e->fork, 0));
+    launch_engine_wpartial(e->aux, ea);
+    RA_CUDA(cudaEventRecord(e->join, e->aux));
+  }
   RA_CUDA(cudaEventRecord(e->ev[0], s));
   if (e->n_pool > 0) {
     SearchArgs sa{};
@@ -535,6 +570,12 @@ void engine_enqueue(ra_engine* e, const float* q_dev) {
     RA_CUDA(cudaMemsetAsync(e->expanded.p, 0, H * 4, s));
   }
   RA_CUDA(cudaEventRecord(e->ev[1], s));
+  if (e->fast_attn) {
+    RA_CUDA(cudaStreamWaitEvent(s, e->join, 0));
+    launch_engine_omega_merge(s, ea);
+    RA_CUDA(cudaEventRecord(e->ev[2], s));
+    return;
+  }
   launch_partial_attention_ex(s, e->kvrefs.p, d, H, q_dev, e->w_ids.p, 0, e->w_m.p, nullptr, 0,
                               e->ow.p, e->zw.p, e->sw.p, nullptr, 0, e->w_empty.p, e->flag.p);
   launch_partial_attention_ex(s, e->kvrefs.p, d, H, q_dev, e->ids.p, e->k, e->n_out.p,

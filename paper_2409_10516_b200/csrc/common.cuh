@@ -203,4 +203,27 @@ void launch_merge(cudaStream_t s, uint32_t B, uint32_t d, const double* ow, cons
                   const double* zo, const double* so, const uint8_t* o_empty, double* out,
                   double* gw, double* go, uint32_t* err_flag);
 
+// engine fast path (attention.cu): W partial per (group, 64-row chunk) on a
+// side stream (overlaps the search), then Omega partial + chunk fold + merge
+// per head on the main stream after the search.
+struct EngineAttn {
+  const KVRef* gkv;   // [G] per group
+  const KVRef* hkv;   // [H] per head
+  const float* q;     // [H][d]
+  const uint32_t* W;  // static ids
+  uint32_t nW, G, H, hpg, d, k;
+  double inv_sqrt_d;
+  const uint32_t* ids;   // [H][k] omega
+  const double* s64;     // [H][k] exact scores
+  const uint32_t* n_out; // [H]
+  double* part_out;      // [G][C][hpg][d]
+  double* part_m;        // [G][C][hpg]
+  double* part_s;
+  double* out;           // [H][d]
+};
+bool engine_attention_supported(uint32_t d);
+size_t engine_attention_part_doubles(uint32_t G, uint32_t hpg, uint32_t nW, uint32_t d);
+void launch_engine_wpartial(cudaStream_t st, const EngineAttn& a);
+void launch_engine_omega_merge(cudaStream_t st, const EngineAttn& a);
+
 }  // namespace ra

@@ -22,6 +22,7 @@
 #include <cfloat>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace ra {
 namespace {
@@ -84,10 +85,44 @@ struct ListRef {
   uint8_t* fl;
 };
 
+// in-order f64 dot of q (f64, smem) and a key row staged in shared memory
 template <int D>
-__global__ void __launch_bounds__(256) k_graph_search(SearchArgs a, uint32_t wpb, uint32_t cap,
-                                                      uint32_t spill_cap, int vis_smem,
-                                                      uint32_t vis_words, uint32_t d_pad) {
+__device__ __forceinline__ double smem_dot(const double* __restrict__ qd,
+                                           const float* __restrict__ row) {
+  double acc = 0.0;
+  const float4* r4 = reinterpret_cast<const float4*>(row);
+#pragma unroll 8
+  for (int c = 0; c < D / 4; ++c) {
+    const float4 k = r4[c];
+    acc = fma(qd[4 * c + 0], (double)k.x, acc);
+    acc = fma(qd[4 * c + 1], (double)k.y, acc);
+    acc = fma(qd[4 * c + 2], (double)k.z, acc);
+    acc = fma(qd[4 * c + 3], (double)k.w, acc);
+  }
+  return acc;
+}
+
+// Per-warp shared-memory layout (16-B aligned pieces):
+//   mbarrier | q as f64 [d_pad] | key-row tile [32][d+4] f32 (TMA target,
+//   D > 0 only) | list L: s f64[cap], id u32[cap], flags u8[cap] | visited bitset
+template <int D>
+struct WarpLayout {
+  uint32_t d_pad, cap, vis_words, vis_smem, row_stride;
+  __host__ __device__ size_t rows_bytes() const {
+    return D > 0 ? size_t(32) * row_stride * 4 : 0;
+  }
+  __host__ __device__ size_t list_off() const { return 16 + size_t(d_pad) * 8 + rows_bytes(); }
+  __host__ __device__ size_t vis_off() const {
+    return list_off() + ((size_t(cap) * 13 + 15) & ~size_t(15));
+  }
+  __host__ __device__ size_t bytes() const {
+    return vis_off() + (vis_smem ? ((size_t(vis_words) * 4 + 15) & ~size_t(15)) : 0);
+  }
+};
+
+template <int D>
+__global__ void __launch_bounds__(128, 1) k_graph_search(SearchArgs a, uint32_t wpb,
+                                                      WarpLayout<D> lay, uint32_t spill_cap) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t b = blockIdx.x * wpb + warp;
@@ -97,21 +132,22 @@ __global__ void __launch_bounds__(256) k_graph_search(SearchArgs a, uint32_t wpb
   const uint32_t d = a.d, M = g.M, ef = g.ef, k = a.k;
   const float* __restrict__ keys = g.keys;
   const uint32_t* __restrict__ adj = g.adj;
+  const uint32_t cap = lay.cap, vis_words = lay.vis_words;
 
-  // ---- per-warp shared memory carve-up ----
-  const size_t per_warp = size_t(d_pad) * 8 + size_t(cap) * 13 + (vis_smem ? vis_words * 4 : 0);
-  const size_t per_warp_al = (per_warp + 15) & ~size_t(15);
-  uint8_t* base = smem + warp * per_warp_al;
-  double* qd = reinterpret_cast<double*>(base);
-  ListRef L{reinterpret_cast<double*>(base + size_t(d_pad) * 8), nullptr, nullptr};
+  uint8_t* base = smem + size_t(warp) * lay.bytes();
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base);
+  double* qd = reinterpret_cast<double*>(base + 16);
+  float* rows = reinterpret_cast<float*>(base + 16 + size_t(lay.d_pad) * 8);
+  ListRef L{reinterpret_cast<double*>(base + lay.list_off()), nullptr, nullptr};
   L.id = reinterpret_cast<uint32_t*>(L.s + cap);
   L.fl = reinterpret_cast<uint8_t*>(L.id + cap);
-  uint32_t* vis = vis_smem ? reinterpret_cast<uint32_t*>(base + size_t(d_pad) * 8 +
-                                                         ((size_t(cap) * 13 + 3) & ~size_t(3)))
-                           : a.vis_global + size_t(b) * vis_words;
+  uint32_t* vis = lay.vis_smem ? reinterpret_cast<uint32_t*>(base + lay.vis_off())
+                               : a.vis_global + size_t(b) * vis_words;
   uint32_t lcap = cap;
   bool spilled = false;
+  uint32_t phase = 0;
 
+  if (lane == 0) mbar_init(bar);
   for (uint32_t w = lane; w < vis_words; w += 32) vis[w] = 0;
   for (uint32_t i = lane; i < d; i += 32) qd[i] = (double)a.q[size_t(b) * d + i];
   __syncwarp();
@@ -119,11 +155,28 @@ __global__ void __launch_bounds__(256) k_graph_search(SearchArgs a, uint32_t wpb
   auto masked_id = [&](uint32_t v) -> bool {
     return a.mask_bits != nullptr && ((__ldg(a.mask_bits + (v >> 5)) >> (v & 31)) & 1u);
   };
+  // exact scores of the lanes in `m` (lane j scores node v): key rows land in
+  // the shared tile through TMA bulk copies (one round trip for all rows),
+  // then each lane runs its in-order f64 chain from shared memory
+  auto score_lanes = [&](uint32_t m, bool mine, uint32_t v) -> double {
+    if constexpr (D > 0) {
+      const uint32_t slot = __popc(m & ((1u << lane) - 1u));
+      float* row = rows + size_t(slot) * lay.row_stride;
+      fence_proxy_async();
+      if (lane == 0) mbar_arrive_expect_tx(bar, __popc(m) * uint32_t(D) * 4u);
+      __syncwarp();
+      if (mine) bulk_g2s(row, keys + size_t(v) * D, uint32_t(D) * 4u, bar);
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+      return mine ? smem_dot<D>(qd, row) : -DBL_MAX;
+    } else {
+      return mine ? exact_dot<0>(qd, keys + size_t(v) * d, d) : -DBL_MAX;
+    }
+  };
 
   // ---- entry (:379-384) ----
   const uint32_t entry = (uint32_t)g.entry;
-  double s0 = 0.0;
-  if (lane == 0) s0 = exact_dot<D>(qd, keys + size_t(entry) * d, d);
+  double s0 = score_lanes(1u, lane == 0, entry);
   s0 = __shfl_sync(kFull, s0, 0);
   const bool m0 = masked_id(entry);
   if (lane == 0) {
@@ -138,6 +191,9 @@ __global__ void __launch_bounds__(256) k_graph_search(SearchArgs a, uint32_t wpb
   uint32_t expanded = 0;
   bool pool_full = false;
   double worst_s = -DBL_MAX;
+  // speculation: adjacency row of the likely next top, held in registers
+  uint32_t pre_u = kSentinel, pre_v = kSentinel;
+  const bool spec = M <= 32;
 
   // position of the ef-th unmasked entry; then drop dead tail entries
   auto refresh_pool = [&]() {
@@ -183,26 +239,58 @@ __global__ void __launch_bounds__(256) k_graph_search(SearchArgs a, uint32_t wpb
 
   for (;;) {
     // frontier top = first unexpanded entry at or after cursor
-    uint32_t top = len;
+    uint32_t top = len, ubm = 0, ubase = 0;
     for (uint32_t c = cursor; c < len; c += 32) {
       const uint32_t i = c + lane;
       const uint32_t bm = __ballot_sync(kFull, i < len && !(L.fl[i] & kExpanded));
       if (bm) {
         top = c + __ffs(bm) - 1;
+        ubm = bm & (bm - 1);  // further unexpanded entries of this chunk
+        ubase = c;
         break;
       }
     }
     cursor = top;
-    if (top >= len) break;                             // frontier exhausted
-    if (pool_full && L.s[top] < worst_s) break;        // :390
+    if (top >= len) break;                       // frontier exhausted
+    if (pool_full && L.s[top] < worst_s) break;  // :390
     const uint32_t u = L.id[top];
     __syncwarp();
     if (lane == 0) L.fl[top] |= kExpanded;
     ++expanded;
 
+    // adjacency of u: from the speculation registers when it guessed right
+    uint32_t vrow;
+    if (spec && pre_u == u) {
+      vrow = pre_v;
+    } else {
+      vrow = lane < M ? __ldg(adj + size_t(u) * M + lane) : kSentinel;
+    }
+    // speculate: the next unexpanded entry is the likely next top; start
+    // loading its adjacency now and prefetch the two after it into L2
+    uint32_t nxt = kSentinel;
+    if (spec && ubm) {
+      const uint32_t i1 = ubase + __ffs(ubm) - 1;
+      nxt = L.id[i1];
+      pre_v = lane < M ? __ldg(adj + size_t(nxt) * M + lane) : kSentinel;
+      const uint32_t rest = ubm & (ubm - 1);
+      if (lane < 2 && rest) {
+        uint32_t r = rest;
+        if (lane == 1) r &= r - 1;
+        if (r) {
+          const uint32_t cand = L.id[ubase + __ffs(r) - 1];
+          if ((M * 4) % 16 == 0)
+            bulk_prefetch_l2(adj + size_t(cand) * M, M * 4);
+          else
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(adj + size_t(cand) * M));
+        }
+      }
+    }
+    pre_u = nxt;
+
     for (uint32_t c0 = 0; c0 < M; c0 += 32) {
-      const uint32_t j = c0 + lane;
-      const uint32_t v = j < M ? __ldg(adj + size_t(u) * M + j) : kSentinel;
+      const uint32_t v = c0 == 0 ? vrow
+                                 : (c0 + lane < M ? __ldg(adj + size_t(u) * M + c0 + lane)
+                                                  : kSentinel);
       const bool valid = v != kSentinel;
       const uint32_t grp = __match_any_sync(kFull, v);
       const bool first = (uint32_t)(__ffs(grp) - 1) == lane;
@@ -213,8 +301,12 @@ __global__ void __launch_bounds__(256) k_graph_search(SearchArgs a, uint32_t wpb
       const uint32_t newmask = __ballot_sync(kFull, isnew);
       if (!newmask) continue;
       scanned += __popc(newmask);
-      double s = -DBL_MAX;
-      if (isnew) s = exact_dot<D>(qd, keys + size_t(v) * d, d);
+      const double s = score_lanes(newmask, isnew, v);
+      // second speculation level: the likely next top's unvisited neighbours'
+      // key rows go to L2 while this expansion's list work runs
+      if (c0 == 0 && pre_u != kSentinel && pre_v != kSentinel &&
+          !((vis[pre_v >> 5] >> (pre_v & 31)) & 1u))
+        bulk_prefetch_l2(keys + size_t(pre_v) * d, d * 4);
       const bool msk = isnew && masked_id(v);
       const bool live = isnew && !(pool_full && s < worst_s);
       const uint32_t livemask = __ballot_sync(kFull, live);
@@ -336,24 +428,31 @@ __global__ void k_mask_bitset(const uint32_t* mask, uint64_t mask_n, uint32_t* b
   }
 }
 
+bool tiled_dim(uint32_t d) { return d == 128 || d == 64 || d == 32 || d == 16 || d == 8; }
+
 struct Plan {
-  uint32_t wpb, cap, vis_smem, vis_words, d_pad;
-  size_t smem;
+  uint32_t wpb, cap, vis_smem, vis_words, d_pad, row_stride;
+  size_t per_warp, smem;
 };
 
+// Shared-memory plan: one query per CTA while the batch cannot fill the SMs
+// (each search then owns an SM's L1 and DFMA pipe), else 4 per CTA; the
+// list capacity takes what is left after q, the TMA row tile and (if it
+// fits) the visited bitset.
 Plan plan(const ra_ctx* ctx, uint32_t B, uint32_t max_n, uint32_t d) {
   Plan p{};
   p.d_pad = (d + 1) & ~1u;
   p.vis_words = (max_n + 31) / 32;
+  p.row_stride = d + 4;
+  const size_t rows = tiled_dim(d) ? size_t(32) * p.row_stride * 4 : 0;
   const size_t budget = ctx->smem_optin ? ctx->smem_optin : 227 * 1024;
-  // one query per CTA while the batch cannot fill the SMs; else 4 per CTA
   p.wpb = B <= uint32_t(ctx->num_sms) ? 1 : 4;
   for (;;) {
     const size_t per_warp_budget = budget / p.wpb;
-    const size_t fixed = size_t(p.d_pad) * 8 + 16;
-    const size_t vis_bytes = size_t(p.vis_words) * 4;
+    const size_t fixed = 16 + size_t(p.d_pad) * 8 + rows + 32;
+    const size_t vis_bytes = (size_t(p.vis_words) * 4 + 15) & ~size_t(15);
     p.vis_smem = fixed + vis_bytes + 13 * 512 <= per_warp_budget;
-    size_t rest = per_warp_budget - fixed - (p.vis_smem ? vis_bytes : 0);
+    const size_t rest = per_warp_budget - fixed - (p.vis_smem ? vis_bytes : 0);
     uint32_t cap = uint32_t(std::min<size_t>(rest / 13, 8192));
     cap = std::min<uint32_t>(cap, std::max<uint32_t>(max_n, 64));
     cap &= ~31u;
@@ -363,19 +462,20 @@ Plan plan(const ra_ctx* ctx, uint32_t B, uint32_t max_n, uint32_t d) {
     }
     p.wpb /= 2;
   }
-  const size_t per_warp = size_t(p.d_pad) * 8 + size_t(p.cap) * 13 + 4 +
-                          (p.vis_smem ? size_t(p.vis_words) * 4 : 0);
-  p.smem = ((per_warp + 15) & ~size_t(15)) * p.wpb;
+  p.per_warp = 16 + size_t(p.d_pad) * 8 + rows + ((size_t(p.cap) * 13 + 15) & ~size_t(15)) +
+               (p.vis_smem ? ((size_t(p.vis_words) * 4 + 15) & ~size_t(15)) : 0);
+  p.smem = p.per_warp * p.wpb;
   return p;
 }
 
 template <int D>
 void launch_d(ra_ctx* ctx, const SearchArgs& a, const Plan& p, uint32_t spill_cap) {
   auto kern = k_graph_search<D>;
+  WarpLayout<D> lay{p.d_pad, p.cap, p.vis_words, p.vis_smem, p.row_stride};
+  if (lay.bytes() != p.per_warp) throw Error(RA_ERR_RUNTIME, "search smem layout mismatch");
   RA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   const uint32_t grid = (a.B + p.wpb - 1) / p.wpb;
-  kern<<<grid, 32 * p.wpb, p.smem, ctx->stream>>>(a, p.wpb, p.cap, spill_cap, p.vis_smem,
-                                                  p.vis_words, p.d_pad);
+  kern<<<grid, 32 * p.wpb, p.smem, ctx->stream>>>(a, p.wpb, lay, spill_cap);
   RA_LAUNCH_CHECK();
 }
 
