@@ -265,7 +265,7 @@ ra_status ra_graph_search_batch(ra_ctx* ctx, const ra_graph* const* graphs, uint
   return guard([&] {
     check_ctx(ctx);
     if (B == 0) return;
-    uint32_t max_n = 0;
+    uint32_t max_n = 0, max_M = 0;
     std::vector<GraphDesc> desc(B);
     for (uint32_t b = 0; b < B; ++b) {
       const ra_graph* g = graphs[b];
@@ -277,6 +277,7 @@ ra_status ra_graph_search_batch(ra_ctx* ctx, const ra_graph* const* graphs, uint
       desc[b] = GraphDesc{g->adj.p, g->kv->keys.p, g->entry, uint32_t(g->n), g->max_degree,
                           uint32_t(std::min<uint64_t>(e, 0xFFFFFFFFu)), 0};
       max_n = std::max<uint32_t>(max_n, uint32_t(g->n));
+      max_M = std::max<uint32_t>(max_M, g->max_degree);
     }
     DeviceGuard dg(ctx->device);
     const uint64_t words = (uint64_t(max_n) + 31) / 32;
@@ -294,6 +295,7 @@ ra_status ra_graph_search_batch(ra_ctx* ctx, const ra_graph* const* graphs, uint
     sa.B = B;
     sa.d = q_dim;
     sa.k = k;
+    sa.max_M = max_M;
     sa.ids = ids;
     sa.scores = scores;
     sa.scores64 = nullptr;
@@ -402,7 +404,7 @@ struct ra_engine {
   DevBuf<uint64_t> scanned;
   DevBuf<uint8_t> truncated;
   DevBuf<uint8_t> search_scratch;
-  uint32_t max_n = 0;
+  uint32_t max_n = 0, max_M = 0;
   // events bracketing the search kernel and the attention kernels of the
   // last step, recorded on the ctx stream (ra_engine_last_timing)
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -466,6 +468,7 @@ ra_status ra_engine_create(ra_ctx* ctx, ra_kv* const* groups, uint32_t n_groups,
                           uint32_t(std::min<uint64_t>(ef, 0xFFFFFFFFu)), 0};
       refs[h] = KVRef{g->kv->keys.p, g->kv->values.p, g->kv->n};
       e->max_n = std::max<uint32_t>(e->max_n, uint32_t(g->n));
+      e->max_M = std::max<uint32_t>(e->max_M, g->max_degree);
     }
     auto up = [&](auto& buf, const auto& vec) {
       buf.alloc(std::max<size_t>(vec.size(), 1));
@@ -556,6 +559,7 @@ void engine_enqueue(ra_engine* e, const float* q_dev) {
     sa.B = H;
     sa.d = d;
     sa.k = e->k;
+    sa.max_M = e->max_M;
     sa.ids = e->ids.p;
     sa.scores = e->scores.p;
     sa.scores64 = e->scores64.p;

@@ -165,6 +165,7 @@ struct SearchArgs {
   const float* q;             // [B][d]
   const uint32_t* mask_bits;  // bitset over ids, nullptr = no mask (shared by batch)
   uint32_t B, d, k;
+  uint32_t max_M;             // max degree bound over the batch's graphs
   uint32_t* ids;              // [B][k]
   float* scores;              // [B][k]
   double* scores64;           // optional [B][k] exact f64 scores

@@ -428,6 +428,396 @@ __global__ void k_mask_bitset(const uint32_t* mask, uint64_t mask_n, uint32_t* b
   }
 }
 
+// ---------------------------------------------------------------------------
+// K6 v3: one CTA (4 warps) per query, speculative parallel pre-expansion.
+//
+// Round r: (A) every warp pre-expands frontier candidates chosen by warp 0 —
+// adjacency row, visited filter, TMA row copies, exact in-order chains — into
+// a "packet" {neighbour ids, exact scores} sorted best-first; (B) warp 0
+// commits packets strictly in the reference's pop order: top = best
+// unexpanded entry, stop rule (:390), re-filter the packet against the
+// visited set as it is NOW (earlier commits may have visited some), mark,
+// count, offer. The round ends at the first top without a packet; its
+// candidates are packeted next round. Packets are pure functions of
+// (query, node), so only the committed expansion SET matters and the result
+// is bit-identical to the reference (same proof as v2).
+constexpr uint32_t kCW = 4;   // warps per CTA
+constexpr uint32_t kCB = 8;   // candidates pre-expanded per round
+constexpr uint32_t kCP = 16;  // packet slots
+
+template <int D>
+struct CtaLayout {
+  uint32_t d_pad, cap, vis_words, vis_smem;
+  static constexpr uint32_t kRow = D + 4;  // padded row stride (floats)
+  __host__ __device__ static size_t tiles_off() { return 64 + size_t(D) * 8; }
+  __host__ __device__ static size_t pk_off() {
+    return tiles_off() + size_t(kCW) * 32 * kRow * 4;
+  }
+  // packets: tag u32[P], cnt u32[P], cand u32[B], slotof u32[B], ctrl u32[8],
+  // stage u32[32], ids u32[P][32], s f64[P][32]
+  __host__ __device__ static size_t pk_bytes() {
+    return ((size_t(kCP) * 8 + kCB * 8 + 32 + 128 + 15) & ~size_t(15)) + size_t(kCP) * 32 * 12;
+  }
+  __host__ __device__ size_t list_off() const { return pk_off() + pk_bytes(); }
+  __host__ __device__ size_t vis_off() const {
+    return list_off() + ((size_t(cap) * 13 + 15) & ~size_t(15));
+  }
+  __host__ __device__ size_t bytes() const {
+    return vis_off() + (vis_smem ? ((size_t(vis_words) * 4 + 15) & ~size_t(15)) : 0);
+  }
+};
+
+template <int D>
+__global__ void __launch_bounds__(kCW * 32, 1)
+    k_graph_search_cta(SearchArgs a, CtaLayout<D> lay, uint32_t spill_cap) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t b = blockIdx.x;
+  const GraphDesc g = a.desc[b];
+  const uint32_t M = g.M, ef = g.ef, k = a.k;
+  const float* __restrict__ keys = g.keys;
+  const uint32_t* __restrict__ adj = g.adj;
+  const uint32_t cap = lay.cap, vis_words = lay.vis_words;
+  constexpr uint32_t RS = CtaLayout<D>::kRow;
+
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // [kCW]
+  double* qd = reinterpret_cast<double*>(smem + 64);
+  float* tile = reinterpret_cast<float*>(smem + CtaLayout<D>::tiles_off()) + size_t(warp) * 32 * RS;
+  uint8_t* pk = smem + CtaLayout<D>::pk_off();
+  uint32_t* pk_tag = reinterpret_cast<uint32_t*>(pk);
+  uint32_t* pk_cnt = pk_tag + kCP;
+  uint32_t* cand = pk_cnt + kCP;
+  uint32_t* slotof = cand + kCB;
+  uint32_t* ctrl = slotof + kCB;  // [0] = #candidates, [1] = done
+  uint32_t* stage = ctrl + 8;     // 32 insertion points (warp 0)
+  uint32_t* pk_id = reinterpret_cast<uint32_t*>(
+      pk + ((size_t(kCP) * 8 + kCB * 8 + 32 + 128 + 15) & ~size_t(15)));
+  double* pk_s = reinterpret_cast<double*>(pk_id + kCP * 32);
+  ListRef L{reinterpret_cast<double*>(smem + lay.list_off()), nullptr, nullptr};
+  L.id = reinterpret_cast<uint32_t*>(L.s + cap);
+  L.fl = reinterpret_cast<uint8_t*>(L.id + cap);
+  uint32_t* vis = lay.vis_smem ? reinterpret_cast<uint32_t*>(smem + lay.vis_off())
+                               : a.vis_global + size_t(b) * vis_words;
+  uint64_t* bar = bars + warp;
+  uint32_t phase = 0;
+
+  if (lane == 0) mbar_init(bar);
+  for (uint32_t w = threadIdx.x; w < vis_words; w += blockDim.x) vis[w] = 0;
+  for (uint32_t i = threadIdx.x; i < D; i += blockDim.x) qd[i] = (double)a.q[size_t(b) * D + i];
+  if (threadIdx.x < kCP) pk_tag[threadIdx.x] = kSentinel;
+  __syncthreads();
+
+  auto masked_id = [&](uint32_t v) -> bool {
+    return a.mask_bits != nullptr && ((__ldg(a.mask_bits + (v >> 5)) >> (v & 31)) & 1u);
+  };
+  auto visited = [&](uint32_t v) -> bool { return (vis[v >> 5] >> (v & 31)) & 1u; };
+  // TMA rows of the lanes in m into this warp's tile, then in-order chains
+  auto score_lanes = [&](uint32_t m, bool mine, uint32_t v) -> double {
+    const uint32_t slot = __popc(m & ((1u << lane) - 1u));
+    float* row = tile + size_t(slot) * RS;
+    fence_proxy_async();
+    if (lane == 0) mbar_arrive_expect_tx(bar, __popc(m) * uint32_t(D) * 4u);
+    __syncwarp();
+    if (mine) bulk_g2s(row, keys + size_t(v) * D, uint32_t(D) * 4u, bar);
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    return mine ? smem_dot<D>(qd, row) : -DBL_MAX;
+  };
+
+  // warp-0 state (the committed search)
+  uint32_t len = 0, cursor = 0, n_unmasked = 0, expanded = 0;
+  uint64_t scanned = 0;
+  uint32_t lcap = cap;
+  bool spilled = false, pool_full = false;
+  double worst_s = -DBL_MAX;
+
+  auto refresh_pool = [&]() {
+    if (n_unmasked < ef) {
+      pool_full = false;
+      return;
+    }
+    uint32_t need = ef, pos = 0;
+    for (uint32_t c = 0; c < len; c += 32) {
+      const uint32_t i = c + lane;
+      const bool um = i < len && !(L.fl[i] & kMasked);
+      const uint32_t bm = __ballot_sync(kFull, um);
+      const uint32_t cnt = __popc(bm);
+      if (need <= cnt) {
+        const bool hit = um && (uint32_t)__popc(bm & ((1u << lane) - 1u)) == need - 1;
+        pos = c + __ffs(__ballot_sync(kFull, hit)) - 1;
+        break;
+      }
+      need -= cnt;
+    }
+    pool_full = true;
+    worst_s = L.s[pos];
+    uint32_t lo = pos + 1, hi = len;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (L.s[mid] < worst_s)
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    if (lo < len) {
+      uint32_t dropped_um = 0;
+      for (uint32_t c = lo; c < len; c += 32) {
+        const uint32_t i = c + lane;
+        dropped_um += __popc(__ballot_sync(kFull, i < len && !(L.fl[i] & kMasked)));
+      }
+      n_unmasked -= dropped_um;
+      len = lo;
+    }
+  };
+
+  // insert the lanes' live (s, v, masked) — already sorted best-first across
+  // lanes in `livemask` order — into L (warp 0)
+  auto insert_sorted = [&](uint32_t livemask, bool live, double s, uint32_t v, bool msk) {
+    const uint32_t nnew = __popc(livemask);
+    if (len + nnew > lcap) {
+      if (spilled || a.spill == nullptr) __trap();  // unreachable: spill_cap >= n
+      uint8_t* sb = a.spill + size_t(b) * ((size_t(spill_cap) * 13 + 15) & ~size_t(15));
+      ListRef G{reinterpret_cast<double*>(sb), nullptr, nullptr};
+      G.id = reinterpret_cast<uint32_t*>(G.s + spill_cap);
+      G.fl = reinterpret_cast<uint8_t*>(G.id + spill_cap);
+      for (uint32_t i = lane; i < len; i += 32) {
+        G.s[i] = L.s[i];
+        G.id[i] = L.id[i];
+        G.fl[i] = L.fl[i];
+      }
+      __syncwarp();
+      L = G;
+      lcap = spill_cap;
+      spilled = true;
+    }
+    const uint32_t r = __popc(livemask & ((1u << lane) - 1u));
+    uint32_t p = 0;
+    if (live) {
+      uint32_t lo = 0, hi = len;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (better(L.s[mid], L.id[mid], s, v))
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      p = lo;
+      stage[r] = p;
+    }
+    __syncwarp();
+    const uint32_t pmin = stage[0];
+    for (int topi = (int)len; topi > (int)pmin; topi -= 32) {
+      const int i = topi - 32 + (int)lane;
+      const bool act = i >= (int)pmin;
+      double si = 0.0;
+      uint32_t idi = 0;
+      uint8_t fi = 0;
+      uint32_t cnt = 0;
+      if (act) {
+        si = L.s[i];
+        idi = L.id[i];
+        fi = L.fl[i];
+#pragma unroll
+        for (uint32_t step = 16; step >= 1; step >>= 1) {
+          const uint32_t mid = cnt + step - 1;
+          if (mid < nnew && (int)stage[mid] <= i) cnt += step;
+        }
+        if (cnt == 31 && nnew == 32 && (int)stage[31] <= i) cnt = 32;
+      }
+      __syncwarp();
+      if (act) {
+        L.s[i + cnt] = si;
+        L.id[i + cnt] = idi;
+        L.fl[i + cnt] = fi;
+      }
+      __syncwarp();
+    }
+    if (live) {
+      L.s[p + r] = s;
+      L.id[p + r] = v;
+      L.fl[p + r] = msk ? kMasked : 0;
+    }
+    __syncwarp();
+    len += nnew;
+    n_unmasked += __popc(__ballot_sync(kFull, live && !msk));
+    if (pmin < cursor) cursor = pmin;
+    refresh_pool();
+    __syncwarp();
+  };
+
+  // choose up to kCB frontier candidates (in order), keeping packets that
+  // are still among them and assigning free slots to the rest (warp 0)
+  auto select = [&]() {
+    uint32_t tops = kSentinel, ntop = 0;
+    for (uint32_t c = cursor; c < len && ntop < kCB; c += 32) {
+      const uint32_t i = c + lane;
+      const bool un = i < len && !(L.fl[i] & kExpanded);
+      const uint32_t bm = __ballot_sync(kFull, un);
+      const uint32_t r = ntop + __popc(bm & ((1u << lane) - 1u));
+      const uint32_t id = un ? L.id[i] : kSentinel;
+      // lane r of `tops` receives the r-th unexpanded id
+      for (uint32_t q = bm; q; q &= q - 1) {
+        const uint32_t src = __ffs(q) - 1;
+        const uint32_t rr = ntop + __popc(bm & ((1u << src) - 1u));
+        const uint32_t vid = __shfl_sync(kFull, id, src);
+        if (lane == rr) tops = vid;
+      }
+      (void)r;
+      ntop = min(kCB, ntop + (uint32_t)__popc(bm));
+    }
+    // keep slots whose tag is a current top; free others
+    const uint32_t tag = lane < kCP ? pk_tag[lane] : kSentinel;
+    bool keep = false;
+    for (uint32_t t = 0; t < ntop; ++t) keep |= (tag == __shfl_sync(kFull, tops, t));
+    if (lane < kCP && !keep) pk_tag[lane] = kSentinel;
+    __syncwarp();
+    uint32_t freemask = __ballot_sync(kFull, lane < kCP && !keep);
+    uint32_t nc = 0;
+    for (uint32_t t = 0; t < ntop; ++t) {
+      const uint32_t id = __shfl_sync(kFull, tops, t);
+      const bool has = __ballot_sync(kFull, lane < kCP && tag == id && keep) != 0;
+      if (!has) {
+        const uint32_t sl = __ffs(freemask) - 1;
+        freemask &= freemask - 1;
+        if (lane == 0) {
+          pk_tag[sl] = id;
+          cand[nc] = id;
+          slotof[nc] = sl;
+        }
+        ++nc;
+      }
+    }
+    if (lane == 0) ctrl[0] = nc;
+  };
+
+  if (warp == 0) {
+    // entry (:379-384)
+    const uint32_t entry = (uint32_t)g.entry;
+    double s0 = score_lanes(1u, lane == 0, entry);
+    s0 = __shfl_sync(kFull, s0, 0);
+    const bool m0 = masked_id(entry);
+    if (lane == 0) {
+      vis[entry >> 5] |= 1u << (entry & 31);
+      L.s[0] = s0;
+      L.id[0] = entry;
+      L.fl[0] = m0 ? kMasked : 0;
+      ctrl[1] = 0;
+    }
+    __syncwarp();
+    len = 1;
+    n_unmasked = m0 ? 0 : 1;
+    scanned = 1;
+    refresh_pool();
+    select();
+  }
+  __syncthreads();
+
+  for (;;) {
+    // ---- (A) pre-expand candidates into packets, all warps ----
+    const uint32_t nc = ctrl[0];
+    for (uint32_t ci = warp; ci < nc; ci += kCW) {
+      const uint32_t c = cand[ci], sl = slotof[ci];
+      const uint32_t v = lane < M ? __ldg(adj + size_t(c) * M + lane) : kSentinel;
+      const bool valid = v != kSentinel;
+      const uint32_t grp = __match_any_sync(kFull, v);
+      const bool first = (uint32_t)(__ffs(grp) - 1) == lane;
+      const bool isnew = valid && first && !visited(v);
+      const uint32_t newmask = __ballot_sync(kFull, isnew);
+      double s = -DBL_MAX;
+      if (newmask) s = score_lanes(newmask, isnew, v);
+      double ks = isnew ? s : -DBL_MAX;
+      uint32_t kid = isnew ? v : kSentinel, kfl = 0;
+      warp_sort32(ks, kid, kfl, lane);
+      const uint32_t cnt = __popc(newmask);
+      if (lane < cnt) {
+        pk_id[sl * 32 + lane] = kid;
+        pk_s[sl * 32 + lane] = ks;
+        // the likely next frontier tops: their adjacency rows go to L2 now
+        if ((M * 4) % 16 == 0) bulk_prefetch_l2(adj + size_t(kid) * M, M * 4);
+      }
+      if (lane == 0) pk_cnt[sl] = cnt;
+    }
+    __syncthreads();
+    // ---- (B) commit in reference order, warp 0 ----
+    if (warp == 0) {
+      bool done = false;
+      for (;;) {
+        uint32_t top = len;
+        for (uint32_t c = cursor; c < len; c += 32) {
+          const uint32_t i = c + lane;
+          const uint32_t bm = __ballot_sync(kFull, i < len && !(L.fl[i] & kExpanded));
+          if (bm) {
+            top = c + __ffs(bm) - 1;
+            break;
+          }
+        }
+        cursor = top;
+        if (top >= len || (pool_full && L.s[top] < worst_s)) {
+          done = true;  // frontier exhausted / :390
+          break;
+        }
+        const uint32_t u = L.id[top];
+        const uint32_t hit = __ballot_sync(kFull, lane < kCP && pk_tag[lane] == u);
+        if (!hit) break;  // next round pre-expands it
+        const uint32_t sl = __ffs(hit) - 1;
+        __syncwarp();
+        if (lane == 0) {
+          L.fl[top] |= kExpanded;
+          pk_tag[sl] = kSentinel;
+        }
+        ++expanded;
+        const uint32_t cnt = pk_cnt[sl];
+        const uint32_t v = lane < cnt ? pk_id[sl * 32 + lane] : kSentinel;
+        const double s = lane < cnt ? pk_s[sl * 32 + lane] : -DBL_MAX;
+        const bool isnew = lane < cnt && !visited(v);
+        __syncwarp();
+        if (isnew) atomicOr(&vis[v >> 5], 1u << (v & 31));
+        const uint32_t newmask = __ballot_sync(kFull, isnew);
+        scanned += __popc(newmask);
+        const bool msk = isnew && masked_id(v);
+        const bool live = isnew && !(pool_full && s < worst_s);
+        const uint32_t livemask = __ballot_sync(kFull, live);
+        if (livemask) insert_sorted(livemask, live, s, v, msk);
+      }
+      if (done) {
+        if (lane == 0) ctrl[1] = 1;
+      } else {
+        select();
+      }
+    }
+    __syncthreads();
+    if (ctrl[1]) break;
+  }
+
+  if (warp != 0) return;
+  // ---- result (:402-410) ----
+  uint32_t taken = 0;
+  for (uint32_t c = 0; c < len && taken < k; c += 32) {
+    const uint32_t i = c + lane;
+    const bool um = i < len && !(L.fl[i] & kMasked);
+    const uint32_t bm = __ballot_sync(kFull, um);
+    const uint32_t r = taken + __popc(bm & ((1u << lane) - 1u));
+    if (um && r < k) {
+      a.ids[size_t(b) * k + r] = L.id[i];
+      a.scores[size_t(b) * k + r] = (float)L.s[i];
+      if (a.scores64) a.scores64[size_t(b) * k + r] = L.s[i];
+    }
+    taken += __popc(bm);
+  }
+  const uint32_t take = taken < k ? taken : k;
+  for (uint32_t r = take + lane; r < k; r += 32) {
+    a.ids[size_t(b) * k + r] = kSentinel;
+    a.scores[size_t(b) * k + r] = __int_as_float(0x7fc00000);
+    if (a.scores64) a.scores64[size_t(b) * k + r] = __longlong_as_double(0x7ff8000000000000ll);
+  }
+  if (lane == 0) {
+    a.n_out[b] = take;
+    a.scanned[b] = scanned;
+    a.truncated[b] = take < k;
+    if (a.expanded) a.expanded[b] = expanded;
+  }
+}
+
 bool tiled_dim(uint32_t d) { return d == 128 || d == 64 || d == 32 || d == 16 || d == 8; }
 
 struct Plan {
@@ -482,15 +872,77 @@ void launch_d(ra_ctx* ctx, const SearchArgs& a, const Plan& p, uint32_t spill_ca
 }  // namespace
 
 size_t search_scratch_bytes(const ra_ctx* ctx, uint32_t B, uint32_t max_n, uint32_t d) {
+  // sized for the warp-per-query fallback, which never needs less than v3
   const Plan p = plan(ctx, B, max_n, d);
-  size_t bytes = 0;
-  if (p.cap < max_n) bytes += size_t(B) * ((size_t(max_n) * 13 + 15) & ~size_t(15)) + 256;
-  if (!p.vis_smem) bytes += size_t(B) * p.vis_words * 4 + 256;
+  size_t bytes = size_t(B) * ((size_t(max_n) * 13 + 15) & ~size_t(15)) + 256;
+  (void)p;
+  bytes += size_t(B) * ((max_n + 31) / 32) * 4 + 256;  // HBM visited bitsets
   return bytes;
+}
+
+struct CtaPlan {
+  bool ok;
+  uint32_t cap, vis_smem, vis_words;
+  size_t bytes;
+};
+
+template <int D>
+CtaPlan cta_plan(const ra_ctx* ctx, uint32_t max_n) {
+  CtaPlan p{};
+  const size_t budget = ctx->smem_optin ? ctx->smem_optin : 227 * 1024;
+  p.vis_words = (max_n + 31) / 32;
+  CtaLayout<D> lay{0, 0, p.vis_words, 0};
+  const size_t fixed = lay.list_off();
+  const size_t vis_bytes = (size_t(p.vis_words) * 4 + 15) & ~size_t(15);
+  p.vis_smem = fixed + vis_bytes + 13 * 512 + 16 <= budget;
+  const size_t rest = budget - fixed - (p.vis_smem ? vis_bytes : 0) - 16;
+  if (fixed + 13 * 128 > budget) return p;
+  uint32_t cap = uint32_t(std::min<size_t>(rest / 13, 8192));
+  cap = std::min<uint32_t>(cap, std::max<uint32_t>(max_n, 64));
+  p.cap = std::max<uint32_t>(cap & ~31u, 32);
+  lay.cap = p.cap;
+  lay.vis_smem = p.vis_smem;
+  p.bytes = lay.bytes();
+  p.ok = p.bytes <= budget;
+  return p;
+}
+
+template <int D>
+bool try_launch_cta(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* scratch) {
+  const CtaPlan p = cta_plan<D>(ctx, max_n);
+  if (!p.ok) return false;
+  SearchArgs s = a;
+  uint8_t* cur = scratch;
+  s.spill = nullptr;
+  s.vis_global = nullptr;
+  if (p.cap < max_n) {
+    s.spill = cur;
+    cur += (size_t(a.B) * ((size_t(max_n) * 13 + 15) & ~size_t(15)) + 255) & ~size_t(255);
+  }
+  if (!p.vis_smem) s.vis_global = reinterpret_cast<uint32_t*>(cur);
+  CtaLayout<D> lay{uint32_t(D), p.cap, p.vis_words, p.vis_smem};
+  auto kern = k_graph_search_cta<D>;
+  RA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.bytes));
+  kern<<<a.B, kCW * 32, p.bytes, ctx->stream>>>(s, lay, max_n);
+  RA_LAUNCH_CHECK();
+  return true;
 }
 
 void launch_graph_search(ra_ctx* ctx, SearchArgs a, uint32_t max_n, uint8_t* scratch) {
   if (a.B == 0) return;
+  // v3 (CTA per query, speculative pre-expansion) for the common shapes
+  if (a.max_M <= 32) {
+    bool done = false;
+    switch (a.d) {
+      case 128: done = try_launch_cta<128>(ctx, a, max_n, scratch); break;
+      case 64: done = try_launch_cta<64>(ctx, a, max_n, scratch); break;
+      case 32: done = try_launch_cta<32>(ctx, a, max_n, scratch); break;
+      case 16: done = try_launch_cta<16>(ctx, a, max_n, scratch); break;
+      case 8: done = try_launch_cta<8>(ctx, a, max_n, scratch); break;
+      default: break;
+    }
+    if (done) return;
+  }
   const Plan p = plan(ctx, a.B, max_n, a.d);
   uint8_t* cur = scratch;
   a.spill = nullptr;
