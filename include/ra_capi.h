@@ -191,6 +191,9 @@ ra_status ra_engine_last_stats(ra_engine* e, uint64_t* total_scanned,
 /* CUDA-event durations of the last step's search kernel and of its
  * attention + merge kernels (recorded on the ctx stream). Synchronizes. */
 ra_status ra_engine_last_timing(ra_engine* e, float* search_ms, float* attention_ms);
+/* Profiling aid: search-kernel counters of the last step summed over heads:
+ * {rounds, cycles pre-expanding, cycles committing, commits}. */
+ra_status ra_engine_debug_counters(ra_engine* e, uint64_t* out4);
 
 #ifdef __cplusplus
 }

@@ -91,6 +91,7 @@ _SIGS = {
     "ra_engine_step_host": (C.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "ra_engine_last_stats": (C.c_int, [c_vp, c_u64p, c_u64p]),
     "ra_engine_last_timing": (C.c_int, [c_vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+    "ra_engine_debug_counters": (C.c_int, [c_vp, c_u64p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -523,6 +523,12 @@ class Engine:
         _check(lib.ra_engine_last_timing(self.h, C.byref(a), C.byref(b)))
         return float(a.value), float(b.value)
 
+    def debug_counters(self):
+        """{rounds, cycles_pre_expand, cycles_commit, commits} of the last step."""
+        out = (C.c_uint64 * 4)()
+        _check(lib.ra_engine_debug_counters(self.h, out))
+        return dict(zip(("rounds", "cycles_pre_expand", "cycles_commit", "commits"), list(out)))
+
     def last_stats(self):
         s, e = C.c_uint64(), C.c_uint64()
         _check(lib.ra_engine_last_stats(self.h, C.byref(s), C.byref(e)))

@@ -404,6 +404,7 @@ struct ra_engine {
   DevBuf<uint64_t> scanned;
   DevBuf<uint8_t> truncated;
   DevBuf<uint8_t> search_scratch;
+  DevBuf<uint64_t> dbg;
   uint32_t max_n = 0, max_M = 0;
   // events bracketing the search kernel and the attention kernels of the
   // last step, recorded on the ctx stream (ra_engine_last_timing)
@@ -501,6 +502,8 @@ ra_status ra_engine_create(ra_ctx* ctx, ra_kv* const* groups, uint32_t n_groups,
     e->truncated.alloc(H);
     e->expanded.alloc(H);
     e->o_empty.alloc(H);
+    e->dbg.alloc(size_t(H) * 4);
+    RA_CUDA(cudaMemset(e->dbg.p, 0, size_t(H) * 32));
     e->flag.alloc(1);
     for (auto* b : {&e->ow, &e->oo, &e->out}) b->alloc(size_t(H) * d);
     for (auto* b : {&e->zw, &e->sw, &e->zo, &e->so}) b->alloc(H);
@@ -567,6 +570,7 @@ void engine_enqueue(ra_engine* e, const float* q_dev) {
     sa.scanned = e->scanned.p;
     sa.truncated = e->truncated.p;
     sa.expanded = e->expanded.p;
+    sa.dbg = e->dbg.p;
     launch_graph_search(ctx, sa, e->max_n, e->search_scratch.p);
   } else {
     RA_CUDA(cudaMemsetAsync(e->n_out.p, 0, H * 4, s));
@@ -647,6 +651,20 @@ ra_status ra_engine_last_timing(ra_engine* e, float* search_ms, float* attention
     RA_CUDA(cudaEventSynchronize(e->ev[2]));
     if (search_ms) RA_CUDA(cudaEventElapsedTime(search_ms, e->ev[0], e->ev[1]));
     if (attention_ms) RA_CUDA(cudaEventElapsedTime(attention_ms, e->ev[1], e->ev[2]));
+  });
+}
+
+// Search-kernel counters of the last step summed over heads: rounds,
+// cycles in pre-expansion, cycles in commit, commits (profiling aid).
+ra_status ra_engine_debug_counters(ra_engine* e, uint64_t* out4) {
+  return guard([&] {
+    if (!e) invalid("null engine");
+    DeviceGuard dg(e->ctx->device);
+    std::vector<uint64_t> h(size_t(e->H) * 4);
+    RA_CUDA(cudaMemcpyAsync(h.data(), e->dbg.p, h.size() * 8, cudaMemcpyDeviceToHost, e->ctx->stream));
+    RA_CUDA(cudaStreamSynchronize(e->ctx->stream));
+    for (int j = 0; j < 4; ++j) out4[j] = 0;
+    for (size_t i = 0; i < h.size(); ++i) out4[i % 4] += h[i];
   });
 }
 

@@ -173,6 +173,7 @@ struct SearchArgs {
   uint64_t* scanned;          // [B]
   uint8_t* truncated;         // [B]
   uint32_t* expanded;         // optional [B]
+  uint64_t* dbg;              // optional [B][4]: rounds, cycles A, cycles B, commits
   // HBM spill area used when a query outgrows its shared-memory list
   // (per query: max_n entries of f64 + u32 + u8) and the visited bitset
   // when it does not fit shared memory (per query: ceil(max_n/32) words).

@@ -444,6 +444,7 @@ __global__ void k_mask_bitset(const uint32_t* mask, uint64_t mask_n, uint32_t* b
 constexpr uint32_t kCW = 4;   // warps per CTA
 constexpr uint32_t kCB = 8;   // candidates pre-expanded per round
 constexpr uint32_t kCP = 16;  // packet slots
+constexpr uint32_t kFC = 16;  // list chunks (x32 entries) held in registers by the commit warp
 
 template <int D>
 struct CtaLayout {
@@ -456,7 +457,7 @@ struct CtaLayout {
   // packets: tag u32[P], cnt u32[P], cand u32[B], slotof u32[B], ctrl u32[8],
   // stage u32[32], ids u32[P][32], s f64[P][32]
   __host__ __device__ static size_t pk_bytes() {
-    return ((size_t(kCP) * 8 + kCB * 8 + 32 + 128 + 15) & ~size_t(15)) + size_t(kCP) * 32 * 12;
+    return ((size_t(kCP) * 12 + kCB * 8 + 32 + 128 + 15) & ~size_t(15)) + size_t(kCP) * 32 * 12;
   }
   __host__ __device__ size_t list_off() const { return pk_off() + pk_bytes(); }
   __host__ __device__ size_t vis_off() const {
@@ -490,8 +491,9 @@ __global__ void __launch_bounds__(kCW * 32, 1)
   uint32_t* slotof = cand + kCB;
   uint32_t* ctrl = slotof + kCB;  // [0] = #candidates, [1] = done
   uint32_t* stage = ctrl + 8;     // 32 insertion points (warp 0)
+  uint32_t* pk_mbits = stage + 32;  // [kCP] masked-bit per packet entry
   uint32_t* pk_id = reinterpret_cast<uint32_t*>(
-      pk + ((size_t(kCP) * 8 + kCB * 8 + 32 + 128 + 15) & ~size_t(15)));
+      pk + ((size_t(kCP) * 12 + kCB * 8 + 32 + 128 + 15) & ~size_t(15)));
   double* pk_s = reinterpret_cast<double*>(pk_id + kCP * 32);
   ListRef L{reinterpret_cast<double*>(smem + lay.list_off()), nullptr, nullptr};
   L.id = reinterpret_cast<uint32_t*>(L.s + cap);
@@ -645,6 +647,125 @@ __global__ void __launch_bounds__(kCW * 32, 1)
     __syncwarp();
   };
 
+  // ---- ILP fast path (list window <= kFC*32 entries, shared memory) ----
+  // nth set bit (1-based n) of a uniform mask
+  auto nth_set = [&](uint32_t m, uint32_t n) -> uint32_t {
+    const bool hit = ((m >> lane) & 1u) && (uint32_t)__popc(m & ((1u << lane) - 1u)) == n - 1;
+    return __ffs(__ballot_sync(kFull, hit)) - 1;
+  };
+  auto refresh_fast = [&]() {
+    if (n_unmasked < ef) {
+      pool_full = false;
+      return;
+    }
+    double rs[kFC];
+    uint32_t um[kFC];
+#pragma unroll
+    for (uint32_t c = 0; c < kFC; ++c) {
+      const uint32_t i = c * 32 + lane;
+      const bool in = i < len;
+      rs[c] = in ? L.s[i] : -DBL_MAX;
+      um[c] = __ballot_sync(kFull, in && !(L.fl[in ? i : 0] & kMasked));
+    }
+    uint32_t need = ef, pos = kSentinel;
+#pragma unroll
+    for (uint32_t c = 0; c < kFC; ++c) {
+      const uint32_t cnt = __popc(um[c]);
+      if (pos == kSentinel) {
+        if (need <= cnt)
+          pos = c * 32 + nth_set(um[c], need);
+        else
+          need -= cnt;
+      }
+    }
+    pool_full = true;
+    worst_s = L.s[pos];
+    uint32_t lo = len;
+#pragma unroll
+    for (uint32_t c = 0; c < kFC; ++c) {
+      const uint32_t i = c * 32 + lane;
+      const uint32_t m = __ballot_sync(kFull, i < len && i > pos && rs[c] < worst_s);
+      if (lo == len && m) lo = c * 32 + __ffs(m) - 1;
+    }
+    if (lo < len) {
+      uint32_t dropped = 0;
+#pragma unroll
+      for (uint32_t c = 0; c < kFC; ++c) {
+        const uint32_t base = c * 32;
+        uint32_t keepmask = 0;
+        if (lo > base) keepmask = lo - base >= 32 ? kFull : ((1u << (lo - base)) - 1u);
+        dropped += __popc(um[c] & ~keepmask);
+      }
+      n_unmasked -= dropped;
+      len = lo;
+    }
+  };
+  auto insert_fast = [&](uint32_t livemask, bool live, double s, uint32_t v, bool msk) {
+    const uint32_t nnew = __popc(livemask);
+    const uint32_t r = __popc(livemask & ((1u << lane) - 1u));
+    double rs[kFC];
+    uint32_t ri[kFC], rf[kFC];
+#pragma unroll
+    for (uint32_t c = 0; c < kFC; ++c) {
+      const uint32_t i = c * 32 + lane;
+      const bool in = i < len;
+      rs[c] = in ? L.s[i] : -DBL_MAX;
+      ri[c] = in ? L.id[i] : kSentinel;
+      rf[c] = in ? L.fl[i] : 0u;
+    }
+    // insertion point of each live entry = #list entries better than it
+    uint32_t p = 0;
+    for (uint32_t q = livemask; q; q &= q - 1) {
+      const uint32_t j = __ffs(q) - 1;
+      const double xs = __shfl_sync(kFull, s, j);
+      const uint32_t xi = __shfl_sync(kFull, v, j);
+      uint32_t cnt = 0;
+#pragma unroll
+      for (uint32_t c = 0; c < kFC; ++c)
+        cnt += __popc(__ballot_sync(kFull, c * 32 + lane < len && better(rs[c], ri[c], xs, xi)));
+      if (lane == j) p = cnt;
+    }
+    if (live) stage[r] = p;
+    __syncwarp();
+    const uint32_t pr = lane < nnew ? stage[lane] : kSentinel;  // non-decreasing
+    const uint32_t pmin = __shfl_sync(kFull, pr, 0);
+    uint32_t sh[kFC];
+#pragma unroll
+    for (uint32_t c = 0; c < kFC; ++c) {
+      const uint32_t i = c * 32 + lane;
+      uint32_t cnt = 0;
+#pragma unroll
+      for (uint32_t step = 16; step >= 1; step >>= 1) {
+        const uint32_t pm = __shfl_sync(kFull, pr, (cnt + step - 1) & 31);
+        if (cnt + step - 1 < nnew && pm <= i) cnt += step;
+      }
+      const uint32_t p31 = __shfl_sync(kFull, pr, 31);
+      if (cnt == 31 && nnew == 32 && p31 <= i) cnt = 32;
+      sh[c] = cnt;
+    }
+    __syncwarp();
+#pragma unroll
+    for (uint32_t c = 0; c < kFC; ++c) {
+      const uint32_t i = c * 32 + lane;
+      if (i < len && i >= pmin) {
+        L.s[i + sh[c]] = rs[c];
+        L.id[i + sh[c]] = ri[c];
+        L.fl[i + sh[c]] = (uint8_t)rf[c];
+      }
+    }
+    if (live) {
+      L.s[p + r] = s;
+      L.id[p + r] = v;
+      L.fl[p + r] = msk ? kMasked : 0;
+    }
+    __syncwarp();
+    len += nnew;
+    n_unmasked += __popc(__ballot_sync(kFull, live && !msk));
+    if (pmin < cursor) cursor = pmin;
+    refresh_fast();
+    __syncwarp();
+  };
+
   // choose up to kCB frontier candidates (in order), keeping packets that
   // are still among them and assigning free slots to the rest (warp 0)
   auto select = [&]() {
@@ -690,6 +811,8 @@ __global__ void __launch_bounds__(kCW * 32, 1)
     if (lane == 0) ctrl[0] = nc;
   };
 
+  uint64_t cyc_a = 0, cyc_b = 0, t_mark = clock64();
+  uint32_t rounds = 0;
   if (warp == 0) {
     // entry (:379-384)
     const uint32_t entry = (uint32_t)g.entry;
@@ -715,6 +838,7 @@ __global__ void __launch_bounds__(kCW * 32, 1)
   for (;;) {
     // ---- (A) pre-expand candidates into packets, all warps ----
     const uint32_t nc = ctrl[0];
+    ++rounds;
     for (uint32_t ci = warp; ci < nc; ci += kCW) {
       const uint32_t c = cand[ci], sl = slotof[ci];
       const uint32_t v = lane < M ? __ldg(adj + size_t(c) * M + lane) : kSentinel;
@@ -735,9 +859,18 @@ __global__ void __launch_bounds__(kCW * 32, 1)
         // the likely next frontier tops: their adjacency rows go to L2 now
         if ((M * 4) % 16 == 0) bulk_prefetch_l2(adj + size_t(kid) * M, M * 4);
       }
-      if (lane == 0) pk_cnt[sl] = cnt;
+      const uint32_t mb = __ballot_sync(kFull, lane < cnt && masked_id(kid));
+      if (lane == 0) {
+        pk_cnt[sl] = cnt;
+        pk_mbits[sl] = mb;
+      }
     }
     __syncthreads();
+    {
+      const uint64_t t = clock64();
+      cyc_a += t - t_mark;
+      t_mark = t;
+    }
     // ---- (B) commit in reference order, warp 0 ----
     if (warp == 0) {
       bool done = false;
@@ -774,10 +907,15 @@ __global__ void __launch_bounds__(kCW * 32, 1)
         if (isnew) atomicOr(&vis[v >> 5], 1u << (v & 31));
         const uint32_t newmask = __ballot_sync(kFull, isnew);
         scanned += __popc(newmask);
-        const bool msk = isnew && masked_id(v);
+        const bool msk = isnew && ((pk_mbits[sl] >> lane) & 1u);
         const bool live = isnew && !(pool_full && s < worst_s);
         const uint32_t livemask = __ballot_sync(kFull, live);
-        if (livemask) insert_sorted(livemask, live, s, v, msk);
+        if (livemask) {
+          if (!spilled && len + __popc(livemask) <= kFC * 32)
+            insert_fast(livemask, live, s, v, msk);
+          else
+            insert_sorted(livemask, live, s, v, msk);
+        }
       }
       if (done) {
         if (lane == 0) ctrl[1] = 1;
@@ -786,10 +924,21 @@ __global__ void __launch_bounds__(kCW * 32, 1)
       }
     }
     __syncthreads();
+    {
+      const uint64_t t = clock64();
+      cyc_b += t - t_mark;
+      t_mark = t;
+    }
     if (ctrl[1]) break;
   }
 
   if (warp != 0) return;
+  if (a.dbg && lane == 0) {
+    a.dbg[size_t(b) * 4 + 0] = rounds;
+    a.dbg[size_t(b) * 4 + 1] = cyc_a;
+    a.dbg[size_t(b) * 4 + 2] = cyc_b;
+    a.dbg[size_t(b) * 4 + 3] = expanded;
+  }
   // ---- result (:402-410) ----
   uint32_t taken = 0;
   for (uint32_t c = 0; c < len && taken < k; c += 32) {

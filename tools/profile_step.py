@@ -44,6 +44,8 @@ def main():
     s, e = eng.last_stats()
     print(f"steps={a.steps} heads={len(graphs)} scanned/head={s / len(graphs):.1f} "
           f"expanded/head={e / len(graphs):.1f} timing={eng.last_timing()}")
+    dc = eng.debug_counters()
+    print({k: v / len(graphs) for k, v in dc.items()})
 
 
 if __name__ == "__main__":
