@@ -429,43 +429,67 @@ __global__ void k_mask_bitset(const uint32_t* mask, uint64_t mask_n, uint32_t* b
 }
 
 // ---------------------------------------------------------------------------
-// K6 v3: one CTA (4 warps) per query, speculative parallel pre-expansion.
+// K6 v4: one CTA (4 warps) per query, speculative parallel pre-expansion.
 //
 // Round r: (A) every warp pre-expands frontier candidates chosen by warp 0 —
 // adjacency row, visited filter, TMA row copies, exact in-order chains — into
-// a "packet" {neighbour ids, exact scores} sorted best-first; (B) warp 0
-// commits packets strictly in the reference's pop order: top = best
-// unexpanded entry, stop rule (:390), re-filter the packet against the
-// visited set as it is NOW (earlier commits may have visited some), mark,
-// count, offer. The round ends at the first top without a packet; its
-// candidates are packeted next round. Packets are pure functions of
-// (query, node), so only the committed expansion SET matters and the result
-// is bit-identical to the reference (same proof as v2).
+// a "packet" {neighbour ids, exact scores, masked bits}; (B) warp 0 commits
+// packets strictly in the reference's pop order. The round ends at the
+// first top without a packet; it is pre-expanded next round. Packets are
+// pure functions of (query, node), so only the committed expansion SET
+// matters and the result is bit-identical to the reference.
+//
+// Commit-side state needs no sorting (the v2/v3 sorted list cost ~800
+// dependent instructions per pop):
+//   F = unexpanded visited nodes with score >= thr (unsorted); the reference's
+//       frontier top (:387) is argmax_(score desc, id asc) F;
+//   U = unmasked visited nodes with score >= thr (unsorted) = the pool's
+//       candidates; pool full <=> #unmasked visited >= ef, and
+//       top.score < pool.worst (:390)  <=>  #{u in U : u.score > top.score} >= ef,
+//       a count (independent ballots), exact as long as thr <= pool worst;
+//   thr = the exact pool worst at the last compaction (U sorted, cut to ef
+//       + ties) — monotone, so dropping nodes below it never changes a pop
+//       or the pool.
+// Arrays live in shared memory and migrate to the query's HBM spill slot if
+// they outgrow it, so no input can exceed capacity.
 constexpr uint32_t kCW = 4;   // warps per CTA
-constexpr uint32_t kCB = 8;   // candidates pre-expanded per round
+constexpr uint32_t kCB = 6;   // candidates pre-expanded per round
 constexpr uint32_t kCP = 16;  // packet slots
-constexpr uint32_t kFC = 16;  // list chunks (x32 entries) held in registers by the commit warp
+constexpr uint32_t kUSlack = 96;  // U grows to ef + slack before compaction
 
 template <int D>
 struct CtaLayout {
-  uint32_t d_pad, cap, vis_words, vis_smem;
-  static constexpr uint32_t kRow = D + 4;  // padded row stride (floats)
+  uint32_t d_pad, cap, vis_words, vis_smem;  // cap = capacity of F and of U
+  static constexpr uint32_t kRow = D + 4;     // padded TMA row stride (floats)
   __host__ __device__ static size_t tiles_off() { return 64 + size_t(D) * 8; }
   __host__ __device__ static size_t pk_off() {
     return tiles_off() + size_t(kCW) * 32 * kRow * 4;
   }
-  // packets: tag u32[P], cnt u32[P], cand u32[B], slotof u32[B], ctrl u32[8],
-  // stage u32[32], ids u32[P][32], s f64[P][32]
-  __host__ __device__ static size_t pk_bytes() {
-    return ((size_t(kCP) * 12 + kCB * 8 + 32 + 128 + 15) & ~size_t(15)) + size_t(kCP) * 32 * 12;
+  // packets: tag u32[P], cnt u32[P], mbits u32[P], cand u32[B], slotof u32[B],
+  // ctrl u32[8] | ids u32[P][32] | scores f64[P][32]
+  __host__ __device__ static size_t pk_hdr() {
+    return (size_t(kCP) * 12 + kCB * 8 + 32 + 15) & ~size_t(15);
   }
+  __host__ __device__ static size_t pk_bytes() { return pk_hdr() + size_t(kCP) * 32 * 12; }
   __host__ __device__ size_t list_off() const { return pk_off() + pk_bytes(); }
-  __host__ __device__ size_t vis_off() const {
-    return list_off() + ((size_t(cap) * 13 + 15) & ~size_t(15));
+  // F: s f64[cap], id u32[cap], m u8[cap] | U: s f64[cap], id u32[cap]
+  __host__ __device__ static size_t list_bytes(uint32_t c) {
+    return ((size_t(c) * 13 + 15) & ~size_t(15)) + ((size_t(c) * 12 + 15) & ~size_t(15));
   }
+  __host__ __device__ size_t vis_off() const { return list_off() + list_bytes(cap); }
   __host__ __device__ size_t bytes() const {
     return vis_off() + (vis_smem ? ((size_t(vis_words) * 4 + 15) & ~size_t(15)) : 0);
   }
+};
+
+struct FArr {
+  double* s;
+  uint32_t* id;
+  uint8_t* m;
+};
+struct UArr {
+  double* s;
+  uint32_t* id;
 };
 
 template <int D>
@@ -478,29 +502,30 @@ __global__ void __launch_bounds__(kCW * 32, 1)
   const uint32_t M = g.M, ef = g.ef, k = a.k;
   const float* __restrict__ keys = g.keys;
   const uint32_t* __restrict__ adj = g.adj;
-  const uint32_t cap = lay.cap, vis_words = lay.vis_words;
+  const uint32_t vis_words = lay.vis_words;
   constexpr uint32_t RS = CtaLayout<D>::kRow;
 
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // [kCW]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + warp;
   double* qd = reinterpret_cast<double*>(smem + 64);
   float* tile = reinterpret_cast<float*>(smem + CtaLayout<D>::tiles_off()) + size_t(warp) * 32 * RS;
   uint8_t* pk = smem + CtaLayout<D>::pk_off();
   uint32_t* pk_tag = reinterpret_cast<uint32_t*>(pk);
   uint32_t* pk_cnt = pk_tag + kCP;
-  uint32_t* cand = pk_cnt + kCP;
+  uint32_t* pk_mbits = pk_cnt + kCP;
+  uint32_t* cand = pk_mbits + kCP;
   uint32_t* slotof = cand + kCB;
   uint32_t* ctrl = slotof + kCB;  // [0] = #candidates, [1] = done
-  uint32_t* stage = ctrl + 8;     // 32 insertion points (warp 0)
-  uint32_t* pk_mbits = stage + 32;  // [kCP] masked-bit per packet entry
-  uint32_t* pk_id = reinterpret_cast<uint32_t*>(
-      pk + ((size_t(kCP) * 12 + kCB * 8 + 32 + 128 + 15) & ~size_t(15)));
+  uint32_t* pk_id = reinterpret_cast<uint32_t*>(pk + CtaLayout<D>::pk_hdr());
   double* pk_s = reinterpret_cast<double*>(pk_id + kCP * 32);
-  ListRef L{reinterpret_cast<double*>(smem + lay.list_off()), nullptr, nullptr};
-  L.id = reinterpret_cast<uint32_t*>(L.s + cap);
-  L.fl = reinterpret_cast<uint8_t*>(L.id + cap);
+  uint8_t* lists = smem + lay.list_off();
+  const uint32_t cap = lay.cap;
+  FArr F{reinterpret_cast<double*>(lists), nullptr, nullptr};
+  F.id = reinterpret_cast<uint32_t*>(F.s + cap);
+  F.m = reinterpret_cast<uint8_t*>(F.id + cap);
+  UArr U{reinterpret_cast<double*>(lists + ((size_t(cap) * 13 + 15) & ~size_t(15))), nullptr};
+  U.id = reinterpret_cast<uint32_t*>(U.s + cap);
   uint32_t* vis = lay.vis_smem ? reinterpret_cast<uint32_t*>(smem + lay.vis_off())
                                : a.vis_global + size_t(b) * vis_words;
-  uint64_t* bar = bars + warp;
   uint32_t phase = 0;
 
   if (lane == 0) mbar_init(bar);
@@ -526,267 +551,156 @@ __global__ void __launch_bounds__(kCW * 32, 1)
     return mine ? smem_dot<D>(qd, row) : -DBL_MAX;
   };
 
-  // warp-0 state (the committed search)
-  uint32_t len = 0, cursor = 0, n_unmasked = 0, expanded = 0;
-  uint64_t scanned = 0;
-  uint32_t lcap = cap;
-  bool spilled = false, pool_full = false;
-  double worst_s = -DBL_MAX;
+  // ---- commit-warp state ----
+  uint32_t nF = 0, nU = 0, capF = cap, capU = cap, expanded = 0;
+  uint64_t scanned = 0, u_total = 0;
+  double thr = -DBL_MAX;  // exact pool worst at the last compaction
+  bool spilledF = false, spilledU = false;
+  uint8_t* spill_slot = a.spill ? a.spill + size_t(b) * CtaLayout<D>::list_bytes(spill_cap) : nullptr;
 
-  auto refresh_pool = [&]() {
-    if (n_unmasked < ef) {
-      pool_full = false;
-      return;
-    }
-    uint32_t need = ef, pos = 0;
-    for (uint32_t c = 0; c < len; c += 32) {
-      const uint32_t i = c + lane;
-      const bool um = i < len && !(L.fl[i] & kMasked);
-      const uint32_t bm = __ballot_sync(kFull, um);
-      const uint32_t cnt = __popc(bm);
-      if (need <= cnt) {
-        const bool hit = um && (uint32_t)__popc(bm & ((1u << lane) - 1u)) == need - 1;
-        pos = c + __ffs(__ballot_sync(kFull, hit)) - 1;
-        break;
-      }
-      need -= cnt;
-    }
-    pool_full = true;
-    worst_s = L.s[pos];
-    uint32_t lo = pos + 1, hi = len;
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (L.s[mid] < worst_s)
-        hi = mid;
-      else
-        lo = mid + 1;
-    }
-    if (lo < len) {
-      uint32_t dropped_um = 0;
-      for (uint32_t c = lo; c < len; c += 32) {
-        const uint32_t i = c + lane;
-        dropped_um += __popc(__ballot_sync(kFull, i < len && !(L.fl[i] & kMasked)));
-      }
-      n_unmasked -= dropped_um;
-      len = lo;
-    }
+  auto spill_F = [&]() {
+    if (spilledF || !spill_slot) __trap();  // unreachable: spill_cap >= n
+    FArr G{reinterpret_cast<double*>(spill_slot), nullptr, nullptr};
+    G.id = reinterpret_cast<uint32_t*>(G.s + spill_cap);
+    G.m = reinterpret_cast<uint8_t*>(G.id + spill_cap);
+    for (uint32_t i = lane; i < nF; i += 32) G.s[i] = F.s[i], G.id[i] = F.id[i], G.m[i] = F.m[i];
+    __syncwarp();
+    F = G;
+    capF = spill_cap;
+    spilledF = true;
+  };
+  auto spill_U = [&]() {
+    if (spilledU || !spill_slot) __trap();
+    UArr G{reinterpret_cast<double*>(spill_slot + ((size_t(spill_cap) * 13 + 15) & ~size_t(15))),
+           nullptr};
+    G.id = reinterpret_cast<uint32_t*>(G.s + spill_cap);
+    for (uint32_t i = lane; i < nU; i += 32) G.s[i] = U.s[i], G.id[i] = U.id[i];
+    __syncwarp();
+    U = G;
+    capU = spill_cap;
+    spilledU = true;
   };
 
-  // insert the lanes' live (s, v, masked) — already sorted best-first across
-  // lanes in `livemask` order — into L (warp 0)
-  auto insert_sorted = [&](uint32_t livemask, bool live, double s, uint32_t v, bool msk) {
-    const uint32_t nnew = __popc(livemask);
-    if (len + nnew > lcap) {
-      if (spilled || a.spill == nullptr) __trap();  // unreachable: spill_cap >= n
-      uint8_t* sb = a.spill + size_t(b) * ((size_t(spill_cap) * 13 + 15) & ~size_t(15));
-      ListRef G{reinterpret_cast<double*>(sb), nullptr, nullptr};
-      G.id = reinterpret_cast<uint32_t*>(G.s + spill_cap);
-      G.fl = reinterpret_cast<uint8_t*>(G.id + spill_cap);
-      for (uint32_t i = lane; i < len; i += 32) {
-        G.s[i] = L.s[i];
-        G.id[i] = L.id[i];
-        G.fl[i] = L.fl[i];
-      }
-      __syncwarp();
-      L = G;
-      lcap = spill_cap;
-      spilled = true;
-    }
-    const uint32_t r = __popc(livemask & ((1u << lane) - 1u));
-    uint32_t p = 0;
-    if (live) {
-      uint32_t lo = 0, hi = len;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (better(L.s[mid], L.id[mid], s, v))
-          lo = mid + 1;
-        else
-          hi = mid;
-      }
-      p = lo;
-      stage[r] = p;
-    }
+  // sort U[0, nU) best-first (bitonic over the next power of two)
+  auto sort_U = [&]() {
+    uint32_t p2 = 32;
+    while (p2 < nU) p2 <<= 1;
+    if (p2 > capU) spill_U();
+    for (uint32_t i = nU + lane; i < p2; i += 32) U.s[i] = -DBL_MAX, U.id[i] = kSentinel;
     __syncwarp();
-    const uint32_t pmin = stage[0];
-    for (int topi = (int)len; topi > (int)pmin; topi -= 32) {
-      const int i = topi - 32 + (int)lane;
-      const bool act = i >= (int)pmin;
-      double si = 0.0;
-      uint32_t idi = 0;
-      uint8_t fi = 0;
-      uint32_t cnt = 0;
-      if (act) {
-        si = L.s[i];
-        idi = L.id[i];
-        fi = L.fl[i];
-#pragma unroll
-        for (uint32_t step = 16; step >= 1; step >>= 1) {
-          const uint32_t mid = cnt + step - 1;
-          if (mid < nnew && (int)stage[mid] <= i) cnt += step;
+    for (uint32_t kk = 2; kk <= p2; kk <<= 1) {
+      for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+        for (uint32_t i = lane; i < p2; i += 32) {
+          const uint32_t pj = i ^ j;
+          if (pj > i) {
+            const bool desc = (i & kk) == 0;
+            const double si = U.s[i], sp = U.s[pj];
+            const uint32_t ii = U.id[i], ip = U.id[pj];
+            if (desc ? better(sp, ip, si, ii) : better(si, ii, sp, ip)) {
+              U.s[i] = sp, U.s[pj] = si;
+              U.id[i] = ip, U.id[pj] = ii;
+            }
+          }
         }
-        if (cnt == 31 && nnew == 32 && (int)stage[31] <= i) cnt = 32;
+        __syncwarp();
       }
-      __syncwarp();
-      if (act) {
-        L.s[i + cnt] = si;
-        L.id[i + cnt] = idi;
-        L.fl[i + cnt] = fi;
-      }
-      __syncwarp();
     }
-    if (live) {
-      L.s[p + r] = s;
-      L.id[p + r] = v;
-      L.fl[p + r] = msk ? kMasked : 0;
-    }
-    __syncwarp();
-    len += nnew;
-    n_unmasked += __popc(__ballot_sync(kFull, live && !msk));
-    if (pmin < cursor) cursor = pmin;
-    refresh_pool();
-    __syncwarp();
   };
 
-  // ---- ILP fast path (list window <= kFC*32 entries, shared memory) ----
-  // nth set bit (1-based n) of a uniform mask
-  auto nth_set = [&](uint32_t m, uint32_t n) -> uint32_t {
-    const bool hit = ((m >> lane) & 1u) && (uint32_t)__popc(m & ((1u << lane) - 1u)) == n - 1;
-    return __ffs(__ballot_sync(kFull, hit)) - 1;
-  };
-  auto refresh_fast = [&]() {
-    if (n_unmasked < ef) {
-      pool_full = false;
-      return;
+  // raise thr to the exact pool worst; keep U = pool + worst ties, drop dead F
+  auto compact = [&]() {
+    sort_U();
+    thr = U.s[ef - 1];
+    uint32_t keep = ef;
+    for (uint32_t c = ef; c < nU; c += 32) {  // ties with the worst score stay
+      const uint32_t bm = __ballot_sync(kFull, c + lane < nU && U.s[c + lane] >= thr);
+      keep += __popc(bm);
+      if (bm != kFull) break;
     }
-    double rs[kFC];
-    uint32_t um[kFC];
-#pragma unroll
-    for (uint32_t c = 0; c < kFC; ++c) {
-      const uint32_t i = c * 32 + lane;
-      const bool in = i < len;
-      rs[c] = in ? L.s[i] : -DBL_MAX;
-      um[c] = __ballot_sync(kFull, in && !(L.fl[in ? i : 0] & kMasked));
-    }
-    uint32_t need = ef, pos = kSentinel;
-#pragma unroll
-    for (uint32_t c = 0; c < kFC; ++c) {
-      const uint32_t cnt = __popc(um[c]);
-      if (pos == kSentinel) {
-        if (need <= cnt)
-          pos = c * 32 + nth_set(um[c], need);
-        else
-          need -= cnt;
+    nU = keep;
+    uint32_t w = 0;
+    for (uint32_t c = 0; c < nF; c += 32) {
+      const uint32_t i = c + lane;
+      const bool in = i < nF;
+      const double s = in ? F.s[i] : 0.0;
+      const uint32_t id = in ? F.id[i] : 0;
+      const uint8_t m = in ? F.m[i] : 0;
+      const bool kp = in && s >= thr;
+      const uint32_t bm = __ballot_sync(kFull, kp);
+      __syncwarp();
+      if (kp) {
+        const uint32_t o = w + __popc(bm & ((1u << lane) - 1u));
+        F.s[o] = s, F.id[o] = id, F.m[o] = m;
       }
+      w += __popc(bm);
+      __syncwarp();
     }
-    pool_full = true;
-    worst_s = L.s[pos];
-    uint32_t lo = len;
-#pragma unroll
-    for (uint32_t c = 0; c < kFC; ++c) {
-      const uint32_t i = c * 32 + lane;
-      const uint32_t m = __ballot_sync(kFull, i < len && i > pos && rs[c] < worst_s);
-      if (lo == len && m) lo = c * 32 + __ffs(m) - 1;
-    }
-    if (lo < len) {
-      uint32_t dropped = 0;
-#pragma unroll
-      for (uint32_t c = 0; c < kFC; ++c) {
-        const uint32_t base = c * 32;
-        uint32_t keepmask = 0;
-        if (lo > base) keepmask = lo - base >= 32 ? kFull : ((1u << (lo - base)) - 1u);
-        dropped += __popc(um[c] & ~keepmask);
-      }
-      n_unmasked -= dropped;
-      len = lo;
-    }
-  };
-  auto insert_fast = [&](uint32_t livemask, bool live, double s, uint32_t v, bool msk) {
-    const uint32_t nnew = __popc(livemask);
-    const uint32_t r = __popc(livemask & ((1u << lane) - 1u));
-    double rs[kFC];
-    uint32_t ri[kFC], rf[kFC];
-#pragma unroll
-    for (uint32_t c = 0; c < kFC; ++c) {
-      const uint32_t i = c * 32 + lane;
-      const bool in = i < len;
-      rs[c] = in ? L.s[i] : -DBL_MAX;
-      ri[c] = in ? L.id[i] : kSentinel;
-      rf[c] = in ? L.fl[i] : 0u;
-    }
-    // insertion point of each live entry = #list entries better than it
-    uint32_t p = 0;
-    for (uint32_t q = livemask; q; q &= q - 1) {
-      const uint32_t j = __ffs(q) - 1;
-      const double xs = __shfl_sync(kFull, s, j);
-      const uint32_t xi = __shfl_sync(kFull, v, j);
-      uint32_t cnt = 0;
-#pragma unroll
-      for (uint32_t c = 0; c < kFC; ++c)
-        cnt += __popc(__ballot_sync(kFull, c * 32 + lane < len && better(rs[c], ri[c], xs, xi)));
-      if (lane == j) p = cnt;
-    }
-    if (live) stage[r] = p;
-    __syncwarp();
-    const uint32_t pr = lane < nnew ? stage[lane] : kSentinel;  // non-decreasing
-    const uint32_t pmin = __shfl_sync(kFull, pr, 0);
-    uint32_t sh[kFC];
-#pragma unroll
-    for (uint32_t c = 0; c < kFC; ++c) {
-      const uint32_t i = c * 32 + lane;
-      uint32_t cnt = 0;
-#pragma unroll
-      for (uint32_t step = 16; step >= 1; step >>= 1) {
-        const uint32_t pm = __shfl_sync(kFull, pr, (cnt + step - 1) & 31);
-        if (cnt + step - 1 < nnew && pm <= i) cnt += step;
-      }
-      const uint32_t p31 = __shfl_sync(kFull, pr, 31);
-      if (cnt == 31 && nnew == 32 && p31 <= i) cnt = 32;
-      sh[c] = cnt;
-    }
-    __syncwarp();
-#pragma unroll
-    for (uint32_t c = 0; c < kFC; ++c) {
-      const uint32_t i = c * 32 + lane;
-      if (i < len && i >= pmin) {
-        L.s[i + sh[c]] = rs[c];
-        L.id[i + sh[c]] = ri[c];
-        L.fl[i + sh[c]] = (uint8_t)rf[c];
-      }
-    }
-    if (live) {
-      L.s[p + r] = s;
-      L.id[p + r] = v;
-      L.fl[p + r] = msk ? kMasked : 0;
-    }
-    __syncwarp();
-    len += nnew;
-    n_unmasked += __popc(__ballot_sync(kFull, live && !msk));
-    if (pmin < cursor) cursor = pmin;
-    refresh_fast();
-    __syncwarp();
+    nF = w;
   };
 
-  // choose up to kCB frontier candidates (in order), keeping packets that
-  // are still among them and assigning free slots to the rest (warp 0)
+  // frontier top: argmax (score desc, id asc) over F
+  auto argmax_F = [&](double& bs, uint32_t& bid, uint32_t& bidx) {
+    bs = -DBL_MAX, bid = kSentinel, bidx = kSentinel;
+    for (uint32_t i = lane; i < nF; i += 32) {
+      const double s = F.s[i];
+      const uint32_t id = F.id[i];
+      if (better(s, id, bs, bid)) bs = s, bid = id, bidx = i;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double os = __shfl_xor_sync(kFull, bs, o);
+      const uint32_t oid = __shfl_xor_sync(kFull, bid, o);
+      const uint32_t oix = __shfl_xor_sync(kFull, bidx, o);
+      if (better(os, oid, bs, bid)) bs = os, bid = oid, bidx = oix;
+    }
+  };
+
+  // add new visited nodes (lane-held) to F and, if unmasked, to U
+  auto add_nodes = [&](bool isnew, double s, uint32_t v, bool msk) {
+    u_total += __popc(__ballot_sync(kFull, isnew && !msk));
+    const bool inF = isnew && s >= thr;
+    const bool inU = inF && !msk;
+    const uint32_t mf = __ballot_sync(kFull, inF), mu = __ballot_sync(kFull, inU);
+    if (nF + __popc(mf) > capF) spill_F();
+    if (nU + __popc(mu) + 32 > capU) spill_U();  // +32: sort_U pads to a power of two
+    if (inF) {
+      const uint32_t o = nF + __popc(mf & ((1u << lane) - 1u));
+      F.s[o] = s, F.id[o] = v, F.m[o] = msk ? 1 : 0;
+    }
+    if (inU) {
+      const uint32_t o = nU + __popc(mu & ((1u << lane) - 1u));
+      U.s[o] = s, U.id[o] = v;
+    }
+    nF += __popc(mf);
+    nU += __popc(mu);
+    __syncwarp();
+    if (u_total >= ef && nU >= ef + kUSlack) compact();
+  };
+
+  // next round's candidates: the best kCB frontier nodes without a packet,
+  // by successive thresholded argmax; packets of other nodes are dropped
   auto select = [&]() {
     uint32_t tops = kSentinel, ntop = 0;
-    for (uint32_t c = cursor; c < len && ntop < kCB; c += 32) {
-      const uint32_t i = c + lane;
-      const bool un = i < len && !(L.fl[i] & kExpanded);
-      const uint32_t bm = __ballot_sync(kFull, un);
-      const uint32_t r = ntop + __popc(bm & ((1u << lane) - 1u));
-      const uint32_t id = un ? L.id[i] : kSentinel;
-      // lane r of `tops` receives the r-th unexpanded id
-      for (uint32_t q = bm; q; q &= q - 1) {
-        const uint32_t src = __ffs(q) - 1;
-        const uint32_t rr = ntop + __popc(bm & ((1u << src) - 1u));
-        const uint32_t vid = __shfl_sync(kFull, id, src);
-        if (lane == rr) tops = vid;
+    double ps = DBL_MAX;
+    uint32_t pid = 0;
+    for (; ntop < kCB; ++ntop) {
+      double bs = -DBL_MAX;
+      uint32_t bid = kSentinel;
+      for (uint32_t i = lane; i < nF; i += 32) {
+        const double s = F.s[i];
+        const uint32_t id = F.id[i];
+        if (better(ps, pid, s, id) && better(s, id, bs, bid)) bs = s, bid = id;
       }
-      (void)r;
-      ntop = min(kCB, ntop + (uint32_t)__popc(bm));
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double os = __shfl_xor_sync(kFull, bs, o);
+        const uint32_t oid = __shfl_xor_sync(kFull, bid, o);
+        if (better(os, oid, bs, bid)) bs = os, bid = oid;
+      }
+      if (bid == kSentinel) break;
+      if (lane == ntop) tops = bid;
+      ps = bs, pid = bid;
     }
-    // keep slots whose tag is a current top; free others
     const uint32_t tag = lane < kCP ? pk_tag[lane] : kSentinel;
     bool keep = false;
     for (uint32_t t = 0; t < ntop; ++t) keep |= (tag == __shfl_sync(kFull, tops, t));
@@ -821,16 +735,10 @@ __global__ void __launch_bounds__(kCW * 32, 1)
     const bool m0 = masked_id(entry);
     if (lane == 0) {
       vis[entry >> 5] |= 1u << (entry & 31);
-      L.s[0] = s0;
-      L.id[0] = entry;
-      L.fl[0] = m0 ? kMasked : 0;
       ctrl[1] = 0;
     }
-    __syncwarp();
-    len = 1;
-    n_unmasked = m0 ? 0 : 1;
     scanned = 1;
-    refresh_pool();
+    add_nodes(lane == 0, s0, entry, m0);
     select();
   }
   __syncthreads();
@@ -849,19 +757,20 @@ __global__ void __launch_bounds__(kCW * 32, 1)
       const uint32_t newmask = __ballot_sync(kFull, isnew);
       double s = -DBL_MAX;
       if (newmask) s = score_lanes(newmask, isnew, v);
-      double ks = isnew ? s : -DBL_MAX;
-      uint32_t kid = isnew ? v : kSentinel, kfl = 0;
-      warp_sort32(ks, kid, kfl, lane);
-      const uint32_t cnt = __popc(newmask);
-      if (lane < cnt) {
-        pk_id[sl * 32 + lane] = kid;
-        pk_s[sl * 32 + lane] = ks;
-        // the likely next frontier tops: their adjacency rows go to L2 now
-        if ((M * 4) % 16 == 0) bulk_prefetch_l2(adj + size_t(kid) * M, M * 4);
+      const uint32_t o = __popc(newmask & ((1u << lane) - 1u));
+      if (isnew) {
+        pk_id[sl * 32 + o] = v;
+        pk_s[sl * 32 + o] = s;
+        // likely future frontier tops: their adjacency rows go to L2 now
+        if ((M * 4) % 16 == 0) bulk_prefetch_l2(adj + size_t(v) * M, M * 4);
       }
-      const uint32_t mb = __ballot_sync(kFull, lane < cnt && masked_id(kid));
+      // masked bit per compacted entry: rebuild from the compacted order
+      const uint32_t mraw = __ballot_sync(kFull, isnew && masked_id(v));
       if (lane == 0) {
-        pk_cnt[sl] = cnt;
+        uint32_t mb = 0, bitpos = 0;
+        for (uint32_t q = newmask; q; q &= q - 1, ++bitpos)
+          if ((mraw >> (__ffs(q) - 1)) & 1u) mb |= 1u << bitpos;
+        pk_cnt[sl] = __popc(newmask);
         pk_mbits[sl] = mb;
       }
     }
@@ -875,29 +784,33 @@ __global__ void __launch_bounds__(kCW * 32, 1)
     if (warp == 0) {
       bool done = false;
       for (;;) {
-        uint32_t top = len;
-        for (uint32_t c = cursor; c < len; c += 32) {
-          const uint32_t i = c + lane;
-          const uint32_t bm = __ballot_sync(kFull, i < len && !(L.fl[i] & kExpanded));
-          if (bm) {
-            top = c + __ffs(bm) - 1;
+        double ts;
+        uint32_t tid, tix;
+        argmax_F(ts, tid, tix);
+        if (tid == kSentinel) {  // frontier exhausted
+          done = true;
+          break;
+        }
+        if (u_total >= ef) {  // :390 — pool full and top below its worst
+          uint32_t above = 0;
+          for (uint32_t c = 0; c < nU; c += 32)
+            above += __popc(__ballot_sync(kFull, c + lane < nU && U.s[c + lane] > ts));
+          if (above >= ef) {
+            done = true;
             break;
           }
         }
-        cursor = top;
-        if (top >= len || (pool_full && L.s[top] < worst_s)) {
-          done = true;  // frontier exhausted / :390
-          break;
-        }
-        const uint32_t u = L.id[top];
-        const uint32_t hit = __ballot_sync(kFull, lane < kCP && pk_tag[lane] == u);
+        const uint32_t hit = __ballot_sync(kFull, lane < kCP && pk_tag[lane] == tid);
         if (!hit) break;  // next round pre-expands it
         const uint32_t sl = __ffs(hit) - 1;
-        __syncwarp();
+        // pop: swap-remove from F
         if (lane == 0) {
-          L.fl[top] |= kExpanded;
+          --nF;
+          F.s[tix] = F.s[nF], F.id[tix] = F.id[nF], F.m[tix] = F.m[nF];
           pk_tag[sl] = kSentinel;
         }
+        nF = __shfl_sync(kFull, nF, 0);
+        __syncwarp();
         ++expanded;
         const uint32_t cnt = pk_cnt[sl];
         const uint32_t v = lane < cnt ? pk_id[sl * 32 + lane] : kSentinel;
@@ -905,17 +818,9 @@ __global__ void __launch_bounds__(kCW * 32, 1)
         const bool isnew = lane < cnt && !visited(v);
         __syncwarp();
         if (isnew) atomicOr(&vis[v >> 5], 1u << (v & 31));
-        const uint32_t newmask = __ballot_sync(kFull, isnew);
-        scanned += __popc(newmask);
+        scanned += __popc(__ballot_sync(kFull, isnew));
         const bool msk = isnew && ((pk_mbits[sl] >> lane) & 1u);
-        const bool live = isnew && !(pool_full && s < worst_s);
-        const uint32_t livemask = __ballot_sync(kFull, live);
-        if (livemask) {
-          if (!spilled && len + __popc(livemask) <= kFC * 32)
-            insert_fast(livemask, live, s, v, msk);
-          else
-            insert_sorted(livemask, live, s, v, msk);
-        }
+        add_nodes(isnew, s, v, msk);
       }
       if (done) {
         if (lane == 0) ctrl[1] = 1;
@@ -939,25 +844,15 @@ __global__ void __launch_bounds__(kCW * 32, 1)
     a.dbg[size_t(b) * 4 + 2] = cyc_b;
     a.dbg[size_t(b) * 4 + 3] = expanded;
   }
-  // ---- result (:402-410) ----
-  uint32_t taken = 0;
-  for (uint32_t c = 0; c < len && taken < k; c += 32) {
-    const uint32_t i = c + lane;
-    const bool um = i < len && !(L.fl[i] & kMasked);
-    const uint32_t bm = __ballot_sync(kFull, um);
-    const uint32_t r = taken + __popc(bm & ((1u << lane) - 1u));
-    if (um && r < k) {
-      a.ids[size_t(b) * k + r] = L.id[i];
-      a.scores[size_t(b) * k + r] = (float)L.s[i];
-      if (a.scores64) a.scores64[size_t(b) * k + r] = L.s[i];
-    }
-    taken += __popc(bm);
-  }
-  const uint32_t take = taken < k ? taken : k;
-  for (uint32_t r = take + lane; r < k; r += 32) {
-    a.ids[size_t(b) * k + r] = kSentinel;
-    a.scores[size_t(b) * k + r] = __int_as_float(0x7fc00000);
-    if (a.scores64) a.scores64[size_t(b) * k + r] = __longlong_as_double(0x7ff8000000000000ll);
+  // ---- result (:402-410): the pool's top min(k, |pool|), best-first ----
+  sort_U();
+  const uint32_t take = nU < k ? nU : k;
+  for (uint32_t r = lane; r < k; r += 32) {
+    const bool have = r < take;
+    a.ids[size_t(b) * k + r] = have ? U.id[r] : kSentinel;
+    a.scores[size_t(b) * k + r] = have ? (float)U.s[r] : __int_as_float(0x7fc00000);
+    if (a.scores64)
+      a.scores64[size_t(b) * k + r] = have ? U.s[r] : __longlong_as_double(0x7ff8000000000000ll);
   }
   if (lane == 0) {
     a.n_out[b] = take;
@@ -1021,10 +916,13 @@ void launch_d(ra_ctx* ctx, const SearchArgs& a, const Plan& p, uint32_t spill_ca
 }  // namespace
 
 size_t search_scratch_bytes(const ra_ctx* ctx, uint32_t B, uint32_t max_n, uint32_t d) {
-  // sized for the warp-per-query fallback, which never needs less than v3
-  const Plan p = plan(ctx, B, max_n, d);
-  size_t bytes = size_t(B) * ((size_t(max_n) * 13 + 15) & ~size_t(15)) + 256;
-  (void)p;
+  (void)ctx;
+  (void)d;
+  // covers both kernels: v4's F+U spill slots (pow2 capacity) dominate v2's list
+  uint32_t p2 = 32;
+  while (p2 < max_n) p2 <<= 1;
+  size_t bytes = size_t(B) * (((size_t(p2) * 13 + 15) & ~size_t(15)) +
+                              ((size_t(p2) * 12 + 15) & ~size_t(15))) + 256;
   bytes += size_t(B) * ((max_n + 31) / 32) * 4 + 256;  // HBM visited bitsets
   return bytes;
 }
@@ -1035,6 +933,12 @@ struct CtaPlan {
   size_t bytes;
 };
 
+uint32_t pow2_at_least(uint32_t x) {
+  uint32_t p = 32;
+  while (p < x) p <<= 1;
+  return p;
+}
+
 template <int D>
 CtaPlan cta_plan(const ra_ctx* ctx, uint32_t max_n) {
   CtaPlan p{};
@@ -1043,11 +947,11 @@ CtaPlan cta_plan(const ra_ctx* ctx, uint32_t max_n) {
   CtaLayout<D> lay{0, 0, p.vis_words, 0};
   const size_t fixed = lay.list_off();
   const size_t vis_bytes = (size_t(p.vis_words) * 4 + 15) & ~size_t(15);
-  p.vis_smem = fixed + vis_bytes + 13 * 512 + 16 <= budget;
-  const size_t rest = budget - fixed - (p.vis_smem ? vis_bytes : 0) - 16;
-  if (fixed + 13 * 128 > budget) return p;
-  uint32_t cap = uint32_t(std::min<size_t>(rest / 13, 8192));
-  cap = std::min<uint32_t>(cap, std::max<uint32_t>(max_n, 64));
+  if (fixed + CtaLayout<D>::list_bytes(256) > budget) return p;
+  p.vis_smem = fixed + vis_bytes + CtaLayout<D>::list_bytes(512) <= budget;
+  const size_t rest = budget - fixed - (p.vis_smem ? vis_bytes : 0) - 32;
+  uint32_t cap = uint32_t(std::min<size_t>(rest / 25, 8192));
+  cap = std::min<uint32_t>(cap, pow2_at_least(std::max<uint32_t>(max_n, 64)));
   p.cap = std::max<uint32_t>(cap & ~31u, 32);
   lay.cap = p.cap;
   lay.vis_smem = p.vis_smem;
@@ -1061,18 +965,15 @@ bool try_launch_cta(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* s
   const CtaPlan p = cta_plan<D>(ctx, max_n);
   if (!p.ok) return false;
   SearchArgs s = a;
+  const uint32_t spill_cap = pow2_at_least(max_n);
   uint8_t* cur = scratch;
-  s.spill = nullptr;
-  s.vis_global = nullptr;
-  if (p.cap < max_n) {
-    s.spill = cur;
-    cur += (size_t(a.B) * ((size_t(max_n) * 13 + 15) & ~size_t(15)) + 255) & ~size_t(255);
-  }
-  if (!p.vis_smem) s.vis_global = reinterpret_cast<uint32_t*>(cur);
+  s.spill = cur;
+  cur += (size_t(a.B) * CtaLayout<D>::list_bytes(spill_cap) + 255) & ~size_t(255);
+  s.vis_global = p.vis_smem ? nullptr : reinterpret_cast<uint32_t*>(cur);
   CtaLayout<D> lay{uint32_t(D), p.cap, p.vis_words, p.vis_smem};
   auto kern = k_graph_search_cta<D>;
   RA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.bytes));
-  kern<<<a.B, kCW * 32, p.bytes, ctx->stream>>>(s, lay, max_n);
+  kern<<<a.B, kCW * 32, p.bytes, ctx->stream>>>(s, lay, spill_cap);
   RA_LAUNCH_CHECK();
   return true;
 }
