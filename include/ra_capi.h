@@ -192,8 +192,9 @@ ra_status ra_engine_last_stats(ra_engine* e, uint64_t* total_scanned,
  * attention + merge kernels (recorded on the ctx stream). Synchronizes. */
 ra_status ra_engine_last_timing(ra_engine* e, float* search_ms, float* attention_ms);
 /* Profiling aid: search-kernel counters of the last step summed over heads:
- * {rounds, cycles pre-expanding, cycles committing, commits}. */
-ra_status ra_engine_debug_counters(ra_engine* e, uint64_t* out4);
+ * {rounds, cycles pre-expanding, cycles committing, commits, commit-phase
+ * cycles in argmax / stop test / packet apply / add+compact / select, 0,0,0}. */
+ra_status ra_engine_debug_counters(ra_engine* e, uint64_t* out12);
 
 #ifdef __cplusplus
 }

@@ -525,9 +525,10 @@ class Engine:
 
     def debug_counters(self):
         """{rounds, cycles_pre_expand, cycles_commit, commits} of the last step."""
-        out = (C.c_uint64 * 4)()
+        out = (C.c_uint64 * 12)()
         _check(lib.ra_engine_debug_counters(self.h, out))
-        return dict(zip(("rounds", "cycles_pre_expand", "cycles_commit", "commits"), list(out)))
+        return dict(zip(("rounds", "cycles_pre_expand", "cycles_commit", "commits", "cy_argmax",
+                         "cy_stop", "cy_packet", "cy_add", "cy_select"), list(out)))
 
     def last_stats(self):
         s, e = C.c_uint64(), C.c_uint64()

@@ -502,8 +502,8 @@ ra_status ra_engine_create(ra_ctx* ctx, ra_kv* const* groups, uint32_t n_groups,
     e->truncated.alloc(H);
     e->expanded.alloc(H);
     e->o_empty.alloc(H);
-    e->dbg.alloc(size_t(H) * 4);
-    RA_CUDA(cudaMemset(e->dbg.p, 0, size_t(H) * 32));
+    e->dbg.alloc(size_t(H) * 12);
+    RA_CUDA(cudaMemset(e->dbg.p, 0, size_t(H) * 96));
     e->flag.alloc(1);
     for (auto* b : {&e->ow, &e->oo, &e->out}) b->alloc(size_t(H) * d);
     for (auto* b : {&e->zw, &e->sw, &e->zo, &e->so}) b->alloc(H);
@@ -656,15 +656,15 @@ ra_status ra_engine_last_timing(ra_engine* e, float* search_ms, float* attention
 
 // Search-kernel counters of the last step summed over heads: rounds,
 // cycles in pre-expansion, cycles in commit, commits (profiling aid).
-ra_status ra_engine_debug_counters(ra_engine* e, uint64_t* out4) {
+ra_status ra_engine_debug_counters(ra_engine* e, uint64_t* out12) {
   return guard([&] {
     if (!e) invalid("null engine");
     DeviceGuard dg(e->ctx->device);
-    std::vector<uint64_t> h(size_t(e->H) * 4);
+    std::vector<uint64_t> h(size_t(e->H) * 12);
     RA_CUDA(cudaMemcpyAsync(h.data(), e->dbg.p, h.size() * 8, cudaMemcpyDeviceToHost, e->ctx->stream));
     RA_CUDA(cudaStreamSynchronize(e->ctx->stream));
-    for (int j = 0; j < 4; ++j) out4[j] = 0;
-    for (size_t i = 0; i < h.size(); ++i) out4[i % 4] += h[i];
+    for (int j = 0; j < 12; ++j) out12[j] = 0;
+    for (size_t i = 0; i < h.size(); ++i) out12[i % 12] += h[i];
   });
 }
 

@@ -465,10 +465,10 @@ struct CtaLayout {
   __host__ __device__ static size_t pk_off() {
     return tiles_off() + size_t(kCW) * 32 * kRow * 4;
   }
-  // packets: tag u32[P], cnt u32[P], mbits u32[P], cand u32[B], slotof u32[B],
-  // ctrl u32[8] | ids u32[P][32] | scores f64[P][32]
+  // packets: tag u32[P], cnt u32[P], cand u32[B], slotof u32[B], ctrl u32[8],
+  // masked u8[P][32] | ids u32[P][32] | scores f64[P][32]
   __host__ __device__ static size_t pk_hdr() {
-    return (size_t(kCP) * 12 + kCB * 8 + 32 + 15) & ~size_t(15);
+    return (size_t(kCP) * 8 + kCB * 8 + 32 + size_t(kCP) * 32 + 15) & ~size_t(15);
   }
   __host__ __device__ static size_t pk_bytes() { return pk_hdr() + size_t(kCP) * 32 * 12; }
   __host__ __device__ size_t list_off() const { return pk_off() + pk_bytes(); }
@@ -511,10 +511,10 @@ __global__ void __launch_bounds__(kCW * 32, 1)
   uint8_t* pk = smem + CtaLayout<D>::pk_off();
   uint32_t* pk_tag = reinterpret_cast<uint32_t*>(pk);
   uint32_t* pk_cnt = pk_tag + kCP;
-  uint32_t* pk_mbits = pk_cnt + kCP;
-  uint32_t* cand = pk_mbits + kCP;
+  uint32_t* cand = pk_cnt + kCP;
   uint32_t* slotof = cand + kCB;
   uint32_t* ctrl = slotof + kCB;  // [0] = #candidates, [1] = done
+  uint8_t* pk_m = reinterpret_cast<uint8_t*>(ctrl + 8);  // [kCP][32]
   uint32_t* pk_id = reinterpret_cast<uint32_t*>(pk + CtaLayout<D>::pk_hdr());
   double* pk_s = reinterpret_cast<double*>(pk_id + kCP * 32);
   uint8_t* lists = smem + lay.list_off();
@@ -638,14 +638,19 @@ __global__ void __launch_bounds__(kCW * 32, 1)
     nF = w;
   };
 
-  // frontier top: argmax (score desc, id asc) over F
+  // frontier top: argmax (score desc, id asc) over F; the lane-local bests
+  // are kept for select()
+  double lane_bs = -DBL_MAX;
+  uint32_t lane_bid = kSentinel;
   auto argmax_F = [&](double& bs, uint32_t& bid, uint32_t& bidx) {
     bs = -DBL_MAX, bid = kSentinel, bidx = kSentinel;
+#pragma unroll 4
     for (uint32_t i = lane; i < nF; i += 32) {
       const double s = F.s[i];
       const uint32_t id = F.id[i];
       if (better(s, id, bs, bid)) bs = s, bid = id, bidx = i;
     }
+    lane_bs = bs, lane_bid = bid;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       const double os = __shfl_xor_sync(kFull, bs, o);
@@ -662,7 +667,7 @@ __global__ void __launch_bounds__(kCW * 32, 1)
     const bool inU = inF && !msk;
     const uint32_t mf = __ballot_sync(kFull, inF), mu = __ballot_sync(kFull, inU);
     if (nF + __popc(mf) > capF) spill_F();
-    if (nU + __popc(mu) + 32 > capU) spill_U();  // +32: sort_U pads to a power of two
+    if (nU + __popc(mu) > capU) spill_U();
     if (inF) {
       const uint32_t o = nF + __popc(mf & ((1u << lane) - 1u));
       F.s[o] = s, F.id[o] = v, F.m[o] = msk ? 1 : 0;
@@ -677,30 +682,23 @@ __global__ void __launch_bounds__(kCW * 32, 1)
     if (u_total >= ef && nU >= ef + kUSlack) compact();
   };
 
-  // next round's candidates: the best kCB frontier nodes without a packet,
-  // by successive thresholded argmax; packets of other nodes are dropped
-  auto select = [&]() {
-    uint32_t tops = kSentinel, ntop = 0;
-    double ps = DBL_MAX;
-    uint32_t pid = 0;
-    for (; ntop < kCB; ++ntop) {
-      double bs = -DBL_MAX;
-      uint32_t bid = kSentinel;
+  // next round's candidates: each lane's best frontier node, warp-sorted,
+  // first kCB taken (approximate top-kCB; the true top is always in it);
+  // packets of other nodes are dropped
+  auto select = [&](bool fresh) {
+    double bs = lane_bs;
+    uint32_t bid = lane_bid, dummy = 0;
+    if (!fresh) {
+      bs = -DBL_MAX, bid = kSentinel;
       for (uint32_t i = lane; i < nF; i += 32) {
         const double s = F.s[i];
         const uint32_t id = F.id[i];
-        if (better(ps, pid, s, id) && better(s, id, bs, bid)) bs = s, bid = id;
+        if (better(s, id, bs, bid)) bs = s, bid = id;
       }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const double os = __shfl_xor_sync(kFull, bs, o);
-        const uint32_t oid = __shfl_xor_sync(kFull, bid, o);
-        if (better(os, oid, bs, bid)) bs = os, bid = oid;
-      }
-      if (bid == kSentinel) break;
-      if (lane == ntop) tops = bid;
-      ps = bs, pid = bid;
     }
+    warp_sort32(bs, bid, dummy, lane);
+    const uint32_t ntop = min(kCB, (uint32_t)__popc(__ballot_sync(kFull, bid != kSentinel)));
+    const uint32_t tops = bid;
     const uint32_t tag = lane < kCP ? pk_tag[lane] : kSentinel;
     bool keep = false;
     for (uint32_t t = 0; t < ntop; ++t) keep |= (tag == __shfl_sync(kFull, tops, t));
@@ -726,6 +724,7 @@ __global__ void __launch_bounds__(kCW * 32, 1)
   };
 
   uint64_t cyc_a = 0, cyc_b = 0, t_mark = clock64();
+  uint64_t cy[5] = {0, 0, 0, 0, 0};  // argmax, stop test, packet apply, add/compact, select
   uint32_t rounds = 0;
   if (warp == 0) {
     // entry (:379-384)
@@ -739,7 +738,7 @@ __global__ void __launch_bounds__(kCW * 32, 1)
     }
     scanned = 1;
     add_nodes(lane == 0, s0, entry, m0);
-    select();
+    select(false);
   }
   __syncthreads();
 
@@ -747,6 +746,7 @@ __global__ void __launch_bounds__(kCW * 32, 1)
     // ---- (A) pre-expand candidates into packets, all warps ----
     const uint32_t nc = ctrl[0];
     ++rounds;
+    if (threadIdx.x == 0) ctrl[2] = 0;
     for (uint32_t ci = warp; ci < nc; ci += kCW) {
       const uint32_t c = cand[ci], sl = slotof[ci];
       const uint32_t v = lane < M ? __ldg(adj + size_t(c) * M + lane) : kSentinel;
@@ -761,18 +761,11 @@ __global__ void __launch_bounds__(kCW * 32, 1)
       if (isnew) {
         pk_id[sl * 32 + o] = v;
         pk_s[sl * 32 + o] = s;
+        pk_m[sl * 32 + o] = masked_id(v) ? 1 : 0;
         // likely future frontier tops: their adjacency rows go to L2 now
         if ((M * 4) % 16 == 0) bulk_prefetch_l2(adj + size_t(v) * M, M * 4);
       }
-      // masked bit per compacted entry: rebuild from the compacted order
-      const uint32_t mraw = __ballot_sync(kFull, isnew && masked_id(v));
-      if (lane == 0) {
-        uint32_t mb = 0, bitpos = 0;
-        for (uint32_t q = newmask; q; q &= q - 1, ++bitpos)
-          if ((mraw >> (__ffs(q) - 1)) & 1u) mb |= 1u << bitpos;
-        pk_cnt[sl] = __popc(newmask);
-        pk_mbits[sl] = mb;
-      }
+      if (lane == 0) pk_cnt[sl] = __popc(newmask);
     }
     __syncthreads();
     {
@@ -786,19 +779,28 @@ __global__ void __launch_bounds__(kCW * 32, 1)
       for (;;) {
         double ts;
         uint32_t tid, tix;
+        uint64_t tc0 = clock64();
         argmax_F(ts, tid, tix);
+        uint64_t tc1 = clock64();
+        cy[0] += tc1 - tc0;
         if (tid == kSentinel) {  // frontier exhausted
           done = true;
           break;
         }
         if (u_total >= ef) {  // :390 — pool full and top below its worst
           uint32_t above = 0;
+#pragma unroll 4
           for (uint32_t c = 0; c < nU; c += 32)
             above += __popc(__ballot_sync(kFull, c + lane < nU && U.s[c + lane] > ts));
           if (above >= ef) {
             done = true;
             break;
           }
+        }
+        {
+          const uint64_t t = clock64();
+          cy[1] += t - tc1;
+          tc1 = t;
         }
         const uint32_t hit = __ballot_sync(kFull, lane < kCP && pk_tag[lane] == tid);
         if (!hit) break;  // next round pre-expands it
@@ -819,13 +821,40 @@ __global__ void __launch_bounds__(kCW * 32, 1)
         __syncwarp();
         if (isnew) atomicOr(&vis[v >> 5], 1u << (v & 31));
         scanned += __popc(__ballot_sync(kFull, isnew));
-        const bool msk = isnew && ((pk_mbits[sl] >> lane) & 1u);
+        const bool msk = isnew && pk_m[sl * 32 + lane];
+        {
+          const uint64_t t = clock64();
+          cy[2] += t - tc1;
+          tc1 = t;
+        }
         add_nodes(isnew, s, v, msk);
+        cy[3] += clock64() - tc1;
       }
+      const uint64_t tsel = clock64();
       if (done) {
         if (lane == 0) ctrl[1] = 1;
       } else {
-        select();
+        select(true);  // F unchanged since the argmax that ended the loop
+      }
+      cy[4] += clock64() - tsel;
+      __threadfence_block();
+      if (lane == 0) *reinterpret_cast<volatile uint32_t*>(&ctrl[2]) = 1;
+    } else {
+      // helpers: 2-hop L2 prefetch for the likely next tops — neighbours that
+      // beat their parent in this round's packets — while warp 0 commits
+      for (uint32_t ci = warp - 1; ci < nc; ci += kCW - 1) {
+        const uint32_t sl = slotof[ci];
+        const uint32_t cnt = pk_cnt[sl];
+        const double ps = -DBL_MAX;  // parent score unknown here: use all entries
+        (void)ps;
+        const uint32_t want = __ballot_sync(kFull, lane < cnt);
+        uint32_t done_n = 0;
+        for (uint32_t q = want; q && done_n < 4; q &= q - 1, ++done_n) {
+          if (*reinterpret_cast<volatile uint32_t*>(&ctrl[2])) break;
+          const uint32_t x = pk_id[sl * 32 + (__ffs(q) - 1)];
+          const uint32_t nb = lane < M ? __ldg(adj + size_t(x) * M + lane) : kSentinel;
+          if (nb != kSentinel && !visited(nb)) bulk_prefetch_l2(keys + size_t(nb) * D, D * 4u);
+        }
       }
     }
     __syncthreads();
@@ -839,10 +868,11 @@ __global__ void __launch_bounds__(kCW * 32, 1)
 
   if (warp != 0) return;
   if (a.dbg && lane == 0) {
-    a.dbg[size_t(b) * 4 + 0] = rounds;
-    a.dbg[size_t(b) * 4 + 1] = cyc_a;
-    a.dbg[size_t(b) * 4 + 2] = cyc_b;
-    a.dbg[size_t(b) * 4 + 3] = expanded;
+    a.dbg[size_t(b) * 12 + 0] = rounds;
+    a.dbg[size_t(b) * 12 + 1] = cyc_a;
+    a.dbg[size_t(b) * 12 + 2] = cyc_b;
+    a.dbg[size_t(b) * 12 + 3] = expanded;
+    for (int j = 0; j < 5; ++j) a.dbg[size_t(b) * 12 + 4 + j] = cy[j];
   }
   // ---- result (:402-410): the pool's top min(k, |pool|), best-first ----
   sort_U();
