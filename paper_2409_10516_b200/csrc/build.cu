@@ -27,6 +27,8 @@
 
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace ra {
 namespace {
 
@@ -206,6 +208,17 @@ __global__ void __launch_bounds__(KTHREADS)
     compact_query(bs, bi, cnt[ql], kt, lane);
     for (uint32_t r = lane; r < kt; r += 32) knn[(q0 + ql) * kt + r] = bi[r];
   }
+}
+
+__global__ void k_gather_rows(const float* __restrict__ Q, uint32_t d,
+                              const uint32_t* __restrict__ rows, uint32_t nr, float* out) {
+  const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (t < uint64_t(nr) * d) out[t] = Q[uint64_t(rows[t / d]) * d + t % d];
+}
+__global__ void k_scatter_knn(const uint32_t* __restrict__ kf, const uint32_t* __restrict__ rows,
+                              uint32_t nr, uint32_t kt, uint32_t* knn) {
+  const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (t < uint64_t(nr) * kt) knn[uint64_t(rows[t / kt]) * kt + t % kt] = kf[t];
 }
 
 // ---- K2 -------------------------------------------------------------------------
@@ -629,7 +642,30 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
       TQ = tq_own.p;
     }
     DevBuf<uint32_t> knn(std::max<size_t>(size_t(nq) * kt, 1));
-    if (nq) {
+    const char* force_exact = std::getenv("RA_KNN_EXACT");
+    const bool use_tc = nq && !(force_exact && force_exact[0] == '1') &&
+                        knn_tc_supported(d, nq, n, kt);
+    if (use_tc) {
+      // tensor-core filter + exact rescoring; certificate failures -> exact path
+      DevBuf<uint32_t> fail;
+      double ms_gemm = 0;
+      const uint32_t nf = knn_tc(ctx, TQ, nq, K, n, d, kt, knn.p, fail, &ms_gemm);
+      st.knn_rows = nq;
+      st.knn_rows_widened = nf;
+      if (nf) {
+        DevBuf<float> qf(size_t(nf) * d);
+        DevBuf<uint32_t> kf(size_t(nf) * kt);
+        k_gather_rows<<<(nf * d + 255) / 256, 256, 0, s>>>(TQ, d, fail.p, nf, qf.p);
+        uint32_t cb = 1;
+        while (cb < 2 * kt + KK) cb <<= 1;
+        DevBuf<double> bs(size_t((nf + KQ - 1) / KQ * KQ) * cb);
+        DevBuf<uint32_t> bi(size_t((nf + KQ - 1) / KQ * KQ) * cb);
+        k_knn<<<(nf + KQ - 1) / KQ, KTHREADS, 0, s>>>(qf.p, nf, K, n, d, kt, cb, bs.p, bi.p,
+                                                      kf.p, nullptr);
+        k_scatter_knn<<<(nf * kt + 255) / 256, 256, 0, s>>>(kf.p, fail.p, nf, kt, knn.p);
+        RA_LAUNCH_CHECK();
+      }
+    } else if (nq) {
       uint32_t cb = 1;
       while (cb < 2 * kt + KK) cb <<= 1;
       const uint64_t chunk = std::min<uint64_t>(nq, std::max<uint64_t>(KQ, (1ull << 30) / (cb * 12ull)) / KQ * KQ);

@@ -228,4 +228,9 @@ size_t engine_attention_part_doubles(uint32_t G, uint32_t hpg, uint32_t nW, uint
 void launch_engine_wpartial(cudaStream_t st, const EngineAttn& a);
 void launch_engine_omega_merge(cudaStream_t st, const EngineAttn& a);
 
+// tensor-core kNN (knn_tc.cu)
+bool knn_tc_supported(uint32_t d, uint64_t nq, uint32_t n, uint32_t kt);
+uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32_t n, uint32_t d,
+                uint32_t kt, uint32_t* knn, DevBuf<uint32_t>& fail_rows, double* ms_gemm);
+
 }  // namespace ra

@@ -1,0 +1,456 @@
+// K1 on the 5th-generation tensor cores: exact training kNN
+// (/root/reference/proj/src/index_oodgraph.cpp:104-128) via a certified
+// approximate filter.
+//
+//   1. k_split_*: q = qh + ql, k = kh + kl (bf16 hi/lo split of f32) laid
+//      out in the canonical no-swizzle K-major UMMA core-matrix layout
+//      (8 rows x 16 B core matrices) so that a tile is ONE contiguous block
+//      that a 1-D TMA bulk copy lands in shared memory ready for the MMA.
+//   2. k_knn_tc: S~ = qh.kh + qh.kl + ql.kh as one bf16 GEMM with K = 3d
+//      (tcgen05.mma kind::f16, M=128, N=256, fp32 accumulators in TMEM,
+//      double-buffered). Warp-specialised: warp 4 = TMA producer, warp 5 =
+//      MMA issuer (one thread), warps 0-3 = epilogue (thread = query row:
+//      tcgen05.ld, keep S~ > row threshold in an HBM candidate buffer,
+//      warp-cooperative compaction raises the threshold). The nq x n score
+//      matrix never exists.
+//   3. k_rescore: per row, sort candidates by S~, rescore the best K in the
+//      reference's exact in-order f64 dot, rank (score desc, id asc), and
+//      certify: every key not rescored has S~ <= tau, and |S - S~| <= delta
+//      (bf16 split + fp32 accumulation bound), so tau + delta < s_kt proves
+//      the top-kt is exact. Rows that fail go to the exact f64 kernel.
+#include <cfloat>
+#include <cstdint>
+#include <cstring>
+
+#include "common.cuh"
+#include "tma.cuh"
+
+namespace ra {
+namespace {
+
+constexpr uint32_t TM = 128;         // query rows per tile (UMMA M)
+constexpr uint32_t TN = 256;         // keys per tile (UMMA N)
+constexpr uint32_t KS = 64;          // K elements per pipeline stage (bf16)
+constexpr uint32_t NSTAGE = 3;       // B pipeline depth
+constexpr uint32_t EPI_WARPS = 4;    // epilogue warps (thread = row)
+constexpr uint32_t KNN_THREADS = (EPI_WARPS + 2) * 32;
+
+__device__ __forceinline__ uint16_t f2bf_rn(float x) {
+  uint32_t u = __float_as_uint(x);
+  u += 0x7FFFu + ((u >> 16) & 1u);  // round to nearest even (finite inputs)
+  return uint16_t(u >> 16);
+}
+__device__ __forceinline__ float bf2f(uint16_t h) { return __uint_as_float(uint32_t(h) << 16); }
+
+// element (r, kk) of a [R rows x K] K-major no-swizzle tile, chunked in
+// stages of KS: stage | 8-elem chunk | 8-row group | row | elem
+__device__ __forceinline__ size_t tile_off(uint32_t r, uint32_t kk, uint32_t R) {
+  const uint32_t st = kk / KS, ch = (kk % KS) / 8, e = kk % 8;
+  return (((size_t(st) * (KS / 8) + ch) * (R / 8) + r / 8) * 8 + (r % 8)) * 8 + e;
+}
+
+// q rows -> A' = [qh | qh | ql], k rows -> B' = [kh | kl | kh]  (K' = 3d)
+__global__ void k_split(const float* __restrict__ x, uint64_t rows, uint32_t d, uint32_t R,
+                        uint64_t tiles, int is_query, uint16_t* __restrict__ out) {
+  const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  const uint32_t K3 = 3 * d;
+  if (t >= tiles * R * uint64_t(d)) return;
+  const uint64_t r = t / d;
+  const uint32_t i = uint32_t(t % d);
+  const float v = r < rows ? x[r * d + i] : 0.f;
+  const uint16_t hi = f2bf_rn(v);
+  const uint16_t lo = f2bf_rn(v - bf2f(hi));
+  const uint64_t tile = r / R;
+  const uint32_t rr = uint32_t(r % R);
+  uint16_t* base = out + tile * size_t(R) * K3;
+  base[tile_off(rr, i, R)] = hi;
+  base[tile_off(rr, d + i, R)] = is_query ? hi : lo;
+  base[tile_off(rr, 2 * d + i, R)] = is_query ? lo : hi;
+}
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_NONE (layout type 0):
+// LBO = byte distance between K-adjacent core matrices, SBO = between
+// M/N-adjacent 8-row groups (cute/arch/mma_sm100_desc.hpp field layout).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;  // descriptor version for sm_100
+  return d;
+}
+// instruction descriptor: f32 accum, bf16 A/B, K-major both, N, M
+__host__ __device__ constexpr uint32_t instr_desc(uint32_t M, uint32_t N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_c, uint64_t da, uint64_t db, uint32_t idesc,
+                                         uint32_t accum) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(tmem_c),
+      "l"(da), "l"(db), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_init_n(uint64_t* bar, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// 32 lanes x 32 columns of fp32 from TMEM: thread l gets row (lane base + l)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// warp-cooperative: sort row buffer (cnt entries) by approx score desc, keep
+// `keep`; returns the new threshold (score of entry keep-1) or -inf
+__device__ float compact_row(float* bs, uint32_t* bi, uint32_t cnt, uint32_t keep,
+                             uint32_t lane) {
+  uint32_t p2 = 32;
+  while (p2 < cnt) p2 <<= 1;
+  for (uint32_t i = cnt + lane; i < p2; i += 32) bs[i] = -FLT_MAX, bi[i] = kSentinel;
+  __syncwarp();
+  for (uint32_t k = 2; k <= p2; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = lane; i < p2; i += 32) {
+        const uint32_t p = i ^ j;
+        if (p > i) {
+          const bool desc = (i & k) == 0;
+          const float a = bs[i], c = bs[p];
+          if (desc ? (c > a) : (a > c)) {
+            bs[i] = c, bs[p] = a;
+            const uint32_t t = bi[i];
+            bi[i] = bi[p], bi[p] = t;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  return cnt >= keep ? bs[keep - 1] : -FLT_MAX;
+}
+
+struct TcArgs {
+  const uint16_t* A;  // [mtiles][TM x K3] blocked
+  const uint16_t* B;  // [ntiles][TN x K3] blocked
+  uint64_t nq;
+  uint32_t n, K3, keep, cb;
+  float* bufS;        // [nq][cb]
+  uint32_t* bufI;
+  uint32_t* cnt_out;  // [nq]
+  float* thr_out;     // [nq]
+};
+
+__global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t K3 = a.K3, nstages_k = K3 / KS;
+  const uint32_t ntiles = (a.n + TN - 1) / TN;
+  const uint64_t m0 = uint64_t(blockIdx.x) * TM;
+  // layout: A tile | B stages | barriers | tmem slot
+  uint8_t* sA = smem;
+  const uint32_t a_bytes = TM * K3 * 2;
+  uint8_t* sB = smem + a_bytes;
+  const uint32_t b_stage = TN * KS * 2;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + NSTAGE * b_stage);
+  uint64_t* full = bars;                 // [NSTAGE]
+  uint64_t* empty = bars + NSTAGE;       // [NSTAGE]
+  uint64_t* a_full = bars + 2 * NSTAGE;  // [1]
+  uint64_t* t_full = a_full + 1;         // [2]
+  uint64_t* t_empty = t_full + 2;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
+
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < NSTAGE; ++s) {
+      mbar_init_n(full + s, 1);
+      mbar_init_n(empty + s, 1);
+    }
+    mbar_init_n(a_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init_n(t_full + b, 1);
+      mbar_init_n(t_empty + b, EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {  // TMEM: 2 accumulators x 256 fp32 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == EPI_WARPS) {
+    // ---- TMA producer ----
+    if (lane == 0) {
+      mbar_arrive_expect_tx(a_full, a_bytes);
+      const uint8_t* gA = reinterpret_cast<const uint8_t*>(a.A) + size_t(blockIdx.x) * a_bytes;
+      for (uint32_t off = 0; off < a_bytes; off += 32768)
+        bulk_g2s(sA + off, gA + off, min(32768u, a_bytes - off), a_full);
+      uint32_t it = 0;
+      for (uint32_t t = 0; t < ntiles; ++t)
+        for (uint32_t s = 0; s < nstages_k; ++s, ++it) {
+          const uint32_t slot = it % NSTAGE, ph = (it / NSTAGE) & 1u;
+          mbar_wait(empty + slot, ph ^ 1u);
+          mbar_arrive_expect_tx(full + slot, b_stage);
+          const uint8_t* gB = reinterpret_cast<const uint8_t*>(a.B) +
+                              (size_t(t) * nstages_k + s) * b_stage;
+          bulk_g2s(sB + slot * b_stage, gB, b_stage, full + slot);
+        }
+    }
+  } else if (warp == EPI_WARPS + 1) {
+    // ---- MMA issuer (one thread) ----
+    if (lane == 0) {
+      const uint32_t idesc = instr_desc(TM, TN);
+      mbar_wait(a_full, 0);
+      fence_after();
+      const uint32_t a_base = smem_u32(sA), b_base0 = smem_u32(sB);
+      // A: stage-major blocks of [KS/8 chunks][TM/8 groups][128 B]
+      const uint32_t a_lbo = (TM / 8) * 128, b_lbo = (TN / 8) * 128, sbo = 128;
+      uint32_t it = 0;
+      for (uint32_t t = 0; t < ntiles; ++t) {
+        const uint32_t buf = t & 1u, tph = (t >> 1) & 1u;
+        mbar_wait(t_empty + buf, tph ^ 1u);
+        fence_after();
+        const uint32_t tc = tmem + buf * TN;
+        for (uint32_t s = 0; s < nstages_k; ++s, ++it) {
+          const uint32_t slot = it % NSTAGE, ph = (it / NSTAGE) & 1u;
+          mbar_wait(full + slot, ph);
+          fence_after();
+          const uint32_t b_base = b_base0 + slot * b_stage;
+#pragma unroll
+          for (uint32_t kk = 0; kk < KS / 16; ++kk) {
+            const uint64_t da =
+                smem_desc(a_base + s * (KS / 8) * a_lbo + 2 * kk * a_lbo, a_lbo, sbo);
+            const uint64_t db = smem_desc(b_base + 2 * kk * b_lbo, b_lbo, sbo);
+            mma_bf16(tc, da, db, idesc, (s | kk) ? 1u : 0u);
+          }
+          mma_commit(empty + slot);  // frees the stage when these MMAs finish
+        }
+        mma_commit(t_full + buf);    // accumulator ready for the epilogue
+      }
+    }
+  } else {
+    // ---- epilogue: thread = query row ----
+    const uint32_t row = warp * 32 + lane;
+    const uint64_t q = m0 + row;
+    const bool valid_row = q < a.nq;
+    float thr = -FLT_MAX;
+    uint32_t cnt = 0;
+    float* bs = a.bufS + (valid_row ? q : 0) * size_t(a.cb);
+    uint32_t* bi = a.bufI + (valid_row ? q : 0) * size_t(a.cb);
+    for (uint32_t t = 0; t < ntiles; ++t) {
+      const uint32_t buf = t & 1u, tph = (t >> 1) & 1u;
+      mbar_wait(t_full + buf, tph);
+      fence_after();
+      for (uint32_t c0 = 0; c0 < TN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem + ((warp * 32u) << 16) + buf * TN + c0, v);
+        const uint32_t key0 = t * TN + c0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (valid_row && key0 + j < a.n && v[j] > thr) {
+            bs[cnt] = v[j];
+            bi[cnt] = key0 + j;
+            ++cnt;
+          }
+        }
+        // a full buffer is compacted by the whole warp (rare after warm-up)
+        uint32_t need = __ballot_sync(kFull, cnt + 32 > a.cb);
+        while (need) {
+          const uint32_t l = __ffs(need) - 1;
+          need &= need - 1;
+          const uint64_t ql = m0 + warp * 32 + l;
+          const uint32_t cl = __shfl_sync(kFull, cnt, l);
+          const float nt = compact_row(a.bufS + ql * a.cb, a.bufI + ql * a.cb, cl, a.keep, lane);
+          if (lane == l) {
+            cnt = min(cl, a.keep);
+            thr = nt;
+          }
+        }
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(t_empty + buf);
+    }
+    if (valid_row) {
+      a.cnt_out[q] = cnt;
+      a.thr_out[q] = thr;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem)
+                 : "memory");
+}
+
+// ---- exact rescoring + certificate (warp per row) --------------------------
+__global__ void k_rescore(const float* __restrict__ Q, const float* __restrict__ K, uint64_t nq,
+                          uint32_t d, uint32_t kt, uint32_t keep, uint32_t cb,
+                          float* __restrict__ bufS, uint32_t* __restrict__ bufI,
+                          const uint32_t* __restrict__ cnt_in, const float* __restrict__ thr_in,
+                          double delta_scale, double kmax_norm, double* __restrict__ exS,
+                          uint32_t es_stride, uint32_t* __restrict__ knn, uint32_t* __restrict__ fail,
+                          uint32_t* __restrict__ fail_count) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t q = blockIdx.x * uint64_t(blockDim.x / 32) + (threadIdx.x >> 5);
+  if (q >= nq) return;
+  const uint32_t cnt = cnt_in[q];
+  float* bs = bufS + q * cb;
+  uint32_t* bi = bufI + q * cb;
+  // best `keep` by approximate score
+  compact_row(bs, bi, cnt, keep, lane);
+  const uint32_t m = min(cnt, keep);
+  // tau: every key not rescored has S~ <= tau
+  float tau = thr_in[q];
+  if (cnt > keep) tau = fmaxf(tau, bs[keep]);
+  // exact in-order f64 scores of the m candidates
+  const float* qr = Q + q * d;
+  double* es = exS + q * size_t(es_stride);
+  double qn = 0.0;
+  for (uint32_t i = 0; i < d; ++i) qn = fma((double)qr[i], (double)qr[i], qn);
+  for (uint32_t i = lane; i < m; i += 32) {
+    const float* kr = K + size_t(bi[i]) * d;
+    double acc = 0.0;
+    for (uint32_t j = 0; j < d; ++j) acc = fma((double)qr[j], (double)kr[j], acc);
+    es[i] = acc;
+  }
+  __syncwarp();
+  // rank by (exact score desc, id asc) via bitonic over next pow2
+  uint32_t p2 = 32;
+  while (p2 < m) p2 <<= 1;
+  for (uint32_t i = m + lane; i < p2; i += 32) es[i] = -DBL_MAX, bi[i] = kSentinel;
+  __syncwarp();
+  for (uint32_t k = 2; k <= p2; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = lane; i < p2; i += 32) {
+        const uint32_t p = i ^ j;
+        if (p > i) {
+          const bool desc = (i & k) == 0;
+          const double a = es[i], c = es[p];
+          const uint32_t ia = bi[i], ic = bi[p];
+          const bool c_better = c > a || (c == a && ic < ia);
+          const bool a_better = a > c || (a == c && ia < ic);
+          if (desc ? c_better : a_better) {
+            es[i] = c, es[p] = a;
+            bi[i] = ic, bi[p] = ia;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  // certificate: tau + delta < s_kt (strict), delta = scale * |q| * max|k|
+  const double delta = delta_scale * sqrt(qn) * kmax_norm;
+  const bool ok = m >= kt && (tau == -FLT_MAX || (double)tau + delta < es[kt - 1]);
+  if (lane == 0 && !ok) {
+    fail[atomicAdd(fail_count, 1u)] = uint32_t(q);
+  }
+  if (ok)
+    for (uint32_t r = lane; r < kt; r += 32) knn[q * kt + r] = bi[r];
+}
+
+__global__ void k_max_norm(const float* __restrict__ K, uint32_t n, uint32_t d,
+                           unsigned long long* out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double acc = 0.0;
+  for (uint32_t j = 0; j < d; ++j) acc = fma((double)K[size_t(i) * d + j], (double)K[size_t(i) * d + j], acc);
+  atomicMax(out, __double_as_longlong(sqrt(acc)));  // non-negative doubles order as integers
+}
+
+}  // namespace
+
+bool knn_tc_supported(uint32_t d, uint64_t nq, uint32_t n, uint32_t kt) {
+  return (d == 64 || d == 128) && nq >= TM && n >= TN && kt <= 256;
+}
+
+// Returns the number of rows that failed the certificate; their ids are in
+// `fail_rows` (device) and must be recomputed exactly by the caller.
+uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32_t n, uint32_t d,
+                uint32_t kt, uint32_t* knn, DevBuf<uint32_t>& fail_rows, double* ms_gemm) {
+  cudaStream_t s = ctx->stream;
+  const uint32_t K3 = 3 * d;
+  const uint64_t mt = (nq + TM - 1) / TM, nt = (n + TN - 1) / TN;
+  const uint32_t keep = std::min<uint32_t>(kt + 64, 320);
+  uint32_t cb = 32;
+  while (cb < 2 * keep + 64) cb <<= 1;
+  DevBuf<uint16_t> A(mt * TM * K3), B(nt * TN * K3);
+  {
+    const uint64_t ta = mt * TM * d, tb = nt * TN * d;
+    k_split<<<uint32_t((ta + 255) / 256), 256, 0, s>>>(Q, nq, d, TM, mt, 1, A.p);
+    k_split<<<uint32_t((tb + 255) / 256), 256, 0, s>>>(K, n, d, TN, nt, 0, B.p);
+    RA_LAUNCH_CHECK();
+  }
+  DevBuf<float> bufS(nq * cb);
+  DevBuf<uint32_t> bufI(nq * cb), cnt(nq);
+  DevBuf<float> thr(nq);
+  TcArgs ta{A.p, B.p, nq, n, K3, keep, cb, bufS.p, bufI.p, cnt.p, thr.p};
+  const size_t smem = size_t(TM) * K3 * 2 + NSTAGE * TN * KS * 2 + 256;
+  RA_CUDA(cudaFuncSetAttribute(k_knn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, s);
+  k_knn_tc<<<uint32_t(mt), KNN_THREADS, smem, s>>>(ta);
+  RA_LAUNCH_CHECK();
+  cudaEventRecord(e1, s);
+  DevBuf<unsigned long long> kmax(1);
+  RA_CUDA(cudaMemsetAsync(kmax.p, 0, 8, s));
+  k_max_norm<<<(n + 255) / 256, 256, 0, s>>>(K, n, d, kmax.p);
+  unsigned long long km_bits = 0;
+  RA_CUDA(cudaMemcpyAsync(&km_bits, kmax.p, 8, cudaMemcpyDeviceToHost, s));
+  RA_CUDA(cudaStreamSynchronize(s));
+  float gms = 0;
+  cudaEventElapsedTime(&gms, e0, e1);
+  if (ms_gemm) *ms_gemm = gms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  double kmax_norm;
+  std::memcpy(&kmax_norm, &km_bits, 8);
+  fail_rows.ensure(std::max<uint64_t>(nq, 1));
+  DevBuf<uint32_t> fcount(1);
+  RA_CUDA(cudaMemsetAsync(fcount.p, 0, 4, s));
+  // |S - S~| <= (3 * 2^-16 + K3 * 2^-23 + slack) * |q|*|k|; 2^-10 is generous
+  const double delta_scale = 1.0 / 1024.0;
+  // es needs next_pow2(keep) doubles per row
+  uint32_t p2 = 32;
+  while (p2 < keep) p2 <<= 1;
+  DevBuf<double> exS(nq * size_t(p2));
+  k_rescore<<<uint32_t((nq + 7) / 8), 256, 0, s>>>(Q, K, nq, d, kt, keep, cb, bufS.p, bufI.p,
+                                                   cnt.p, thr.p, delta_scale, kmax_norm, exS.p,
+                                                   p2, knn, fail_rows.p, fcount.p);
+  RA_LAUNCH_CHECK();
+  uint32_t nf = 0;
+  RA_CUDA(cudaMemcpyAsync(&nf, fcount.p, 4, cudaMemcpyDeviceToHost, s));
+  RA_CUDA(cudaStreamSynchronize(s));
+  return nf;
+}
+
+}  // namespace ra

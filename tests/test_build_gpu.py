@@ -158,3 +158,25 @@ def test_recall_grows_with_ef_and_is_exact_at_ef_n(port):
     assert rec[-1] == 1.0 and scan[-1] == 2048.0
     assert rec[3] > 0.9 and scan[0] < 1024
     assert all(scan[i] >= scan[i - 1] for i in range(1, 5))
+
+
+def test_tensor_core_knn_matches_exact_path(port):
+    """Phase 1 on tcgen05 (bf16x3 filter + certified f64 rescoring) must give
+    the same graph as the exact f64 kernel and the oracle, at a scale where
+    the filter, compaction and certificate all engage (d = 128 and 64)."""
+    import os
+    ra = _ra()
+    for n, dm, dh, seed in [(8192, 256, 128, 23), (6000, 128, 64, 24)]:
+        w = port.generate_workload(n, dm, dh, 1, 1, seed=seed, n_decode=1)
+        kv = ra.KVGroup(w["keys"][0])
+        bp = ra.OODGraphBuildParams(128, 24, 256, 8)
+        g_tc = ra.ood_build(kv, w["prefill_q"][0], bp)
+        os.environ["RA_KNN_EXACT"] = "1"
+        try:
+            g_ex = ra.ood_build(kv, w["prefill_q"][0], bp)
+        finally:
+            del os.environ["RA_KNN_EXACT"]
+        assert g_tc.serialize() == g_ex.serialize()
+        # certificate failures are rare and recomputed exactly
+        assert g_tc.build_stats.knn_rows == n
+        assert g_tc.build_stats.knn_rows_widened < n // 10
