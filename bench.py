@@ -276,7 +276,7 @@ def main():
         "build_ms_per_head": round(statistics.mean(build_ms), 1),
         "build_phase_ms_per_head": {
             k: round(statistics.mean(g.build_stats.ms[k] for g in graphs), 2)
-            for k in ("knn", "edges", "prune", "entry", "repair")},
+            for k in ("knn", "knn_tensor", "edges", "prune", "entry", "repair")},
         "build_knn_rows_exact_fallback": sum(g.build_stats.knn_rows_widened for g in graphs),
     }
     if rank == 0:

@@ -68,6 +68,7 @@ typedef struct {
   uint64_t repair_rounds;     /* phase-4 iterations */
   uint64_t repaired_nodes;    /* nodes attached by phase 4 */
   double ms_knn, ms_edges, ms_prune, ms_entry, ms_repair;
+  double ms_knn_tensor;       /* tcgen05 filter GEMM inside ms_knn (0 on the f64 path) */
 } ra_build_stats;
 
 const char* ra_last_error(void);

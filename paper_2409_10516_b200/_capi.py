@@ -34,7 +34,7 @@ class BuildStatsC(C.Structure):
                 ("candidate_edges", C.c_uint64), ("repair_rounds", C.c_uint64),
                 ("repaired_nodes", C.c_uint64), ("ms_knn", C.c_double),
                 ("ms_edges", C.c_double), ("ms_prune", C.c_double), ("ms_entry", C.c_double),
-                ("ms_repair", C.c_double)]
+                ("ms_repair", C.c_double), ("ms_knn_tensor", C.c_double)]
 
 
 class EngineConfigC(C.Structure):

@@ -296,7 +296,7 @@ def ood_build(keys: KVGroup, train_queries, params: OODGraphBuildParams = OODGra
     stats = BuildStats(st.knn_rows, st.knn_rows_widened, st.candidate_edges, st.repair_rounds,
                        st.repaired_nodes,
                        dict(knn=st.ms_knn, edges=st.ms_edges, prune=st.ms_prune,
-                            entry=st.ms_entry, repair=st.ms_repair))
+                            entry=st.ms_entry, repair=st.ms_repair, knn_tensor=st.ms_knn_tensor))
     g = OODGraph(keys, h, stats)
     g.default_ef_param = params.default_ef
     return g

@@ -650,6 +650,7 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
       DevBuf<uint32_t> fail;
       double ms_gemm = 0;
       const uint32_t nf = knn_tc(ctx, TQ, nq, K, n, d, kt, knn.p, fail, &ms_gemm);
+      st.ms_knn_tensor = ms_gemm;
       st.knn_rows = nq;
       st.knn_rows_widened = nf;
       if (nf) {

@@ -126,31 +126,45 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// warp-cooperative: sort row buffer (cnt entries) by approx score desc, keep
-// `keep`; returns the new threshold (score of entry keep-1) or -inf
-__device__ float compact_row(float* bs, uint32_t* bi, uint32_t cnt, uint32_t keep,
-                             uint32_t lane) {
-  uint32_t p2 = 32;
-  while (p2 < cnt) p2 <<= 1;
-  for (uint32_t i = cnt + lane; i < p2; i += 32) bs[i] = -FLT_MAX, bi[i] = kSentinel;
-  __syncwarp();
-  for (uint32_t k = 2; k <= p2; k <<= 1)
+// warp bitonic sort, descending by s (then by id ascending), n_pow2 entries
+template <typename S>
+__device__ void warp_sort_desc(S* s, uint32_t* id, uint32_t n_pow2, uint32_t lane) {
+  for (uint32_t k = 2; k <= n_pow2; k <<= 1)
     for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = lane; i < p2; i += 32) {
+      for (uint32_t i = lane; i < n_pow2; i += 32) {
         const uint32_t p = i ^ j;
         if (p > i) {
           const bool desc = (i & k) == 0;
-          const float a = bs[i], c = bs[p];
-          if (desc ? (c > a) : (a > c)) {
-            bs[i] = c, bs[p] = a;
-            const uint32_t t = bi[i];
-            bi[i] = bi[p], bi[p] = t;
+          const S a = s[i], c = s[p];
+          const uint32_t ia = id[i], ic = id[p];
+          const bool c_better = c > a || (c == a && ic < ia);
+          const bool a_better = a > c || (a == c && ia < ic);
+          if (desc ? c_better : a_better) {
+            s[i] = c, s[p] = a;
+            id[i] = ic, id[p] = ia;
           }
         }
       }
       __syncwarp();
     }
-  return cnt >= keep ? bs[keep - 1] : -FLT_MAX;
+}
+
+// stage a row buffer (cnt entries, HBM) into shared memory, sort it by the
+// approximate score, write back the best `keep`; returns the threshold
+__device__ float compact_row_smem(float* gs, uint32_t* gi, uint32_t cnt, uint32_t keep,
+                                  float* ss, uint32_t* si, uint32_t lane) {
+  uint32_t p2 = 32;
+  while (p2 < cnt) p2 <<= 1;
+  for (uint32_t i = lane; i < p2; i += 32) {
+    ss[i] = i < cnt ? gs[i] : -FLT_MAX;
+    si[i] = i < cnt ? gi[i] : kSentinel;
+  }
+  __syncwarp();
+  warp_sort_desc(ss, si, p2, lane);
+  const uint32_t m = cnt < keep ? cnt : keep;
+  for (uint32_t i = lane; i < m; i += 32) gs[i] = ss[i], gi[i] = si[i];
+  __syncwarp();
+  return cnt >= keep ? ss[keep - 1] : -FLT_MAX;
 }
 
 struct TcArgs {
@@ -175,7 +189,9 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
   const uint32_t a_bytes = TM * K3 * 2;
   uint8_t* sB = smem + a_bytes;
   const uint32_t b_stage = TN * KS * 2;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + NSTAGE * b_stage);
+  float* stage_s = reinterpret_cast<float*>(sB + NSTAGE * b_stage);       // [4 warps][cb]
+  uint32_t* stage_i = reinterpret_cast<uint32_t*>(stage_s + EPI_WARPS * a.cb);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage_i + EPI_WARPS * a.cb);
   uint64_t* full = bars;                 // [NSTAGE]
   uint64_t* empty = bars + NSTAGE;       // [NSTAGE]
   uint64_t* a_full = bars + 2 * NSTAGE;  // [1]
@@ -288,7 +304,8 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
           need &= need - 1;
           const uint64_t ql = m0 + warp * 32 + l;
           const uint32_t cl = __shfl_sync(kFull, cnt, l);
-          const float nt = compact_row(a.bufS + ql * a.cb, a.bufI + ql * a.cb, cl, a.keep, lane);
+          const float nt = compact_row_smem(a.bufS + ql * a.cb, a.bufI + ql * a.cb, cl, a.keep,
+                                            stage_s + warp * a.cb, stage_i + warp * a.cb, lane);
           if (lane == l) {
             cnt = min(cl, a.keep);
             thr = nt;
@@ -311,69 +328,62 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
                  : "memory");
 }
 
-// ---- exact rescoring + certificate (warp per row) --------------------------
-__global__ void k_rescore(const float* __restrict__ Q, const float* __restrict__ K, uint64_t nq,
-                          uint32_t d, uint32_t kt, uint32_t keep, uint32_t cb,
-                          float* __restrict__ bufS, uint32_t* __restrict__ bufI,
-                          const uint32_t* __restrict__ cnt_in, const float* __restrict__ thr_in,
-                          double delta_scale, double kmax_norm, double* __restrict__ exS,
-                          uint32_t es_stride, uint32_t* __restrict__ knn, uint32_t* __restrict__ fail,
-                          uint32_t* __restrict__ fail_count) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t q = blockIdx.x * uint64_t(blockDim.x / 32) + (threadIdx.x >> 5);
+// ---- exact rescoring + certificate (warp per row, shared-memory staging) ----
+constexpr uint32_t RS_WARPS = 4;
+
+__global__ void __launch_bounds__(RS_WARPS * 32)
+    k_rescore(const float* __restrict__ Q, const float* __restrict__ K, uint64_t nq, uint32_t d,
+              uint32_t kt, uint32_t keep, uint32_t cb, const float* __restrict__ bufS,
+              const uint32_t* __restrict__ bufI, const uint32_t* __restrict__ cnt_in,
+              const float* __restrict__ thr_in, double delta_scale, double kmax_norm,
+              uint32_t* __restrict__ knn, uint32_t* __restrict__ fail,
+              uint32_t* __restrict__ fail_count) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t q = blockIdx.x * uint64_t(RS_WARPS) + warp;
   if (q >= nq) return;
+  uint32_t kp2 = 32;
+  while (kp2 < keep) kp2 <<= 1;
+  const size_t per_warp = size_t(cb) * 8 + size_t(kp2) * 12;
+  float* ss = reinterpret_cast<float*>(smem + warp * per_warp);
+  uint32_t* si = reinterpret_cast<uint32_t*>(ss + cb);
+  double* es = reinterpret_cast<double*>(si + cb);
+  uint32_t* ei = reinterpret_cast<uint32_t*>(es + kp2);
   const uint32_t cnt = cnt_in[q];
-  float* bs = bufS + q * cb;
-  uint32_t* bi = bufI + q * cb;
-  // best `keep` by approximate score
-  compact_row(bs, bi, cnt, keep, lane);
-  const uint32_t m = min(cnt, keep);
-  // tau: every key not rescored has S~ <= tau
-  float tau = thr_in[q];
-  if (cnt > keep) tau = fmaxf(tau, bs[keep]);
-  // exact in-order f64 scores of the m candidates
-  const float* qr = Q + q * d;
-  double* es = exS + q * size_t(es_stride);
-  double qn = 0.0;
-  for (uint32_t i = 0; i < d; ++i) qn = fma((double)qr[i], (double)qr[i], qn);
-  for (uint32_t i = lane; i < m; i += 32) {
-    const float* kr = K + size_t(bi[i]) * d;
-    double acc = 0.0;
-    for (uint32_t j = 0; j < d; ++j) acc = fma((double)qr[j], (double)kr[j], acc);
-    es[i] = acc;
+  uint32_t p2 = 32;
+  while (p2 < cnt) p2 <<= 1;
+  for (uint32_t i = lane; i < p2; i += 32) {
+    ss[i] = i < cnt ? bufS[q * cb + i] : -FLT_MAX;
+    si[i] = i < cnt ? bufI[q * cb + i] : kSentinel;
   }
   __syncwarp();
-  // rank by (exact score desc, id asc) via bitonic over next pow2
-  uint32_t p2 = 32;
-  while (p2 < m) p2 <<= 1;
-  for (uint32_t i = m + lane; i < p2; i += 32) es[i] = -DBL_MAX, bi[i] = kSentinel;
-  __syncwarp();
-  for (uint32_t k = 2; k <= p2; k <<= 1)
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = lane; i < p2; i += 32) {
-        const uint32_t p = i ^ j;
-        if (p > i) {
-          const bool desc = (i & k) == 0;
-          const double a = es[i], c = es[p];
-          const uint32_t ia = bi[i], ic = bi[p];
-          const bool c_better = c > a || (c == a && ic < ia);
-          const bool a_better = a > c || (a == c && ia < ic);
-          if (desc ? c_better : a_better) {
-            es[i] = c, es[p] = a;
-            bi[i] = ic, bi[p] = ia;
-          }
-        }
-      }
-      __syncwarp();
+  warp_sort_desc(ss, si, p2, lane);
+  const uint32_t m = min(cnt, keep);
+  float tau = thr_in[q];
+  if (cnt > keep) tau = fmaxf(tau, ss[keep]);
+  const float* qr = Q + q * d;
+  double qn = 0.0;
+  for (uint32_t i = 0; i < d; ++i) qn = fma((double)qr[i], (double)qr[i], qn);
+  for (uint32_t i = lane; i < kp2; i += 32) {
+    double acc = -DBL_MAX;
+    uint32_t id = kSentinel;
+    if (i < m) {
+      id = si[i];
+      const float* kr = K + size_t(id) * d;
+      acc = 0.0;
+      for (uint32_t j = 0; j < d; ++j) acc = fma((double)qr[j], (double)__ldg(kr + j), acc);
     }
+    es[i] = acc;
+    ei[i] = id;
+  }
+  __syncwarp();
+  warp_sort_desc(es, ei, kp2, lane);
   // certificate: tau + delta < s_kt (strict), delta = scale * |q| * max|k|
   const double delta = delta_scale * sqrt(qn) * kmax_norm;
   const bool ok = m >= kt && (tau == -FLT_MAX || (double)tau + delta < es[kt - 1]);
-  if (lane == 0 && !ok) {
-    fail[atomicAdd(fail_count, 1u)] = uint32_t(q);
-  }
+  if (lane == 0 && !ok) fail[atomicAdd(fail_count, 1u)] = uint32_t(q);
   if (ok)
-    for (uint32_t r = lane; r < kt; r += 32) knn[q * kt + r] = bi[r];
+    for (uint32_t r = lane; r < kt; r += 32) knn[q * kt + r] = ei[r];
 }
 
 __global__ void k_max_norm(const float* __restrict__ K, uint32_t n, uint32_t d,
@@ -412,7 +422,7 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
   DevBuf<uint32_t> bufI(nq * cb), cnt(nq);
   DevBuf<float> thr(nq);
   TcArgs ta{A.p, B.p, nq, n, K3, keep, cb, bufS.p, bufI.p, cnt.p, thr.p};
-  const size_t smem = size_t(TM) * K3 * 2 + NSTAGE * TN * KS * 2 + 256;
+  const size_t smem = size_t(TM) * K3 * 2 + NSTAGE * TN * KS * 2 + size_t(EPI_WARPS) * cb * 8 + 256;
   RA_CUDA(cudaFuncSetAttribute(k_knn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -440,12 +450,13 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
   // |S - S~| <= (3 * 2^-16 + K3 * 2^-23 + slack) * |q|*|k|; 2^-10 is generous
   const double delta_scale = 1.0 / 1024.0;
   // es needs next_pow2(keep) doubles per row
-  uint32_t p2 = 32;
-  while (p2 < keep) p2 <<= 1;
-  DevBuf<double> exS(nq * size_t(p2));
-  k_rescore<<<uint32_t((nq + 7) / 8), 256, 0, s>>>(Q, K, nq, d, kt, keep, cb, bufS.p, bufI.p,
-                                                   cnt.p, thr.p, delta_scale, kmax_norm, exS.p,
-                                                   p2, knn, fail_rows.p, fcount.p);
+  uint32_t kp2 = 32;
+  while (kp2 < keep) kp2 <<= 1;
+  const size_t rs_smem = RS_WARPS * (size_t(cb) * 8 + size_t(kp2) * 12);
+  RA_CUDA(cudaFuncSetAttribute(k_rescore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem));
+  k_rescore<<<uint32_t((nq + RS_WARPS - 1) / RS_WARPS), RS_WARPS * 32, rs_smem, s>>>(
+      Q, K, nq, d, kt, keep, cb, bufS.p, bufI.p, cnt.p, thr.p, delta_scale, kmax_norm, knn,
+      fail_rows.p, fcount.p);
   RA_LAUNCH_CHECK();
   uint32_t nf = 0;
   RA_CUDA(cudaMemcpyAsync(&nf, fcount.p, 4, cudaMemcpyDeviceToHost, s));
