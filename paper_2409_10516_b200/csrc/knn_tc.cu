@@ -10,14 +10,17 @@
 //      (tcgen05.mma kind::f16, M=128, N=256, fp32 accumulators in TMEM,
 //      double-buffered). Warp-specialised: warp 4 = TMA producer, warp 5 =
 //      MMA issuer (one thread), warps 0-3 = epilogue (thread = query row:
-//      tcgen05.ld, keep S~ > row threshold in an HBM candidate buffer,
-//      warp-cooperative compaction raises the threshold). The nq x n score
-//      matrix never exists.
-//   3. k_rescore: per row, sort candidates by S~, rescore the best K in the
-//      reference's exact in-order f64 dot, rank (score desc, id asc), and
-//      certify: every key not rescored has S~ <= tau, and |S - S~| <= delta
-//      (bf16 split + fp32 accumulation bound), so tau + delta < s_kt proves
-//      the top-kt is exact. Rows that fail go to the exact f64 kernel.
+//      tcgen05.ld, append keys with S~ > the row threshold to an HBM
+//      survivor buffer). The nq x n score matrix never exists. The row
+//      threshold comes from a first, cheap pass of the same kernel over a
+//      strided 2048-key sample (k_select_thr: r-th largest, ~640 expected
+//      survivors per row).
+//   3. k_rescore: every survivor is rescored with the reference's exact
+//      in-order f64 dot, the kt-th exact score is radix-selected, and the
+//      row is certified: every key not kept has S~ <= thr and
+//      |S - S~| <= delta (bf16 split + fp32 accumulation bound), so
+//      thr + delta < s_kt proves the (score desc, id asc) top-kt exact.
+//      Rows that fail (or overflow the buffer) go to the exact f64 kernel.
 #include <cfloat>
 #include <cstdint>
 #include <cstring>
@@ -149,33 +152,15 @@ __device__ void warp_sort_desc(S* s, uint32_t* id, uint32_t n_pow2, uint32_t lan
     }
 }
 
-// stage a row buffer (cnt entries, HBM) into shared memory, sort it by the
-// approximate score, write back the best `keep`; returns the threshold
-__device__ float compact_row_smem(float* gs, uint32_t* gi, uint32_t cnt, uint32_t keep,
-                                  float* ss, uint32_t* si, uint32_t lane) {
-  uint32_t p2 = 32;
-  while (p2 < cnt) p2 <<= 1;
-  for (uint32_t i = lane; i < p2; i += 32) {
-    ss[i] = i < cnt ? gs[i] : -FLT_MAX;
-    si[i] = i < cnt ? gi[i] : kSentinel;
-  }
-  __syncwarp();
-  warp_sort_desc(ss, si, p2, lane);
-  const uint32_t m = cnt < keep ? cnt : keep;
-  for (uint32_t i = lane; i < m; i += 32) gs[i] = ss[i], gi[i] = si[i];
-  __syncwarp();
-  return cnt >= keep ? ss[keep - 1] : -FLT_MAX;
-}
-
 struct TcArgs {
-  const uint16_t* A;  // [mtiles][TM x K3] blocked
-  const uint16_t* B;  // [ntiles][TN x K3] blocked
+  const uint16_t* A;     // [mtiles][TM x K3] blocked
+  const uint16_t* B;     // [ntiles][TN x K3] blocked
   uint64_t nq;
-  uint32_t n, K3, keep, cb;
-  float* bufS;        // [nq][cb]
+  uint32_t n, K3, cb;
+  const float* thr_in;   // [nq] keep S~ > thr (nullptr: keep all)
+  float* bufS;           // [nq][cb]
   uint32_t* bufI;
-  uint32_t* cnt_out;  // [nq]
-  float* thr_out;     // [nq]
+  uint32_t* cnt_out;     // [nq]; cb + 1 = overflow
 };
 
 __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
@@ -189,9 +174,7 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
   const uint32_t a_bytes = TM * K3 * 2;
   uint8_t* sB = smem + a_bytes;
   const uint32_t b_stage = TN * KS * 2;
-  float* stage_s = reinterpret_cast<float*>(sB + NSTAGE * b_stage);       // [4 warps][cb]
-  uint32_t* stage_i = reinterpret_cast<uint32_t*>(stage_s + EPI_WARPS * a.cb);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stage_i + EPI_WARPS * a.cb);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + NSTAGE * b_stage);
   uint64_t* full = bars;                 // [NSTAGE]
   uint64_t* empty = bars + NSTAGE;       // [NSTAGE]
   uint64_t* a_full = bars + 2 * NSTAGE;  // [1]
@@ -273,11 +256,11 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
       }
     }
   } else {
-    // ---- epilogue: thread = query row ----
+    // ---- epilogue: thread = query row; keep S~ > thr (no compaction) ----
     const uint32_t row = warp * 32 + lane;
     const uint64_t q = m0 + row;
     const bool valid_row = q < a.nq;
-    float thr = -FLT_MAX;
+    const float thr = (valid_row && a.thr_in) ? a.thr_in[q] : -FLT_MAX;
     uint32_t cnt = 0;
     float* bs = a.bufS + (valid_row ? q : 0) * size_t(a.cb);
     uint32_t* bi = a.bufI + (valid_row ? q : 0) * size_t(a.cb);
@@ -292,23 +275,11 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           if (valid_row && key0 + j < a.n && v[j] > thr) {
-            bs[cnt] = v[j];
-            bi[cnt] = key0 + j;
-            ++cnt;
-          }
-        }
-        // a full buffer is compacted by the whole warp (rare after warm-up)
-        uint32_t need = __ballot_sync(kFull, cnt + 32 > a.cb);
-        while (need) {
-          const uint32_t l = __ffs(need) - 1;
-          need &= need - 1;
-          const uint64_t ql = m0 + warp * 32 + l;
-          const uint32_t cl = __shfl_sync(kFull, cnt, l);
-          const float nt = compact_row_smem(a.bufS + ql * a.cb, a.bufI + ql * a.cb, cl, a.keep,
-                                            stage_s + warp * a.cb, stage_i + warp * a.cb, lane);
-          if (lane == l) {
-            cnt = min(cl, a.keep);
-            thr = nt;
+            if (cnt < a.cb) {
+              bs[cnt] = v[j];
+              bi[cnt] = key0 + j;
+            }
+            cnt = min(cnt + 1, a.cb + 1);
           }
         }
       }
@@ -316,10 +287,7 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
       __syncwarp();
       if (lane == 0) mbar_arrive(t_empty + buf);
     }
-    if (valid_row) {
-      a.cnt_out[q] = cnt;
-      a.thr_out[q] = thr;
-    }
+    if (valid_row) a.cnt_out[q] = cnt;
   }
   fence_before();
   __syncthreads();
@@ -328,62 +296,154 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
                  : "memory");
 }
 
-// ---- exact rescoring + certificate (warp per row, shared-memory staging) ----
-constexpr uint32_t RS_WARPS = 4;
+// ---- per-row threshold from the sample pass: r-th largest S~ ------------------
+__global__ void k_select_thr(const float* __restrict__ bufS, const uint32_t* __restrict__ cnt,
+                             uint64_t nq, uint32_t cb, uint32_t r, float* __restrict__ thr) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t q = blockIdx.x * uint64_t(blockDim.x / 32) + (threadIdx.x >> 5);
+  if (q >= nq) return;
+  const uint32_t c = min(cnt[q], cb);
+  const float* bs = bufS + q * cb;
+  float last = FLT_MAX;  // r rounds of "largest value below the previous pick"
+  uint32_t taken = 0;
+  float res = -FLT_MAX;
+  while (taken < r) {
+    float m = -FLT_MAX;
+    for (uint32_t i = lane; i < c; i += 32) {
+      const float v = bs[i];
+      if (v < last) m = fmaxf(m, v);
+    }
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+    if (m == -FLT_MAX) break;
+    uint32_t mult = 0;  // multiplicity of m
+    for (uint32_t i = lane; i < c; i += 32) mult += bs[i] == m;
+    for (int o = 16; o; o >>= 1) mult += __shfl_xor_sync(kFull, mult, o);
+    taken += mult;
+    last = m;
+    res = m;
+  }
+  if (lane == 0) thr[q] = taken >= r ? res : -FLT_MAX;
+}
+
+// ---- exact rescoring of every survivor + certificate (warp per row) ----------
+constexpr uint32_t RS_WARPS = 2;
+
+__device__ __forceinline__ uint64_t okey(double x) {  // order-preserving
+  const uint64_t u = __double_as_longlong(x);
+  return (u >> 63) ? ~u : (u | (1ull << 63));
+}
 
 __global__ void __launch_bounds__(RS_WARPS * 32)
     k_rescore(const float* __restrict__ Q, const float* __restrict__ K, uint64_t nq, uint32_t d,
-              uint32_t kt, uint32_t keep, uint32_t cb, const float* __restrict__ bufS,
-              const uint32_t* __restrict__ bufI, const uint32_t* __restrict__ cnt_in,
-              const float* __restrict__ thr_in, double delta_scale, double kmax_norm,
-              uint32_t* __restrict__ knn, uint32_t* __restrict__ fail,
-              uint32_t* __restrict__ fail_count) {
+              uint32_t kt, uint32_t cb, const uint32_t* __restrict__ bufI,
+              const uint32_t* __restrict__ cnt_in, const float* __restrict__ thr_in,
+              double delta_scale, double kmax_norm, uint32_t* __restrict__ knn,
+              uint32_t* __restrict__ fail, uint32_t* __restrict__ fail_count) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t q = blockIdx.x * uint64_t(RS_WARPS) + warp;
   if (q >= nq) return;
-  uint32_t kp2 = 32;
-  while (kp2 < keep) kp2 <<= 1;
-  const size_t per_warp = size_t(cb) * 8 + size_t(kp2) * 12;
-  float* ss = reinterpret_cast<float*>(smem + warp * per_warp);
-  uint32_t* si = reinterpret_cast<uint32_t*>(ss + cb);
-  double* es = reinterpret_cast<double*>(si + cb);
-  uint32_t* ei = reinterpret_cast<uint32_t*>(es + kp2);
+  const size_t per_warp = size_t(cb) * 12 + 256 * 4;
+  double* es = reinterpret_cast<double*>(smem + warp * per_warp);
+  uint32_t* ei = reinterpret_cast<uint32_t*>(es + cb);
+  uint32_t* hist = ei + cb;
   const uint32_t cnt = cnt_in[q];
-  uint32_t p2 = 32;
-  while (p2 < cnt) p2 <<= 1;
-  for (uint32_t i = lane; i < p2; i += 32) {
-    ss[i] = i < cnt ? bufS[q * cb + i] : -FLT_MAX;
-    si[i] = i < cnt ? bufI[q * cb + i] : kSentinel;
-  }
-  __syncwarp();
-  warp_sort_desc(ss, si, p2, lane);
-  const uint32_t m = min(cnt, keep);
-  float tau = thr_in[q];
-  if (cnt > keep) tau = fmaxf(tau, ss[keep]);
-  const float* qr = Q + q * d;
-  double qn = 0.0;
-  for (uint32_t i = 0; i < d; ++i) qn = fma((double)qr[i], (double)qr[i], qn);
-  for (uint32_t i = lane; i < kp2; i += 32) {
-    double acc = -DBL_MAX;
-    uint32_t id = kSentinel;
-    if (i < m) {
-      id = si[i];
+  const float thr = thr_in ? thr_in[q] : -FLT_MAX;
+  bool ok = cnt <= cb && cnt >= kt;
+  if (ok) {
+    const float* qr = Q + q * d;
+    for (uint32_t i = lane; i < cnt; i += 32) {  // the reference's in-order f64 dot
+      const uint32_t id = bufI[q * cb + i];
       const float* kr = K + size_t(id) * d;
-      acc = 0.0;
+      double acc = 0.0;
       for (uint32_t j = 0; j < d; ++j) acc = fma((double)qr[j], (double)__ldg(kr + j), acc);
+      es[i] = acc;
+      ei[i] = id;
     }
-    es[i] = acc;
-    ei[i] = id;
+    __syncwarp();
+    // radix-select the kt-th largest exact score (8 bits per pass)
+    uint64_t prefix = 0, pmask = 0;
+    uint32_t need = kt;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (uint32_t b = lane; b < 256; b += 32) hist[b] = 0;
+      __syncwarp();
+      for (uint32_t i = lane; i < cnt; i += 32) {
+        const uint64_t k = okey(es[i]);
+        if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+      }
+      __syncwarp();
+      // walk buckets from the top: lane l owns buckets 255-8l .. 248-8l
+      uint32_t local = 0;
+      for (int j = 0; j < 8; ++j) local += hist[255 - (lane * 8 + j)];
+      uint32_t incl = local;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, incl, o);
+        if (lane >= uint32_t(o)) incl += t;
+      }
+      const uint32_t excl = incl - local;
+      const uint32_t owner = __ffs(__ballot_sync(kFull, excl < need && incl >= need)) - 1;
+      uint32_t digit = 0, before = 0;
+      if (lane == owner) {
+        uint32_t acc = excl;
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t bkt = 255 - (lane * 8 + j);
+          if (acc + hist[bkt] >= need) {
+            digit = bkt;
+            before = acc;
+            break;
+          }
+          acc += hist[bkt];
+        }
+      }
+      digit = __shfl_sync(kFull, digit, owner);
+      before = __shfl_sync(kFull, before, owner);
+      need -= before;
+      prefix |= uint64_t(digit) << shift;
+      pmask |= uint64_t(255) << shift;
+      __syncwarp();
+    }
+    // prefix = key of the kt-th largest; certificate tau + delta < s_kt
+    double qn = 0.0;
+    for (uint32_t i = 0; i < d; ++i) qn = fma((double)qr[i], (double)qr[i], qn);
+    const uint64_t u = (prefix >> 63) ? (prefix & ~(1ull << 63)) : ~prefix;
+    const double s_kt = __longlong_as_double(u);
+    const double delta = delta_scale * sqrt(qn) * kmax_norm;
+    ok = thr == -FLT_MAX || (double)thr + delta < s_kt;
+    if (ok) {
+      // gather entries >= s_kt (kt + ties), sort (score desc, id asc), emit kt
+      uint32_t base = 0;
+      for (uint32_t c0 = 0; c0 < cnt; c0 += 32) {
+        const uint32_t i = c0 + lane;
+        const bool take = i < cnt && es[i] >= s_kt;
+        const double sv = take ? es[i] : 0.0;
+        const uint32_t iv = take ? ei[i] : 0;
+        const uint32_t m = __ballot_sync(kFull, take);
+        __syncwarp();
+        if (take) {  // compact in place: destination index <= source index
+          const uint32_t o = base + __popc(m & ((1u << lane) - 1u));
+          es[o] = sv;
+          ei[o] = iv;
+        }
+        base += __popc(m);
+        __syncwarp();
+      }
+      uint32_t p2 = 32;
+      while (p2 < base) p2 <<= 1;
+      for (uint32_t i = base + lane; i < p2; i += 32) es[i] = -DBL_MAX, ei[i] = kSentinel;
+      __syncwarp();
+      warp_sort_desc(es, ei, p2, lane);
+      for (uint32_t r = lane; r < kt; r += 32) knn[q * kt + r] = ei[r];
+    }
   }
-  __syncwarp();
-  warp_sort_desc(es, ei, kp2, lane);
-  // certificate: tau + delta < s_kt (strict), delta = scale * |q| * max|k|
-  const double delta = delta_scale * sqrt(qn) * kmax_norm;
-  const bool ok = m >= kt && (tau == -FLT_MAX || (double)tau + delta < es[kt - 1]);
   if (lane == 0 && !ok) fail[atomicAdd(fail_count, 1u)] = uint32_t(q);
-  if (ok)
-    for (uint32_t r = lane; r < kt; r += 32) knn[q * kt + r] = ei[r];
+}
+
+__global__ void k_gather_sample(const float* __restrict__ K, uint32_t n, uint32_t d, uint32_t m,
+                                float* __restrict__ out) {
+  const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (t >= uint64_t(m) * d) return;
+  const uint64_t s = t / d;
+  out[t] = K[(s * n / m) * d + t % d];
 }
 
 __global__ void k_max_norm(const float* __restrict__ K, uint32_t n, uint32_t d,
@@ -408,9 +468,9 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
   cudaStream_t s = ctx->stream;
   const uint32_t K3 = 3 * d;
   const uint64_t mt = (nq + TM - 1) / TM, nt = (n + TN - 1) / TN;
-  const uint32_t keep = std::min<uint32_t>(kt + 64, 320);
-  uint32_t cb = 32;
-  while (cb < 2 * keep + 64) cb <<= 1;
+  constexpr uint32_t cb = 2048;     // survivor buffer per row
+  constexpr uint32_t msamp = 2048;  // strided key sample for the threshold
+  constexpr uint32_t target = 640;  // expected survivors per row (>= kt w.h.p.)
   DevBuf<uint16_t> A(mt * TM * K3), B(nt * TN * K3);
   {
     const uint64_t ta = mt * TM * d, tb = nt * TN * d;
@@ -418,17 +478,30 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
     k_split<<<uint32_t((tb + 255) / 256), 256, 0, s>>>(K, n, d, TN, nt, 0, B.p);
     RA_LAUNCH_CHECK();
   }
-  DevBuf<float> bufS(nq * cb);
+  DevBuf<float> bufS(nq * cb), thr(nq);
   DevBuf<uint32_t> bufI(nq * cb), cnt(nq);
-  DevBuf<float> thr(nq);
-  TcArgs ta{A.p, B.p, nq, n, K3, keep, cb, bufS.p, bufI.p, cnt.p, thr.p};
-  const size_t smem = size_t(TM) * K3 * 2 + NSTAGE * TN * KS * 2 + size_t(EPI_WARPS) * cb * 8 + 256;
+  const size_t smem = size_t(TM) * K3 * 2 + NSTAGE * TN * KS * 2 + 256;
   RA_CUDA(cudaFuncSetAttribute(k_knn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, s);
-  k_knn_tc<<<uint32_t(mt), KNN_THREADS, smem, s>>>(ta);
+  const bool sampled = n > cb;
+  if (sampled) {
+    // pass 1: S~ against a strided sample; threshold = r-th largest
+    DevBuf<float> ks(size_t(msamp) * d);
+    DevBuf<uint16_t> Bs(size_t(msamp) * K3);
+    k_gather_sample<<<(msamp * d + 255) / 256, 256, 0, s>>>(K, n, d, msamp, ks.p);
+    k_split<<<(msamp * d + 255) / 256, 256, 0, s>>>(ks.p, msamp, d, TN, msamp / TN, 0, Bs.p);
+    TcArgs t1{A.p, Bs.p, nq, msamp, K3, cb, nullptr, bufS.p, bufI.p, cnt.p};
+    k_knn_tc<<<uint32_t(mt), KNN_THREADS, smem, s>>>(t1);
+    const uint32_t r = std::max<uint32_t>(1, uint32_t((uint64_t(target) * msamp + n - 1) / n));
+    k_select_thr<<<uint32_t((nq + 7) / 8), 256, 0, s>>>(bufS.p, cnt.p, nq, cb, r, thr.p);
+    RA_LAUNCH_CHECK();
+  }
+  // pass 2: every key, keep S~ > threshold
+  TcArgs t2{A.p, B.p, nq, n, K3, cb, sampled ? thr.p : nullptr, bufS.p, bufI.p, cnt.p};
+  k_knn_tc<<<uint32_t(mt), KNN_THREADS, smem, s>>>(t2);
   RA_LAUNCH_CHECK();
   cudaEventRecord(e1, s);
   DevBuf<unsigned long long> kmax(1);
@@ -447,15 +520,12 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
   fail_rows.ensure(std::max<uint64_t>(nq, 1));
   DevBuf<uint32_t> fcount(1);
   RA_CUDA(cudaMemsetAsync(fcount.p, 0, 4, s));
-  // |S - S~| <= (3 * 2^-16 + K3 * 2^-23 + slack) * |q|*|k|; 2^-10 is generous
+  // |S - S~| <= (3 * 2^-16 + K3 * 2^-23) * |q| |k|; 2^-10 is generous
   const double delta_scale = 1.0 / 1024.0;
-  // es needs next_pow2(keep) doubles per row
-  uint32_t kp2 = 32;
-  while (kp2 < keep) kp2 <<= 1;
-  const size_t rs_smem = RS_WARPS * (size_t(cb) * 8 + size_t(kp2) * 12);
+  const size_t rs_smem = RS_WARPS * (size_t(cb) * 12 + 256 * 4);
   RA_CUDA(cudaFuncSetAttribute(k_rescore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem));
   k_rescore<<<uint32_t((nq + RS_WARPS - 1) / RS_WARPS), RS_WARPS * 32, rs_smem, s>>>(
-      Q, K, nq, d, kt, keep, cb, bufS.p, bufI.p, cnt.p, thr.p, delta_scale, kmax_norm, knn,
+      Q, K, nq, d, kt, cb, bufI.p, cnt.p, sampled ? thr.p : nullptr, delta_scale, kmax_norm, knn,
       fail_rows.p, fcount.p);
   RA_LAUNCH_CHECK();
   uint32_t nf = 0;
