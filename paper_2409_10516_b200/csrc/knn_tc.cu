@@ -352,14 +352,31 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
   bool ok = cnt <= cb && cnt >= kt;
   if (ok) {
     const float* qr = Q + q * d;
+    // q staged as f64 in the (not yet used) histogram area's tail: d <= 128
+    double* qd = reinterpret_cast<double*>(hist);
+    for (uint32_t j = lane; j < d; j += 32) qd[j] = (double)qr[j];
+    __syncwarp();
     for (uint32_t i = lane; i < cnt; i += 32) {  // the reference's in-order f64 dot
       const uint32_t id = bufI[q * cb + i];
-      const float* kr = K + size_t(id) * d;
+      const float4* kr = reinterpret_cast<const float4*>(K + size_t(id) * d);
       double acc = 0.0;
-      for (uint32_t j = 0; j < d; ++j) acc = fma((double)qr[j], (double)__ldg(kr + j), acc);
+      for (uint32_t c0 = 0; c0 < d / 4; c0 += 8) {  // 8 x 16 B loads in flight per lane
+        float4 b[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) b[c] = __ldg(kr + c0 + c);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const double* qq = qd + 4 * (c0 + c);
+          acc = fma(qq[0], (double)b[c].x, acc);
+          acc = fma(qq[1], (double)b[c].y, acc);
+          acc = fma(qq[2], (double)b[c].z, acc);
+          acc = fma(qq[3], (double)b[c].w, acc);
+        }
+      }
       es[i] = acc;
       ei[i] = id;
     }
+    __syncwarp();
     __syncwarp();
     // radix-select the kt-th largest exact score (8 bits per pass)
     uint64_t prefix = 0, pmask = 0;
