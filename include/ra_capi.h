@@ -123,6 +123,10 @@ uint64_t ra_graph_reachable_count(const ra_graph* g);
 uint64_t ra_graph_memory_bytes(const ra_graph* g);
 /* HBM actually held by the device-side adjacency */
 uint64_t ra_graph_device_bytes(const ra_graph* g);
+/* Copies the reference CSR (offsets_[n+1] u64, adjacency_ u32) into host
+ * arrays sized from ra_graph_size / ra_graph_memory_bytes
+ * (index_oodgraph.hpp:74-75). */
+ra_status ra_graph_csr(const ra_graph* g, uint64_t* offsets, uint32_t* adjacency);
 
 /* ---- search (OODGraph::search, index_oodgraph.cpp:357-411) -----------------
  * B queries; query b searches graphs[b] (graphs may repeat) with q + b*d.
@@ -137,6 +141,14 @@ ra_status ra_graph_search_batch(ra_ctx* ctx, const ra_graph* const* graphs, uint
                                 const uint32_t* mask, uint64_t mask_n, uint32_t* ids,
                                 float* scores, uint32_t* n_out, uint64_t* scanned,
                                 uint8_t* truncated, uint32_t* expanded);
+
+/* Single query on HOST buffers (synchronous): the exact shape of
+ * SearchIndex::search for FFI callers (index.hpp:41-42). ids/scores hold k;
+ * *n_out receives the number written. ef < 0 selects default_ef. */
+ra_status ra_graph_search_host(ra_ctx* ctx, const ra_graph* g, const float* q, uint32_t q_dim,
+                               uint32_t k, int64_t ef, const uint32_t* mask, uint64_t mask_n,
+                               uint32_t* ids, float* scores, uint32_t* n_out, uint64_t* scanned,
+                               uint8_t* truncated);
 
 /* FlatIndex::search (index_flat.cpp:22-43): exact top-k by f64 inner product
  * with the same (score desc, id asc) order. Device pointers as above. */

@@ -73,6 +73,9 @@ _SIGS = {
     "ra_graph_reachable_count": (C.c_uint64, [c_vp]),
     "ra_graph_memory_bytes": (C.c_uint64, [c_vp]),
     "ra_graph_device_bytes": (C.c_uint64, [c_vp]),
+    "ra_graph_csr": (C.c_int, [c_vp, c_u64p, c_u32p]),
+    "ra_graph_search_host": (C.c_int, [c_vp, c_vp, c_f32p, C.c_uint32, C.c_uint32, C.c_int64, c_u32p,
+                                       C.c_uint64, c_u32p, c_f32p, c_u32p, c_u64p, c_u8p]),
     "ra_graph_search_batch": (C.c_int, [c_vp, C.POINTER(c_vp), C.c_uint32, c_vp, C.c_uint32,
                                         C.c_uint32, C.c_int64, c_vp, C.c_uint64, c_vp, c_vp,
                                         c_vp, c_vp, c_vp, c_vp]),

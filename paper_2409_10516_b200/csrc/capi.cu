@@ -256,6 +256,14 @@ uint64_t ra_graph_memory_bytes(const ra_graph* g) {
 }
 uint64_t ra_graph_device_bytes(const ra_graph* g) { return g->adj.bytes(); }
 
+ra_status ra_graph_csr(const ra_graph* g, uint64_t* offsets, uint32_t* adjacency) {
+  return guard([&] {
+    if (!g) invalid("null graph");
+    std::copy(g->offsets.begin(), g->offsets.end(), offsets);
+    std::copy(g->adjacency.begin(), g->adjacency.end(), adjacency);
+  });
+}
+
 // ---- search ------------------------------------------------------------------------------
 ra_status ra_graph_search_batch(ra_ctx* ctx, const ra_graph* const* graphs, uint32_t B,
                                 const float* q, uint32_t q_dim, uint32_t k, int64_t ef,
@@ -306,6 +314,47 @@ ra_status ra_graph_search_batch(ra_ctx* ctx, const ra_graph* const* graphs, uint
     const size_t sbytes = search_scratch_bytes(ctx, B, max_n, q_dim);
     uint8_t* scr = sbytes ? arena<uint8_t>(ctx->scratch_b, sbytes) : nullptr;
     launch_graph_search(ctx, sa, max_n, scr);
+  });
+}
+
+ra_status ra_graph_search_host(ra_ctx* ctx, const ra_graph* g, const float* q, uint32_t q_dim,
+                               uint32_t k, int64_t ef, const uint32_t* mask, uint64_t mask_n,
+                               uint32_t* ids, float* scores, uint32_t* n_out, uint64_t* scanned,
+                               uint8_t* truncated) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (!g) invalid("null graph");
+    if (q_dim != g->kv->d) invalid("query dimension mismatch");  // :359 (checked first)
+    DeviceGuard dg(ctx->device);
+    const uint32_t kk = std::max<uint32_t>(k, 1);
+    // one staging block: q | mask | ids | scores | n_out | scanned | truncated
+    const size_t off_mask = (size_t(q_dim) * 4 + 255) & ~size_t(255);
+    const size_t off_ids = off_mask + ((mask_n * 4 + 255) & ~size_t(255));
+    const size_t off_sc = off_ids + ((size_t(kk) * 4 + 255) & ~size_t(255));
+    const size_t off_n = off_sc + ((size_t(kk) * 4 + 255) & ~size_t(255));
+    const size_t total = off_n + 256;
+    uint8_t* d = arena<uint8_t>(ctx->scratch_c, total);
+    cudaStream_t s = ctx->stream;
+    RA_CUDA(cudaMemcpyAsync(d, q, size_t(q_dim) * 4, cudaMemcpyHostToDevice, s));
+    if (mask_n) RA_CUDA(cudaMemcpyAsync(d + off_mask, mask, mask_n * 4, cudaMemcpyHostToDevice, s));
+    uint32_t* d_n = reinterpret_cast<uint32_t*>(d + off_n);
+    uint64_t* d_sc = reinterpret_cast<uint64_t*>(d + off_n + 8);
+    uint8_t* d_tr = d + off_n + 16;
+    const ra_graph* gs[1] = {g};
+    const ra_status st = ra_graph_search_batch(
+        ctx, gs, 1, reinterpret_cast<const float*>(d), q_dim, k, ef,
+        mask_n ? reinterpret_cast<const uint32_t*>(d + off_mask) : nullptr, mask_n,
+        reinterpret_cast<uint32_t*>(d + off_ids), reinterpret_cast<float*>(d + off_sc), d_n, d_sc,
+        d_tr, nullptr);
+    if (st != RA_OK) throw Error(st, g_last_error);
+    uint32_t n = 0;
+    RA_CUDA(cudaMemcpyAsync(&n, d_n, 4, cudaMemcpyDeviceToHost, s));
+    RA_CUDA(cudaMemcpyAsync(scanned, d_sc, 8, cudaMemcpyDeviceToHost, s));
+    RA_CUDA(cudaMemcpyAsync(truncated, d_tr, 1, cudaMemcpyDeviceToHost, s));
+    RA_CUDA(cudaMemcpyAsync(ids, d + off_ids, size_t(kk) * 4, cudaMemcpyDeviceToHost, s));
+    RA_CUDA(cudaMemcpyAsync(scores, d + off_sc, size_t(kk) * 4, cudaMemcpyDeviceToHost, s));
+    RA_CUDA(cudaStreamSynchronize(s));
+    *n_out = n;
   });
 }
 
