@@ -139,7 +139,8 @@ def main():
     H, G = a.heads, a.groups
     hpg = H // G
     n_world = world if a.impl == "ours" else 1
-    my_groups = list(range(rank * G // n_world, (rank + 1) * G // n_world))
+    from paper_2409_10516_b200.shard import OutputGather, groups_for_rank
+    my_groups = groups_for_rank(G, n_world, rank if a.impl == "ours" else 0)
     n_dec = a.warmup + 2 * a.steps + 2
     spec = WorkloadSpec(n_ctx=a.n_ctx, d_model=256, d_head=128, n_heads=H, n_kv_groups=G,
                         seed=7, n_decode=n_dec)
@@ -175,15 +176,12 @@ def main():
     eng = ra.Engine(kvs, graphs, cfg)
     stream = torch.cuda.current_stream()
     flush = torch.empty(a.flush_mb * (1 << 20) // 4, dtype=torch.float32, device=dev)
-    gather_out = None
-    if dist is not None:
-        gather_out = [torch.empty((Hl, 128), dtype=torch.float64, device=dev)
-                      for _ in range(world)]
+    gather = OutputGather(G, hpg, 128, world, rank, dev) if dist is not None else None
 
     def step(i):
         out, om, sc = eng.decode_step_device(Q[i])
         if dist is not None:
-            dist.all_gather(gather_out, out)
+            gather(out, dist)  # all heads' outputs on every rank (NCCL all_gather)
         return out
 
     for i in range(a.warmup):
