@@ -428,6 +428,62 @@ __global__ void k_mask_bitset(const uint32_t* mask, uint64_t mask_n, uint32_t* b
   }
 }
 
+// order-preserving 64-bit key of a double (larger double -> larger key)
+__device__ __forceinline__ uint64_t okey64(double x) {
+  const uint64_t u = __double_as_longlong(x);
+  return (u >> 63) ? ~u : (u | (1ull << 63));
+}
+__device__ __forceinline__ double okey64_inv(uint64_t k) {
+  return __longlong_as_double((k >> 63) ? (k & ~(1ull << 63)) : ~k);
+}
+// k-th largest value of s[0, n) (k >= 1, n >= k): warp radix select, 8 bits
+// per pass, histogram in shared memory (256 words)
+__device__ double warp_kth_largest(const double* s, uint32_t n, uint32_t k, uint32_t* hist,
+                                   uint32_t lane) {
+  uint64_t prefix = 0, pmask = 0;
+  uint32_t need = k;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (uint32_t b = lane; b < 256; b += 32) hist[b] = 0;
+    __syncwarp();
+    for (uint32_t i = lane; i < n; i += 32) {
+      const uint64_t key = okey64(s[i]);
+      if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    uint32_t local = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) local += hist[255 - (lane * 8 + j)];
+    uint32_t incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= uint32_t(o)) incl += t;
+    }
+    const uint32_t excl = incl - local;
+    const uint32_t owner = __ffs(__ballot_sync(kFull, excl < need && incl >= need)) - 1;
+    uint32_t digit = 0, before = 0;
+    if (lane == owner) {
+      uint32_t acc = excl;
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t bkt = 255 - (lane * 8 + j);
+        if (acc + hist[bkt] >= need) {
+          digit = bkt;
+          before = acc;
+          break;
+        }
+        acc += hist[bkt];
+      }
+    }
+    digit = __shfl_sync(kFull, digit, owner);
+    before = __shfl_sync(kFull, before, owner);
+    need -= before;
+    prefix |= uint64_t(digit) << shift;
+    pmask |= uint64_t(255) << shift;
+    __syncwarp();
+  }
+  return okey64_inv(prefix);
+}
+
 // ---------------------------------------------------------------------------
 // K6 v4: one CTA (4 warps) per query, speculative parallel pre-expansion.
 //
@@ -609,13 +665,23 @@ __global__ void __launch_bounds__(kCW * 32, 1)
 
   // raise thr to the exact pool worst; keep U = pool + worst ties, drop dead F
   auto compact = [&]() {
-    sort_U();
-    thr = U.s[ef - 1];
-    uint32_t keep = ef;
-    for (uint32_t c = ef; c < nU; c += 32) {  // ties with the worst score stay
-      const uint32_t bm = __ballot_sync(kFull, c + lane < nU && U.s[c + lane] >= thr);
+    // exact ef-th best score by radix select (warp 0's TMA tile is idle here)
+    thr = warp_kth_largest(U.s, nU, ef, reinterpret_cast<uint32_t*>(tile), lane);
+    uint32_t keep = 0;  // U keeps everything >= thr (the pool plus worst-score ties)
+    for (uint32_t c = 0; c < nU; c += 32) {
+      const uint32_t i = c + lane;
+      const bool in = i < nU;
+      const double sv = in ? U.s[i] : 0.0;
+      const uint32_t iv = in ? U.id[i] : 0;
+      const bool kp = in && sv >= thr;
+      const uint32_t bm = __ballot_sync(kFull, kp);
+      __syncwarp();
+      if (kp) {
+        const uint32_t o = keep + __popc(bm & ((1u << lane) - 1u));
+        U.s[o] = sv, U.id[o] = iv;
+      }
       keep += __popc(bm);
-      if (bm != kFull) break;
+      __syncwarp();
     }
     nU = keep;
     uint32_t w = 0;
