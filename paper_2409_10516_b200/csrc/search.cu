@@ -511,7 +511,7 @@ __device__ double warp_kth_largest(const double* s, uint32_t n, uint32_t k, uint
 constexpr uint32_t kCW = 4;   // warps per CTA
 constexpr uint32_t kCB = 6;   // candidates pre-expanded per round
 constexpr uint32_t kCP = 16;  // packet slots
-constexpr uint32_t kUSlack = 96;  // U grows to ef + slack before compaction
+constexpr uint32_t kUSlack = 64;  // U grows to ef + slack before compaction
 
 template <int D>
 struct CtaLayout {
@@ -764,28 +764,31 @@ __global__ void __launch_bounds__(kCW * 32, 1)
     }
     warp_sort32(bs, bid, dummy, lane);
     const uint32_t ntop = min(kCB, (uint32_t)__popc(__ballot_sync(kFull, bid != kSentinel)));
-    const uint32_t tops = bid;
-    const uint32_t tag = lane < kCP ? pk_tag[lane] : kSentinel;
-    bool keep = false;
-    for (uint32_t t = 0; t < ntop; ++t) keep |= (tag == __shfl_sync(kFull, tops, t));
-    if (lane < kCP && !keep) pk_tag[lane] = kSentinel;
-    __syncwarp();
-    uint32_t freemask = __ballot_sync(kFull, lane < kCP && !keep);
-    uint32_t nc = 0;
-    for (uint32_t t = 0; t < ntop; ++t) {
-      const uint32_t id = __shfl_sync(kFull, tops, t);
-      const bool has = __ballot_sync(kFull, lane < kCP && tag == id && keep) != 0;
-      if (!has) {
-        const uint32_t sl = __ffs(freemask) - 1;
-        freemask &= freemask - 1;
-        if (lane == 0) {
-          pk_tag[sl] = id;
-          cand[nc] = id;
-          slotof[nc] = sl;
-        }
-        ++nc;
-      }
+    // slot bookkeeping in one match: candidate ids in lanes [0, ntop), packet
+    // tags in lanes [16, 16 + kCP); other lanes hold unique dummies
+    static_assert(kCB <= 16 && kCP <= 16, "slot match layout");
+    const uint32_t tag = lane >= 16 ? pk_tag[lane - 16] : kSentinel;
+    uint32_t val = 0xFFFFFF00u + lane;  // unique dummy (never a node id < n)
+    if (lane < ntop) val = bid;
+    else if (lane >= 16 && tag != kSentinel) val = tag;
+    const uint32_t grp = __match_any_sync(kFull, val);
+    const bool is_top = lane < ntop, is_tag = lane >= 16 && tag != kSentinel;
+    const bool keep = is_tag && (grp & 0xFFFFu & ((1u << ntop) - 1u));  // tag is a top
+    const bool has = is_top && (grp >> 16);                               // top has a packet
+    if (lane >= 16 && !keep) pk_tag[lane - 16] = kSentinel;
+    const uint32_t freemask = __ballot_sync(kFull, lane >= 16 && !keep) >> 16;
+    const uint32_t needmask = __ballot_sync(kFull, is_top && !has);
+    if (is_top && !has) {
+      const uint32_t r = __popc(needmask & ((1u << lane) - 1u));
+      uint32_t fm = freemask;  // r-th free slot
+      for (uint32_t j = 0; j < r; ++j) fm &= fm - 1;
+      const uint32_t sl = __ffs(fm) - 1;
+      pk_tag[sl] = bid;
+      cand[r] = bid;
+      slotof[r] = sl;
     }
+    __syncwarp();
+    const uint32_t nc = __popc(needmask);
     if (lane == 0) ctrl[0] = nc;
   };
 
