@@ -208,6 +208,8 @@ ra_status ra_engine_last_timing(ra_engine* e, float* search_ms, float* attention
  * {rounds, cycles pre-expanding, cycles committing, commits, commit-phase
  * cycles in argmax / stop test / packet apply / add+compact / select, 0,0,0}. */
 ra_status ra_engine_debug_counters(ra_engine* e, uint64_t* out12);
+/* Profiling aid: the same 12 counters per head (out = n_heads x 12). */
+ra_status ra_engine_debug_counters_per_head(ra_engine* e, uint64_t* out);
 
 #ifdef __cplusplus
 }

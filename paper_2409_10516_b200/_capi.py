@@ -95,6 +95,7 @@ _SIGS = {
     "ra_engine_last_stats": (C.c_int, [c_vp, c_u64p, c_u64p]),
     "ra_engine_last_timing": (C.c_int, [c_vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "ra_engine_debug_counters": (C.c_int, [c_vp, c_u64p]),
+    "ra_engine_debug_counters_per_head": (C.c_int, [c_vp, c_u64p]),
 }
 
 EXPORTED = tuple(_SIGS)

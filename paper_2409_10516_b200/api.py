@@ -530,6 +530,13 @@ class Engine:
         return dict(zip(("rounds", "cycles_pre_expand", "cycles_commit", "commits", "cy_argmax",
                          "cy_stop", "cy_packet", "cy_add", "cy_select"), list(out)))
 
+    def debug_counters_per_head(self):
+        """The same counters per head: uint64 array [H, 12]."""
+        out = np.zeros((self.H, 12), dtype=np.uint64)
+        _check(lib.ra_engine_debug_counters_per_head(
+            self.h, out.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return out
+
     def last_stats(self):
         s, e = C.c_uint64(), C.c_uint64()
         _check(lib.ra_engine_last_stats(self.h, C.byref(s), C.byref(e)))

@@ -717,4 +717,13 @@ ra_status ra_engine_debug_counters(ra_engine* e, uint64_t* out12) {
   });
 }
 
+ra_status ra_engine_debug_counters_per_head(ra_engine* e, uint64_t* out) {
+  return guard([&] {
+    if (!e) invalid("null engine");
+    DeviceGuard dg(e->ctx->device);
+    RA_CUDA(cudaMemcpyAsync(out, e->dbg.p, size_t(e->H) * 96, cudaMemcpyDeviceToHost, e->ctx->stream));
+    RA_CUDA(cudaStreamSynchronize(e->ctx->stream));
+  });
+}
+
 }  // extern "C"

@@ -179,11 +179,16 @@ struct SearchArgs {
   // when it does not fit shared memory (per query: ceil(max_n/32) words).
   uint8_t* spill;
   uint32_t* vis_global;
+  uint32_t flags;  // profiling switches (RA_PIPE_FLAGS): 1 = helpers idle
 };
 
 // Returns bytes of scratch needed for (B, max_n, d); then launches.
 size_t search_scratch_bytes(const ra_ctx* ctx, uint32_t B, uint32_t max_n, uint32_t d);
 void launch_graph_search(ra_ctx* ctx, SearchArgs a, uint32_t max_n, uint8_t* scratch);
+// v5 pipelined kernel (search_pipe.cu); false when the shape is unsupported
+size_t search_pipe_scratch_bytes(uint32_t B, uint32_t max_n);
+bool launch_graph_search_pipe(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n,
+                              uint8_t* scratch);
 
 void launch_mask_bitset(cudaStream_t s, const uint32_t* mask, uint64_t mask_n, uint32_t* bits,
                         uint64_t words);

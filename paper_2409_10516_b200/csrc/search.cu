@@ -20,6 +20,8 @@
 // bitset sits in HBM when n is too large for shared memory. No capacity
 // limit is ever exposed to the caller.
 #include <cfloat>
+#include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "tma.cuh"
@@ -1023,7 +1025,7 @@ size_t search_scratch_bytes(const ra_ctx* ctx, uint32_t B, uint32_t max_n, uint3
   size_t bytes = size_t(B) * (((size_t(p2) * 13 + 15) & ~size_t(15)) +
                               ((size_t(p2) * 12 + 15) & ~size_t(15))) + 256;
   bytes += size_t(B) * ((max_n + 31) / 32) * 4 + 256;  // HBM visited bitsets
-  return bytes;
+  return std::max(bytes, search_pipe_scratch_bytes(B, max_n));
 }
 
 struct CtaPlan {
@@ -1077,10 +1079,23 @@ bool try_launch_cta(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* s
   return true;
 }
 
+// RA_SEARCH_KERNEL = pipe (default) | cta | warp selects the K6 variant
+int search_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("RA_SEARCH_KERNEL");
+    if (!e) return 0;
+    const std::string s(e);
+    return s == "cta" ? 1 : s == "warp" ? 2 : 0;
+  }();
+  return v;
+}
+
 void launch_graph_search(ra_ctx* ctx, SearchArgs a, uint32_t max_n, uint8_t* scratch) {
   if (a.B == 0) return;
+  const int variant = search_variant();
+  if (variant == 0 && launch_graph_search_pipe(ctx, a, max_n, scratch)) return;
   // v3 (CTA per query, speculative pre-expansion) for the common shapes
-  if (a.max_M <= 32) {
+  if (a.max_M <= 32 && variant <= 1) {
     bool done = false;
     switch (a.d) {
       case 128: done = try_launch_cta<128>(ctx, a, max_n, scratch); break;

@@ -1,0 +1,778 @@
+// K6 v5 ("pipe"): exact OODGraph::search
+// (/root/reference/proj/src/index_oodgraph.cpp:357-411) as a producer /
+// consumer pipeline inside one CTA per query.
+//
+// Warp 0 (the commit warp) replays the reference loop exactly: frontier top
+// (:387), stop rule (:390), pop, visit the top's neighbours in commit order
+// (:393-399). On a hit it never touches HBM: the neighbours' ids and exact
+// in-order f64 scores come from a "packet" computed ahead of time by one of
+// the helper warps 1..kPW-1. Packets are pure functions of (query, node), so
+// only the committed expansion SET matters and ids / f32 scores / scanned /
+// truncated are bit-identical to the reference (the commit warp re-filters a
+// packet against the visited set at commit time; helpers filter only as a
+// hint, and a stale filter can only add entries).
+//
+// Scores travel as order-preserving u64 keys (-0.0 folded into +0.0, so key
+// equality is double equality); (key desc, id asc) is the reference order.
+//
+// Commit-side state, every operation a few independent instructions:
+//   F (frontier): unexpanded visited nodes with key >= thr. kFR entries per
+//     lane in registers, SORTED per lane (insert = one compare per slot plus
+//     predicated moves, pop = shift); a lane that overflows pushes its worst
+//     entry to the shared overflow FO, whose best entry is tracked exactly.
+//     Frontier top = 3-REDUX argmax of the lane heads vs FO's best.
+//   U (pool candidates): unmasked visited nodes with key >= thr, kUR per
+//     lane (unsorted, free mask) + overflow UO. pool.full() <=> #unmasked
+//     visited >= ef, and top < pool.worst (:390) <=> #{u in U : u > top} >=
+//     ef: 8 compares per lane and one REDUX.
+//   thr: a key with >= ef U entries at or above it, i.e. thr <= pool worst
+//     (key bisection, raised when U outgrows ef + slack). Nodes below the
+//     pool worst can never be popped (the stop rule fires first) nor enter
+//     the pool (its worst only rises), so dropping them is exact.
+// Helpers: read the published lane heads (a hint of the next tops), claim a
+// slot of a direct-mapped packet table with one 64-bit CAS, gather the
+// adjacency row, TMA the unvisited neighbours' key rows into their tile,
+// run the exact chains, publish the packet; then chain greedily into the
+// best new neighbour (the likely next top) while it ranks among the heads.
+#include <cfloat>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "tma.cuh"
+
+#ifdef RA_PIPE_PROFILE
+#define PIPE_TICK(slot)                \
+  {                                    \
+    const uint64_t t_ = clock64();     \
+    cy[slot] += t_ - tq;               \
+    tq = t_;                           \
+  }
+#else
+#define PIPE_TICK(slot)
+#endif
+
+namespace ra {
+namespace {
+
+constexpr uint32_t kPW = 8;        // warps per CTA: 0 commits, 1.. pre-expand
+constexpr int kFR = 8;             // frontier entries per lane (sorted)
+constexpr int kUR = 8;             // pool-candidate entries per lane
+constexpr uint32_t kSlots = 64;    // packet table, direct-mapped by node id
+constexpr uint32_t kSlotBits = 6;
+constexpr uint32_t kPick = 12;     // helpers consider the best kPick heads
+constexpr uint32_t kChain = 3;     // greedy chain depth after a pre-expansion
+constexpr uint32_t kSlackU = 64;   // U grows to ef + slack before thr is raised
+constexpr uint32_t sFREE = 0, sBUSY = 1, sREADY = 2, sTAKEN = 3;
+
+// order-preserving key of a double; -0.0 and +0.0 share a key
+__device__ __forceinline__ uint64_t okey(double x) {
+  const uint64_t u = __double_as_longlong(x + 0.0);
+  return (u >> 63) ? ~u : (u | (1ull << 63));
+}
+__device__ __forceinline__ double okey_inv(uint64_t k) {
+  return __longlong_as_double((k >> 63) ? (k & ~(1ull << 63)) : ~k);
+}
+// (key desc, id asc); the empty entry (0, kSentinel) is worse than any node
+__device__ __forceinline__ bool better(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
+  return ka > kb || (ka == kb && ia < ib);
+}
+__device__ __forceinline__ uint64_t slotword(uint32_t key, uint32_t st) {
+  return (uint64_t(st) << 32) | key;
+}
+__device__ __forceinline__ uint32_t slot_of(uint32_t id) {
+  return (id * 2654435761u) >> (32 - kSlotBits);
+}
+__device__ __forceinline__ uint32_t lanemask_lt(uint32_t lane) { return (1u << lane) - 1u; }
+
+// in-order f64 dot of q (f64, smem) and a key row staged in shared memory
+// (dot_f64, index_oodgraph.cpp:40-44; f32 x f32 products are exact in f64)
+template <int D>
+__device__ __forceinline__ double row_dot(const double* __restrict__ qd,
+                                          const float* __restrict__ row) {
+  double acc = 0.0;
+  const float4* r4 = reinterpret_cast<const float4*>(row);
+#pragma unroll 8
+  for (int c = 0; c < D / 4; ++c) {
+    const float4 k = r4[c];
+    acc = fma(qd[4 * c + 0], (double)k.x, acc);
+    acc = fma(qd[4 * c + 1], (double)k.y, acc);
+    acc = fma(qd[4 * c + 2], (double)k.z, acc);
+    acc = fma(qd[4 * c + 3], (double)k.w, acc);
+  }
+  return acc;
+}
+
+// 32-lane bitonic sort, best-first
+__device__ __forceinline__ void sort32(uint64_t& k, uint32_t& id, uint32_t lane) {
+#pragma unroll
+  for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      const uint64_t ko = __shfl_xor_sync(kFull, k, j);
+      const uint32_t io = __shfl_xor_sync(kFull, id, j);
+      const bool lower = (lane & j) == 0;
+      const bool desc = (lane & kk) == 0;
+      const bool take = (lower == desc) ? better(ko, io, k, id) : better(k, id, ko, io);
+      if (take) k = ko, id = io;
+    }
+  }
+}
+
+// warp argmax under (key desc, id asc) with three REDUX; all lanes get it
+__device__ __forceinline__ void warp_best(uint64_t& k, uint32_t& id) {
+  const uint32_t hi = __reduce_max_sync(kFull, uint32_t(k >> 32));
+  const bool m1 = uint32_t(k >> 32) == hi;
+  const uint32_t lo = __reduce_max_sync(kFull, m1 ? uint32_t(k) : 0u);
+  const bool m2 = m1 && uint32_t(k) == lo;
+  id = __reduce_min_sync(kFull, m2 ? id : kSentinel);
+  k = (uint64_t(hi) << 32) | lo;
+}
+
+struct PipeLayout {
+  uint32_t D, MT, vis_words, vis_smem, capO;
+  static constexpr size_t kBars = 0, kCtrl = 64, kPubK = 128, kPubId = 384, kSlotW = 512,
+                          kCnt = 1024, kMb = 1280, kNk = 1536, kPkId = 2048,
+                          kPkK = kPkId + size_t(kSlots) * 32 * 4,
+                          kQd = kPkK + size_t(kSlots) * 32 * 8;
+  __host__ __device__ size_t row_floats() const { return D + 4; }
+  __host__ __device__ size_t tiles_off() const { return kQd + size_t(D) * 8; }
+  __host__ __device__ size_t tile_bytes() const { return size_t(MT) * row_floats() * 4; }
+  __host__ __device__ size_t vis_off() const { return tiles_off() + kPW * tile_bytes(); }
+  __host__ __device__ size_t vis_bytes() const {
+    return vis_smem ? ((size_t(vis_words) * 8 + 15) & ~size_t(15)) : 0;  // visited + expanded
+  }
+  __host__ __device__ size_t fo_off() const { return vis_off() + vis_bytes(); }
+  __host__ __device__ static size_t arr_bytes(uint32_t c) {
+    return (size_t(c) * 12 + 15) & ~size_t(15);
+  }
+  __host__ __device__ size_t uo_off() const { return fo_off() + arr_bytes(capO); }
+  __host__ __device__ size_t bytes() const { return uo_off() + arr_bytes(capO); }
+};
+
+struct Arr {  // (key, id) array: k u64[cap] then id u32[cap]
+  uint64_t* k;
+  uint32_t* id;
+  __device__ static Arr at(uint8_t* base, uint32_t cap) {
+    Arr a{reinterpret_cast<uint64_t*>(base), nullptr};
+    a.id = reinterpret_cast<uint32_t*>(a.k + cap);
+    return a;
+  }
+};
+
+template <int D, bool VS>
+__global__ void __launch_bounds__(kPW * 32, 1)
+    k_graph_search_pipe(SearchArgs a, PipeLayout lay, uint32_t spill_cap) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t b = blockIdx.x;
+  const GraphDesc g = a.desc[b];
+  const uint32_t M = g.M, ef = g.ef, k = a.k, n = g.n;
+  const float* __restrict__ keys = g.keys;
+  const uint32_t* __restrict__ adj = g.adj;
+  constexpr uint32_t RS = D + 4;
+
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + PipeLayout::kBars) + warp;
+  volatile uint32_t* ctrl = reinterpret_cast<volatile uint32_t*>(smem + PipeLayout::kCtrl);
+  volatile uint64_t* pub_k = reinterpret_cast<volatile uint64_t*>(smem + PipeLayout::kPubK);
+  volatile uint32_t* pub_id = reinterpret_cast<volatile uint32_t*>(smem + PipeLayout::kPubId);
+  unsigned long long* slotw = reinterpret_cast<unsigned long long*>(smem + PipeLayout::kSlotW);
+  uint32_t* pk_cnt = reinterpret_cast<uint32_t*>(smem + PipeLayout::kCnt);
+  uint32_t* pk_mb = reinterpret_cast<uint32_t*>(smem + PipeLayout::kMb);
+  volatile uint64_t* pk_nk = reinterpret_cast<volatile uint64_t*>(smem + PipeLayout::kNk);
+  uint32_t* pk_id = reinterpret_cast<uint32_t*>(smem + PipeLayout::kPkId);
+  uint64_t* pk_k = reinterpret_cast<uint64_t*>(smem + PipeLayout::kPkK);
+  double* qd = reinterpret_cast<double*>(smem + PipeLayout::kQd);
+  float* tile = reinterpret_cast<float*>(smem + lay.tiles_off() + warp * lay.tile_bytes());
+  const uint32_t vw = lay.vis_words;
+  uint32_t* vis = VS ? reinterpret_cast<uint32_t*>(smem + lay.vis_off())
+                     : a.vis_global + size_t(b) * 2 * vw;
+  uint32_t* expd = vis + vw;
+  uint8_t* spill_slot = a.spill + size_t(b) * 2 * PipeLayout::arr_bytes(spill_cap);
+
+  if (lane == 0) mbar_init(bar);
+  for (uint32_t w = threadIdx.x; w < 2 * vw; w += blockDim.x) vis[w] = 0;
+  for (uint32_t i = threadIdx.x; i < D; i += blockDim.x) qd[i] = (double)a.q[size_t(b) * D + i];
+  for (uint32_t i = threadIdx.x; i < kSlots; i += blockDim.x) slotw[i] = slotword(kSentinel, sFREE);
+  if (threadIdx.x < 32) pub_k[threadIdx.x] = 0, pub_id[threadIdx.x] = kSentinel;
+  if (threadIdx.x < 16) ctrl[threadIdx.x] = 0;
+  __syncthreads();
+
+  auto masked_id = [&](uint32_t v) -> bool {
+    return a.mask_bits != nullptr && ((__ldg(a.mask_bits + (v >> 5)) >> (v & 31)) & 1u);
+  };
+  auto vbit = [&](const uint32_t* bits, uint32_t v) -> bool {
+    return (reinterpret_cast<const volatile uint32_t*>(bits)[v >> 5] >> (v & 31)) & 1u;
+  };
+  uint32_t phase = 0;
+  // Expansion of node c by this warp: lane l holds adjacency slot l; `isnew`
+  // lanes hold an unvisited (at read time), first-occurrence neighbour v and
+  // its exact score key. Key rows come through this warp's TMA tile.
+  auto expand = [&](uint32_t c, uint32_t& v, uint64_t& sk, bool& isnew) {
+    v = lane < M ? __ldg(adj + size_t(c) * M + lane) : kSentinel;
+    const bool valid = v != kSentinel;
+    const uint32_t grp = __match_any_sync(kFull, v);
+    const bool first = uint32_t(__ffs(grp) - 1) == lane;
+    isnew = valid && first && !vbit(vis, v);
+    const uint32_t newmask = __ballot_sync(kFull, isnew);
+    sk = 0;
+    if (newmask) {
+      float* row = tile + size_t(__popc(newmask & lanemask_lt(lane))) * RS;
+      fence_proxy_async();
+      if (lane == 0) mbar_arrive_expect_tx(bar, __popc(newmask) * uint32_t(D) * 4u);
+      __syncwarp();
+      if (isnew) bulk_g2s(row, keys + size_t(v) * D, uint32_t(D) * 4u, bar);
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+      if (isnew) sk = okey(row_dot<D>(qd, row));
+    }
+  };
+
+  if (warp == 0) {
+    // =================== commit warp ===================
+    uint64_t fk[kFR], uk[kUR];
+    uint32_t fid[kFR], uid[kUR];
+#pragma unroll
+    for (int i = 0; i < kFR; ++i) fk[i] = 0, fid[i] = kSentinel;
+#pragma unroll
+    for (int i = 0; i < kUR; ++i) uk[i] = 0, uid[i] = kSentinel;
+    uint32_t fcnt = 0, ufree = (1u << kUR) - 1u;
+    uint32_t capFO = lay.capO, capUO = lay.capO, nFO = 0, nUO = 0;
+    Arr FO = Arr::at(smem + lay.fo_off(), lay.capO), UO = Arr::at(smem + lay.uo_off(), lay.capO);
+    bool fo_g = false, uo_g = false;
+    uint64_t fo_k = 0;  // best FO entry (exact)
+    uint32_t fo_id = kSentinel, fo_ix = 0;
+    uint64_t thr = 0;
+    // stop-test pivot: cH = #{u in U : key >= H} < ef means no top >= H can
+    // stop the search, so the count is skipped (H = max: no pivot yet)
+    uint64_t H = ~0ull;
+    uint32_t cH = 0;
+    uint64_t u_total = 0, scanned = 0;
+    uint32_t nU = 0, expanded = 0, rot = 0;
+    uint64_t c_wait = 0, c_hit = 0, c_miss = 0, c_comp = 0, c_fopop = 0, c_fsp = 0, c_usp = 0;
+    const uint64_t t_begin = clock64();
+    uint64_t cyc_comp = 0;
+
+    auto fo_rescan = [&]() {
+      uint64_t bk = 0;
+      uint32_t bi = kSentinel, bx = 0;
+#pragma unroll 1
+      for (uint32_t i = lane; i < nFO; i += 32)
+        if (better(FO.k[i], FO.id[i], bk, bi)) bk = FO.k[i], bi = FO.id[i], bx = i;
+      uint64_t wk = bk;
+      uint32_t wi = bi;
+      warp_best(wk, wi);
+      fo_k = wk, fo_id = wi;
+      fo_ix = __shfl_sync(kFull, bx, __ffs(__ballot_sync(kFull, bi == wi && bk == wk)) - 1);
+    };
+    // move an overflow array to its HBM spill region (capacity spill_cap >= n)
+    auto to_global = [&](Arr& A, uint32_t cnt, uint8_t* dst) {
+      Arr G = Arr::at(dst, spill_cap);
+#pragma unroll 1
+      for (uint32_t i = lane; i < cnt; i += 32) G.k[i] = A.k[i], G.id[i] = A.id[i];
+      __syncwarp();
+      A = G;
+    };
+    // sorted insertion of (x, v) into this lane's F; the lane's worst of
+    // kFR + 1 goes to FO when the lane is full
+    auto insert_F = [&](bool ok, uint64_t x, uint32_t v) {
+      uint32_t pos = 0;
+#pragma unroll
+      for (int i = 0; i < kFR; ++i) pos += better(fk[i], fid[i], x, v);
+      const bool sp = ok && fcnt == uint32_t(kFR);
+      const uint64_t sk = pos < uint32_t(kFR) ? fk[kFR - 1] : x;
+      const uint32_t si = pos < uint32_t(kFR) ? fid[kFR - 1] : v;
+      if (ok) {
+#pragma unroll
+        for (int i = kFR - 1; i > 0; --i)
+          if (uint32_t(i) > pos) fk[i] = fk[i - 1], fid[i] = fid[i - 1];
+#pragma unroll
+        for (int i = 0; i < kFR; ++i)
+          if (uint32_t(i) == pos) fk[i] = x, fid[i] = v;
+        fcnt += fcnt < uint32_t(kFR);
+      }
+      const uint32_t sm = __ballot_sync(kFull, sp);
+      if (sm) {
+        ++c_fsp;
+        if (nFO + __popc(sm) > capFO) {
+          if (fo_g) __trap();  // unreachable: spill_cap >= n
+          to_global(FO, nFO, spill_slot);
+          capFO = spill_cap, fo_g = true;
+        }
+        const uint32_t o = nFO + __popc(sm & lanemask_lt(lane));
+        if (sp) FO.k[o] = sk, FO.id[o] = si;
+        uint64_t bk = sp ? sk : 0;
+        uint32_t bi = sp ? si : kSentinel;
+        warp_best(bk, bi);
+        if (better(bk, bi, fo_k, fo_id)) {
+          fo_k = bk, fo_id = bi;
+          fo_ix = nFO + __popc(sm & lanemask_lt(__ffs(__ballot_sync(kFull, sp && si == bi)) - 1));
+        }
+        nFO += __popc(sm);
+        __syncwarp();
+      }
+    };
+    auto insert_U = [&](bool ok, uint64_t x, uint32_t v) {
+      const bool sp = ok && !ufree;
+      if (ok && ufree) {
+        const int fi = __ffs(ufree) - 1;
+#pragma unroll
+        for (int i = 0; i < kUR; ++i)
+          if (i == fi) uk[i] = x, uid[i] = v;
+        ufree &= ufree - 1;
+      }
+      nU += __popc(__ballot_sync(kFull, ok));
+      cH += __popc(__ballot_sync(kFull, ok && x >= H));
+      const uint32_t sm = __ballot_sync(kFull, sp);
+      if (sm) {
+        ++c_usp;
+        if (nUO + __popc(sm) > capUO) {
+          if (uo_g) __trap();
+          to_global(UO, nUO, spill_slot + PipeLayout::arr_bytes(spill_cap));
+          capUO = spill_cap, uo_g = true;
+        }
+        const uint32_t o = nUO + __popc(sm & lanemask_lt(lane));
+        if (sp) UO.k[o] = x, UO.id[o] = v;
+        nUO += __popc(sm);
+        __syncwarp();
+      }
+    };
+    auto count_gt = [&](uint64_t x) -> uint32_t {  // #{u in U : key > x}
+      uint32_t c = 0;
+#pragma unroll
+      for (int i = 0; i < kUR; ++i) c += uk[i] > x;
+#pragma unroll 1
+      for (uint32_t i = lane; i < nUO; i += 32) c += UO.k[i] > x;
+      return __reduce_add_sync(kFull, c);
+    };
+    // raise thr toward the pool worst (the ef-th best key of U) by key
+    // bisection, then drop F / U entries below it
+    auto compact = [&]() {
+      ++c_comp;
+      uint64_t lo = ~0ull, hi = 0;
+#pragma unroll
+      for (int i = 0; i < kUR; ++i)
+        if (uid[i] != kSentinel) lo = min(lo, uk[i]), hi = max(hi, uk[i]);
+#pragma unroll 1
+      for (uint32_t i = lane; i < nUO; i += 32) lo = min(lo, UO.k[i]), hi = max(hi, UO.k[i]);
+      {  // exact warp min / max of u64
+        uint64_t l = lo, h = hi;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          l = min(l, __shfl_xor_sync(kFull, l, o));
+          h = max(h, __shfl_xor_sync(kFull, h, o));
+        }
+        lo = l, hi = h;
+      }
+      const uint64_t hmax = hi;
+      lo = max(lo, thr);  // count(>= lo) >= ef; find the largest such key
+      if (count_gt(hi - 1) >= ef) {
+        lo = hi;
+      } else {
+#pragma unroll 1
+        for (int it = 0; it < 24 && hi - lo > 1; ++it) {
+          const uint64_t mid = lo + ((hi - lo) >> 1);
+          if (count_gt(mid - 1) >= ef) lo = mid;
+          else hi = mid;
+        }
+      }
+      if (lo <= thr) return;
+      thr = lo;
+#pragma unroll
+      for (int i = 0; i < kUR; ++i)
+        if (uid[i] != kSentinel && uk[i] < thr) uk[i] = 0, uid[i] = kSentinel, ufree |= 1u << i;
+      // F is sorted per lane: the dropped entries are a tail
+#pragma unroll
+      for (int i = 0; i < kFR; ++i)
+        if (fid[i] != kSentinel && fk[i] < thr) fk[i] = 0, fid[i] = kSentinel;
+      fcnt = 0;
+#pragma unroll
+      for (int i = 0; i < kFR; ++i) fcnt += fid[i] != kSentinel;
+      auto squeeze = [&](Arr& A, uint32_t& cnt) {
+        uint32_t w = 0;
+#pragma unroll 1
+        for (uint32_t c0 = 0; c0 < cnt; c0 += 32) {
+          const uint32_t i = c0 + lane;
+          const bool in = i < cnt;
+          const uint64_t x = in ? A.k[i] : 0;
+          const uint32_t id = in ? A.id[i] : 0;
+          const bool kp = in && x >= thr;
+          const uint32_t bm = __ballot_sync(kFull, kp);
+          __syncwarp();
+          if (kp) {
+            const uint32_t o = w + __popc(bm & lanemask_lt(lane));
+            A.k[o] = x, A.id[o] = id;
+          }
+          w += __popc(bm);
+          __syncwarp();
+        }
+        cnt = w;
+      };
+      if (nUO) squeeze(UO, nUO);
+      if (nFO) {
+        squeeze(FO, nFO);
+        fo_rescan();
+      }
+      nU = __reduce_add_sync(kFull, uint32_t(kUR) - __popc(ufree)) + nUO;
+      // pivot: the largest key with >= ef - 24 entries at or above it
+      // (bisection between thr and the U max), then its exact count
+      if (ef > 24) {
+        uint64_t plo = thr, phi = hmax;
+        const uint32_t target = ef - 24;
+        if (count_gt(phi - 1) >= target) {
+          plo = phi;
+        } else {
+#pragma unroll 1
+          for (int it = 0; it < 24 && phi - plo > 1; ++it) {
+            const uint64_t mid = plo + ((phi - plo) >> 1);
+            if (count_gt(mid - 1) >= target) plo = mid;
+            else phi = mid;
+          }
+        }
+        H = plo;
+        cH = count_gt(H - 1);
+        if (cH >= ef) H = ~0ull;
+      }
+    };
+    // visit lane-held candidates in commit order (:393-399)
+    auto visit = [&](bool cand, uint64_t x, uint32_t v, bool msk) {
+      const bool isnew = cand && !((vis[v >> 5] >> (v & 31)) & 1u);
+      if (isnew) atomicOr(vis + (v >> 5), 1u << (v & 31));
+      const uint32_t nm = __ballot_sync(kFull, isnew);
+      scanned += __popc(nm);
+      u_total += __popc(__ballot_sync(kFull, isnew && !msk));
+      const bool inF = isnew && x >= thr;
+      insert_F(inF, x, v);
+      insert_U(inF && !msk, x, v);
+      if (u_total >= ef && nU >= ef + kSlackU) {
+        const uint64_t t0 = clock64();
+        compact();
+        cyc_comp += clock64() - t0;
+      }
+    };
+
+    // ---- entry (:379-384), then the loop; every visit goes through ONE
+    // call site (the commit path must stay small in the i-cache) ----
+    bool cand;
+    uint64_t cx;
+    uint32_t cv;
+    bool cm;
+    {
+      const uint32_t entry = uint32_t(g.entry);
+      cx = 0;
+      if (lane == 0) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(bar, uint32_t(D) * 4u);
+        bulk_g2s(tile, keys + size_t(entry) * D, uint32_t(D) * 4u, bar);
+      }
+      __syncwarp();
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+      if (lane == 0) cx = okey(row_dot<D>(qd, tile));
+      cand = lane == 0;
+      cv = entry;
+      cm = masked_id(entry);
+    }
+
+    uint64_t cy[5] = {0, 0, 0, 0, 0};
+    uint64_t tq = clock64();
+    for (;;) {
+      visit(cand, cx, cv, cm);
+      pub_k[lane] = fk[0];  // publish the lane heads (helpers' hint)
+      pub_id[lane] = fid[0];
+      PIPE_TICK(3)
+      // frontier top (:387): lane heads vs the best overflow entry
+      uint64_t tk = fk[0];
+      uint32_t tid = fid[0];
+      warp_best(tk, tid);
+      const bool from_fo = nFO && better(fo_k, fo_id, tk, tid);
+      if (from_fo) tk = fo_k, tid = fo_id;
+      if (tid == kSentinel) break;  // frontier exhausted
+      if (u_total >= ef) {          // :390
+        if (tk < thr) break;
+        if (!(tk >= H && cH < ef) && count_gt(tk) >= ef) break;
+      }
+      PIPE_TICK(0)
+      // pop (:391)
+      if (from_fo) {
+        ++c_fopop;
+        if (lane == 0) {
+          --nFO;
+          FO.k[fo_ix] = FO.k[nFO], FO.id[fo_ix] = FO.id[nFO];
+        }
+        nFO = __shfl_sync(kFull, nFO, 0);
+        __syncwarp();
+        fo_rescan();
+      } else if (fid[0] == tid) {
+#pragma unroll
+        for (int i = 0; i < kFR - 1; ++i) fk[i] = fk[i + 1], fid[i] = fid[i + 1];
+        fk[kFR - 1] = 0, fid[kFR - 1] = kSentinel;
+        --fcnt;
+      }
+      ++expanded;
+      PIPE_TICK(1)
+      // the top's packet: hit (ready or in flight) or expand inline
+      const uint32_t sl = slot_of(tid);
+      uint64_t w = *reinterpret_cast<volatile unsigned long long*>(slotw + sl);
+      bool hit = false;
+      if (uint32_t(w) == tid) {
+        if (uint32_t(w >> 32) == sBUSY) {
+          const uint64_t tw0 = clock64();
+          do {
+            __nanosleep(20);
+            w = *reinterpret_cast<volatile unsigned long long*>(slotw + sl);
+          } while (uint32_t(w >> 32) == sBUSY && uint32_t(w) == tid);
+          c_wait += clock64() - tw0;
+        }
+        if (lane == 0 && uint32_t(w) == tid && uint32_t(w >> 32) == sREADY)
+          hit = atomicCAS(slotw + sl, slotword(tid, sREADY), slotword(tid, sTAKEN)) ==
+                slotword(tid, sREADY);
+        hit = __shfl_sync(kFull, hit, 0);
+      }
+      // expanded bit after the take: helpers may evict packets of expanded nodes
+      if (lane == 0) atomicOr(expd + (tid >> 5), 1u << (tid & 31));
+      PIPE_TICK(2)
+      if (hit) {
+        ++c_hit;
+        __threadfence_block();
+        const uint32_t cnt = pk_cnt[sl], mb = pk_mb[sl];
+        const uint32_t j = (lane + rot) & 31u;
+        cand = j < cnt;
+        cv = cand ? pk_id[sl * 32 + j] : kSentinel;
+        cx = cand ? pk_k[sl * 32 + j] : 0;
+        cm = cand && ((mb >> j) & 1u);
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();
+          *reinterpret_cast<volatile unsigned long long*>(slotw + sl) = slotword(kSentinel, sFREE);
+        }
+        rot += cnt;
+      } else {
+        ++c_miss;
+        expand(tid, cv, cx, cand);
+        cm = cand && masked_id(cv);
+      }
+    }
+    ctrl[0] = 1;  // helpers stop
+    __syncwarp();
+    // ---- result (:402-410): the pool's top min(k, |pool|), best-first ----
+    uint32_t p2 = 32;
+    while (p2 < nU) p2 <<= 1;
+    const bool fin_smem = size_t(p2) * 12 <= size_t(kPW) * lay.tile_bytes();
+    if (lane == 0) {
+      ctrl[4] = p2;
+      ctrl[5] = fin_smem;
+    }
+    __syncthreads();  // helpers are done with their tiles (and TMA)
+    // A: shared tiles when it fits, else FO's (dead) half of the HBM slot
+    Arr A = fin_smem ? Arr::at(smem + lay.tiles_off(), p2) : Arr::at(spill_slot, p2);
+    uint32_t w = 0;
+#pragma unroll
+    for (int i = 0; i < kUR; ++i) {
+      const bool kp = uid[i] != kSentinel;
+      const uint32_t bm = __ballot_sync(kFull, kp);
+      if (kp) {
+        const uint32_t o = w + __popc(bm & lanemask_lt(lane));
+        A.k[o] = uk[i], A.id[o] = uid[i];
+      }
+      w += __popc(bm);
+    }
+    for (uint32_t i = lane; i < nUO; i += 32) A.k[w + i] = UO.k[i], A.id[w + i] = UO.id[i];
+    w += nUO;
+    for (uint32_t i = w + lane; i < p2; i += 32) A.k[i] = 0, A.id[i] = kSentinel;
+    if (a.dbg && lane == 0) {
+      uint64_t* d = a.dbg + size_t(b) * 12;
+      d[0] = c_miss, d[1] = c_wait, d[2] = clock64() - t_begin, d[3] = expanded;
+      d[4] = c_hit, d[5] = ctrl[8], d[6] = c_comp;
+      d[7] = cy[0], d[8] = cy[1], d[9] = cy[2], d[10] = cy[3], d[11] = cyc_comp;
+      (void)c_comp, (void)c_fopop, (void)c_fsp, (void)c_usp;
+    }
+    if (lane == 0) {
+      a.scanned[b] = scanned;
+      if (a.expanded) a.expanded[b] = expanded;
+      ctrl[7] = uint32_t(u_total < ef ? u_total : ef);  // |pool|
+    }
+    __syncthreads();
+  } else {
+    // =================== helper warps ===================
+    uint32_t n_exp = 0, n_chain = 0, n_evict = 0;
+    if (a.flags & 1u) ctrl[0] = 1;  // profiling: commit warp alone
+    const uint32_t chain_max = (a.flags >> 4) & 15u ? (a.flags >> 4) & 15u : kChain;
+    const uint32_t pick = (a.flags >> 8) & 31u ? (a.flags >> 8) & 31u : kPick;
+    // claim node id's slot: free, or evict a ready packet of a node that is
+    // expanded already or ranks below x
+    auto try_claim = [&](uint32_t id, uint64_t x, uint32_t& sl) -> bool {
+      bool ok = false;
+      sl = slot_of(id);
+      if (lane == 0) {
+        const uint64_t w = *reinterpret_cast<volatile unsigned long long*>(slotw + sl);
+        const uint32_t key = uint32_t(w), st = uint32_t(w >> 32);
+        if (key != id) {
+          if (st == sFREE) {
+            ok = atomicCAS(slotw + sl, w, slotword(id, sBUSY)) == w;
+          } else if (st == sREADY && (vbit(expd, key) || pk_nk[sl] < x)) {
+            ok = atomicCAS(slotw + sl, w, slotword(id, sBUSY)) == w;
+            n_evict += ok;
+          }
+        }
+        if (ok) pk_nk[sl] = x;
+      }
+      return __shfl_sync(kFull, ok, 0);
+    };
+    for (;;) {
+      if (ctrl[0]) break;
+      uint64_t pk = pub_k[lane];
+      uint32_t pid = pub_id[lane];
+      if (pid >= n) pk = 0, pid = kSentinel;
+      sort32(pk, pid, lane);
+      const uint64_t floor_k = __shfl_sync(kFull, pk, pick - 1);
+      uint32_t got = kSentinel, sl = 0;
+      for (uint32_t r = 0; r < pick; ++r) {
+        const uint32_t id = __shfl_sync(kFull, pid, r);
+        const uint64_t x = __shfl_sync(kFull, pk, r);
+        if (id == kSentinel) break;
+        if (vbit(expd, id)) continue;
+        {
+          const uint64_t w = *reinterpret_cast<volatile unsigned long long*>(slotw + slot_of(id));
+          if (uint32_t(w) == id) continue;  // in flight or ready
+        }
+        if (try_claim(id, x, sl)) {
+          got = id;
+          break;
+        }
+      }
+      if (got == kSentinel) {
+        __nanosleep(64);
+        continue;
+      }
+      for (uint32_t depth = 0;; ++depth) {
+        uint32_t v;
+        uint64_t x;
+        bool isnew;
+        expand(got, v, x, isnew);
+        ++n_exp;
+        const uint32_t newmask = __ballot_sync(kFull, isnew);
+        const uint32_t o = __popc(newmask & lanemask_lt(lane));
+        const bool msk = isnew && masked_id(v);
+        if (isnew) {
+          pk_id[sl * 32 + o] = v;
+          pk_k[sl * 32 + o] = x;
+          // likely future tops: their adjacency rows go to L2 now
+          if ((M * 4) % 16 == 0) bulk_prefetch_l2(adj + size_t(v) * M, M * 4);
+        }
+        const uint32_t mb = __reduce_or_sync(kFull, msk ? (1u << o) : 0u);
+        if (lane == 0) {
+          pk_cnt[sl] = __popc(newmask);
+          pk_mb[sl] = mb;
+        }
+        __threadfence_block();
+        __syncwarp();
+        if (lane == 0)
+          *reinterpret_cast<volatile unsigned long long*>(slotw + sl) = slotword(got, sREADY);
+        // greedy chain: the best new neighbour is the likely next top
+        uint64_t ck = isnew ? x : 0;
+        uint32_t cid = isnew ? v : kSentinel;
+        warp_best(ck, cid);
+        if (depth + 1 >= chain_max || cid == kSentinel || !(ck > floor_k) || ctrl[0]) break;
+        if (vbit(expd, cid)) break;
+        {
+          const uint64_t w = *reinterpret_cast<volatile unsigned long long*>(slotw + slot_of(cid));
+          if (uint32_t(w) == cid) break;
+        }
+        if (!try_claim(cid, ck, sl)) break;
+        got = cid;
+        ++n_chain;
+      }
+    }
+    if (lane == 0) {
+      atomicAdd(const_cast<uint32_t*>(ctrl) + 8, n_exp);
+      atomicAdd(const_cast<uint32_t*>(ctrl) + 9, n_chain);
+      atomicAdd(const_cast<uint32_t*>(ctrl) + 10, n_evict);
+    }
+    __syncthreads();  // matches the commit warp's first barrier
+    __syncthreads();  // final array gathered
+  }
+
+  // ---- final: CTA bitonic sort of the gathered pool candidates ----
+  const uint32_t p2 = ctrl[4];
+  const bool fin_smem = ctrl[5];
+  Arr A = fin_smem ? Arr::at(smem + lay.tiles_off(), p2) : Arr::at(spill_slot, p2);
+  for (uint32_t kk = 2; kk <= p2; kk <<= 1) {
+    for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < p2; i += blockDim.x) {
+        const uint32_t pj = i ^ j;
+        if (pj > i) {
+          const bool desc = (i & kk) == 0;
+          const uint64_t xi = A.k[i], xp = A.k[pj];
+          const uint32_t ii = A.id[i], ip = A.id[pj];
+          if (desc ? better(xp, ip, xi, ii) : better(xi, ii, xp, ip)) {
+            A.k[i] = xp, A.k[pj] = xi;
+            A.id[i] = ip, A.id[pj] = ii;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const uint32_t pool = ctrl[7];
+  const uint32_t take = pool < k ? pool : k;
+  for (uint32_t r = threadIdx.x; r < k; r += blockDim.x) {
+    const bool have = r < take;
+    const double s = have ? okey_inv(A.k[r]) : __longlong_as_double(0x7ff8000000000000ll);
+    a.ids[size_t(b) * k + r] = have ? A.id[r] : kSentinel;
+    a.scores[size_t(b) * k + r] = have ? (float)s : __int_as_float(0x7fc00000);
+    if (a.scores64) a.scores64[size_t(b) * k + r] = s;
+  }
+  if (threadIdx.x == 0) {
+    a.n_out[b] = take;
+    a.truncated[b] = take < k;
+  }
+}
+
+template <int D>
+bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* scratch) {
+  const size_t budget = ctx->smem_optin ? ctx->smem_optin : 227 * 1024;
+  PipeLayout lay{uint32_t(D), std::max<uint32_t>(a.max_M, 1), (max_n + 31) / 32, 1, 0};
+  if (lay.bytes() + PipeLayout::arr_bytes(512) * 2 > budget) lay.vis_smem = 0;
+  const size_t fixed = lay.bytes();
+  if (fixed + PipeLayout::arr_bytes(256) * 2 > budget) return false;
+  lay.capO = uint32_t(std::min<size_t>((budget - fixed - 64) / 24, 8192)) & ~31u;
+  if (lay.bytes() > budget) return false;
+  uint32_t spill_cap = 32;
+  while (spill_cap < max_n) spill_cap <<= 1;
+  SearchArgs s = a;
+  if (const char* f = std::getenv("RA_PIPE_FLAGS")) s.flags = uint32_t(std::atoi(f));
+  uint8_t* cur = scratch;
+  s.spill = cur;
+  cur += (size_t(a.B) * 2 * PipeLayout::arr_bytes(spill_cap) + 255) & ~size_t(255);
+  s.vis_global = reinterpret_cast<uint32_t*>(cur);
+  auto kern = lay.vis_smem ? k_graph_search_pipe<D, true> : k_graph_search_pipe<D, false>;
+  RA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(lay.bytes())));
+  kern<<<a.B, kPW * 32, lay.bytes(), ctx->stream>>>(s, lay, spill_cap);
+  RA_LAUNCH_CHECK();
+  return true;
+}
+
+}  // namespace
+
+size_t search_pipe_scratch_bytes(uint32_t B, uint32_t max_n) {
+  uint32_t p2 = 32;
+  while (p2 < max_n) p2 <<= 1;
+  return size_t(B) * 2 * PipeLayout::arr_bytes(p2) + 256 +
+         size_t(B) * 2 * ((max_n + 31) / 32) * 4 + 256;
+}
+
+bool launch_graph_search_pipe(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n,
+                              uint8_t* scratch) {
+  if (a.max_M > 32 || a.max_M == 0) return false;
+  switch (a.d) {
+    case 128: return launch_pipe_d<128>(ctx, a, max_n, scratch);
+    case 64: return launch_pipe_d<64>(ctx, a, max_n, scratch);
+    case 32: return launch_pipe_d<32>(ctx, a, max_n, scratch);
+    case 16: return launch_pipe_d<16>(ctx, a, max_n, scratch);
+    case 8: return launch_pipe_d<8>(ctx, a, max_n, scratch);
+    default: return false;
+  }
+}
+
+}  // namespace ra
