@@ -232,6 +232,8 @@ def main():
         e1.synchronize()
         e2e.append(e0.elapsed_time(e1))
 
+    tput = batched_throughput(a, ra, kvs, graphs, Q, cfg, flush, stream)
+
     ms = statistics.mean(times)
     ms_search = statistics.mean(search_ms)
     ms_e2e = statistics.mean(e2e)
@@ -270,6 +272,7 @@ def main():
                    "mean_expanded_per_head": statistics.mean(expanded) / Hl,
                    "scan_fraction": statistics.mean(scanned) / Hl / (a.n_ctx - 640)},
         "clocks": clk.summary(),
+        "throughput": tput,
         "setup_s": round(setup_s, 1),
         "build_ms_per_head": round(statistics.mean(build_ms), 1),
         "build_phase_ms_per_head": {
@@ -285,6 +288,51 @@ def main():
         print(json.dumps(res))
     if dist is not None:
         dist.destroy_process_group()
+
+
+def batched_throughput(a, ra, kvs, graphs, Q, cfg, flush, stream):
+    """Batched decode: R decode queries per head issued as ONE engine step
+    over R x H heads (graphs and KV groups repeated R times, so every query
+    walks its head's real graph and KV): search (throughput-mode kernel) +
+    static/retrieved partial attention + merge for R x H queries. A proxy for
+    the layer-batched step of configs[2] (32 layers x batch 1 on one GPU)
+    with the layer's KV shared by the R queries of a head."""
+    import torch
+    R = min(32, Q.shape[0])
+    Hl = len(graphs)
+    eng = ra.Engine(list(kvs) * R, list(graphs) * R, cfg)
+    qb = [Q[j:j + R].reshape(R * Hl, -1).contiguous()
+          for j in range(0, Q.shape[0] - R + 1, R)]
+    for i in range(3):
+        eng.decode_step_device(qb[i % len(qb)])
+    torch.cuda.synchronize()
+    times, s_ms, sc, ex = [], [], [], []
+    for i in range(max(3, min(a.steps, 10))):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.decode_step_device(qb[i % len(qb)])
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+        s_ms.append(eng.last_timing()[0])
+        s, e = eng.last_stats()
+        sc.append(s)
+        ex.append(e)
+    ms, ms_s = statistics.mean(times), statistics.mean(s_ms)
+    by = statistics.mean([s * 128 * 4 + e * a.max_degree * 4 for s, e in zip(sc, ex)])
+    peak, kind = measured_peaks()
+    gbs = by / (ms_s * 1e-3) / 1e9
+    del eng
+    return {"queries_per_step": R * Hl, "decode_queries_per_head": R,
+            "ms_per_step": round(ms, 4), "us_per_query": round(ms * 1e3 / (R * Hl), 3),
+            "queries_per_s": round(R * Hl / (ms * 1e-3), 1),
+            "search_ms": round(ms_s, 4), "search_kernel": "k_graph_search_pipe (TP mode)",
+            "search_algorithmic_bytes": int(by),
+            "search_GBps": round(gbs, 1), "search_frac": round(gbs / peak, 4),
+            "peak_source": kind,
+            "note": "one engine step over R x H heads; KV of each head shared by its R queries"}
 
 
 def recall(eng, graphs, kvs, Q, a, ra):

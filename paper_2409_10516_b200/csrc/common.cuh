@@ -185,10 +185,11 @@ struct SearchArgs {
 // Returns bytes of scratch needed for (B, max_n, d); then launches.
 size_t search_scratch_bytes(const ra_ctx* ctx, uint32_t B, uint32_t max_n, uint32_t d);
 void launch_graph_search(ra_ctx* ctx, SearchArgs a, uint32_t max_n, uint8_t* scratch);
-// v5 pipelined kernel (search_pipe.cu); false when the shape is unsupported
+// v5 pipelined kernel (search_pipe.cu); false when the shape is unsupported.
+// mode: 0 = auto (latency / throughput by batch size), 1 = throughput, 2 = latency
 size_t search_pipe_scratch_bytes(uint32_t B, uint32_t max_n);
 bool launch_graph_search_pipe(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n,
-                              uint8_t* scratch);
+                              uint8_t* scratch, int mode);
 
 void launch_mask_bitset(cudaStream_t s, const uint32_t* mask, uint64_t mask_n, uint32_t* bits,
                         uint64_t words);

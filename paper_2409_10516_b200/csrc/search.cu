@@ -1079,13 +1079,14 @@ bool try_launch_cta(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* s
   return true;
 }
 
-// RA_SEARCH_KERNEL = pipe (default) | cta | warp selects the K6 variant
+// RA_SEARCH_KERNEL = pipe (default: latency or throughput mode by batch) |
+// tp | lat | cta | warp selects the K6 variant
 int search_variant() {
   static const int v = [] {
     const char* e = std::getenv("RA_SEARCH_KERNEL");
     if (!e) return 0;
     const std::string s(e);
-    return s == "cta" ? 1 : s == "warp" ? 2 : 0;
+    return s == "cta" ? 1 : s == "warp" ? 2 : s == "tp" ? 3 : s == "lat" ? 4 : 0;
   }();
   return v;
 }
@@ -1093,7 +1094,10 @@ int search_variant() {
 void launch_graph_search(ra_ctx* ctx, SearchArgs a, uint32_t max_n, uint8_t* scratch) {
   if (a.B == 0) return;
   const int variant = search_variant();
-  if (variant == 0 && launch_graph_search_pipe(ctx, a, max_n, scratch)) return;
+  if ((variant == 0 || variant >= 3) &&
+      launch_graph_search_pipe(ctx, a, max_n, scratch,
+                               variant == 3 ? 1 : variant == 4 ? 2 : 0))
+    return;
   // v3 (CTA per query, speculative pre-expansion) for the common shapes
   if (a.max_M <= 32 && variant <= 1) {
     bool done = false;

@@ -55,6 +55,10 @@ namespace ra {
 namespace {
 
 constexpr uint32_t kPW = 8;        // warps per CTA: 0 commits, 1.. pre-expand
+constexpr uint32_t kTW = 8;        // TP mode: queries (warps) per CTA
+#ifndef RA_TP_MINB
+#define RA_TP_MINB 2  // <= 128 registers: 16 query warps per SM
+#endif
 constexpr int kFR = 8;             // frontier entries per lane (sorted)
 constexpr int kUR = 8;             // pool-candidate entries per lane
 constexpr uint32_t kSlots = 64;    // packet table, direct-mapped by node id
@@ -147,6 +151,10 @@ struct PipeLayout {
   }
   __host__ __device__ size_t uo_off() const { return fo_off() + arr_bytes(capO); }
   __host__ __device__ size_t bytes() const { return uo_off() + arr_bytes(capO); }
+  // TP mode: per warp q (f64) | FO | UO
+  __host__ __device__ size_t tp_warp_bytes() const {
+    return size_t(D) * 8 + 2 * arr_bytes(capO);
+  }
 };
 
 struct Arr {  // (key, id) array: k u64[cap] then id u32[cap]
@@ -159,12 +167,16 @@ struct Arr {  // (key, id) array: k u64[cap] then id u32[cap]
   }
 };
 
-template <int D, bool VS>
-__global__ void __launch_bounds__(kPW * 32, 1)
+// TP (throughput mode): every warp is a commit warp running its own query
+// with inline expansions (key rows straight into registers), kTW queries
+// per CTA, visited set in HBM/L2; for batches that fill the GPU many times.
+template <int D, bool VS, bool TP>
+__global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     k_graph_search_pipe(SearchArgs a, PipeLayout lay, uint32_t spill_cap) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t b = blockIdx.x;
+  const uint32_t b = TP ? blockIdx.x * kTW + warp : blockIdx.x;
+  if (TP && b >= a.B) return;  // warp-uniform; TP never uses CTA barriers
   const GraphDesc g = a.desc[b];
   const uint32_t M = g.M, ef = g.ef, k = a.k, n = g.n;
   const float* __restrict__ keys = g.keys;
@@ -181,21 +193,29 @@ __global__ void __launch_bounds__(kPW * 32, 1)
   volatile uint64_t* pk_nk = reinterpret_cast<volatile uint64_t*>(smem + PipeLayout::kNk);
   uint32_t* pk_id = reinterpret_cast<uint32_t*>(smem + PipeLayout::kPkId);
   uint64_t* pk_k = reinterpret_cast<uint64_t*>(smem + PipeLayout::kPkK);
-  double* qd = reinterpret_cast<double*>(smem + PipeLayout::kQd);
+  double* qd = TP ? reinterpret_cast<double*>(smem + warp * lay.tp_warp_bytes())
+                  : reinterpret_cast<double*>(smem + PipeLayout::kQd);
   float* tile = reinterpret_cast<float*>(smem + lay.tiles_off() + warp * lay.tile_bytes());
   const uint32_t vw = lay.vis_words;
-  uint32_t* vis = VS ? reinterpret_cast<uint32_t*>(smem + lay.vis_off())
-                     : a.vis_global + size_t(b) * 2 * vw;
+  uint32_t* vis = (VS && !TP) ? reinterpret_cast<uint32_t*>(smem + lay.vis_off())
+                              : a.vis_global + size_t(b) * 2 * vw;
   uint32_t* expd = vis + vw;
   uint8_t* spill_slot = a.spill + size_t(b) * 2 * PipeLayout::arr_bytes(spill_cap);
 
-  if (lane == 0) mbar_init(bar);
-  for (uint32_t w = threadIdx.x; w < 2 * vw; w += blockDim.x) vis[w] = 0;
-  for (uint32_t i = threadIdx.x; i < D; i += blockDim.x) qd[i] = (double)a.q[size_t(b) * D + i];
-  for (uint32_t i = threadIdx.x; i < kSlots; i += blockDim.x) slotw[i] = slotword(kSentinel, sFREE);
-  if (threadIdx.x < 32) pub_k[threadIdx.x] = 0, pub_id[threadIdx.x] = kSentinel;
-  if (threadIdx.x < 16) ctrl[threadIdx.x] = 0;
-  __syncthreads();
+  if constexpr (TP) {
+    for (uint32_t w = lane; w < vw; w += 32) vis[w] = 0;
+    for (uint32_t i = lane; i < D; i += 32) qd[i] = (double)a.q[size_t(b) * D + i];
+    __syncwarp();
+  } else {
+    if (lane == 0) mbar_init(bar);
+    for (uint32_t w = threadIdx.x; w < 2 * vw; w += blockDim.x) vis[w] = 0;
+    for (uint32_t i = threadIdx.x; i < D; i += blockDim.x) qd[i] = (double)a.q[size_t(b) * D + i];
+    for (uint32_t i = threadIdx.x; i < kSlots; i += blockDim.x)
+      slotw[i] = slotword(kSentinel, sFREE);
+    if (threadIdx.x < 32) pub_k[threadIdx.x] = 0, pub_id[threadIdx.x] = kSentinel;
+    if (threadIdx.x < 16) ctrl[threadIdx.x] = 0;
+    __syncthreads();
+  }
 
   auto masked_id = [&](uint32_t v) -> bool {
     return a.mask_bits != nullptr && ((__ldg(a.mask_bits + (v >> 5)) >> (v & 31)) & 1u);
@@ -215,7 +235,21 @@ __global__ void __launch_bounds__(kPW * 32, 1)
     isnew = valid && first && !vbit(vis, v);
     const uint32_t newmask = __ballot_sync(kFull, isnew);
     sk = 0;
-    if (newmask) {
+    if constexpr (TP) {
+      if (isnew) {
+        const float4* r4 = reinterpret_cast<const float4*>(keys + size_t(v) * D);
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < D / 4; ++c) {
+          const float4 kk = __ldg(r4 + c);
+          acc = fma(qd[4 * c + 0], (double)kk.x, acc);
+          acc = fma(qd[4 * c + 1], (double)kk.y, acc);
+          acc = fma(qd[4 * c + 2], (double)kk.z, acc);
+          acc = fma(qd[4 * c + 3], (double)kk.w, acc);
+        }
+        sk = okey(acc);
+      }
+    } else if (newmask) {
       float* row = tile + size_t(__popc(newmask & lanemask_lt(lane))) * RS;
       fence_proxy_async();
       if (lane == 0) mbar_arrive_expect_tx(bar, __popc(newmask) * uint32_t(D) * 4u);
@@ -227,7 +261,7 @@ __global__ void __launch_bounds__(kPW * 32, 1)
     }
   };
 
-  if (warp == 0) {
+  if (TP || warp == 0) {
     // =================== commit warp ===================
     uint64_t fk[kFR], uk[kUR];
     uint32_t fid[kFR], uid[kUR];
@@ -237,7 +271,9 @@ __global__ void __launch_bounds__(kPW * 32, 1)
     for (int i = 0; i < kUR; ++i) uk[i] = 0, uid[i] = kSentinel;
     uint32_t fcnt = 0, ufree = (1u << kUR) - 1u;
     uint32_t capFO = lay.capO, capUO = lay.capO, nFO = 0, nUO = 0;
-    Arr FO = Arr::at(smem + lay.fo_off(), lay.capO), UO = Arr::at(smem + lay.uo_off(), lay.capO);
+    uint8_t* fo_base = TP ? smem + warp * lay.tp_warp_bytes() + size_t(D) * 8 : smem + lay.fo_off();
+    Arr FO = Arr::at(fo_base, lay.capO),
+        UO = Arr::at(fo_base + PipeLayout::arr_bytes(lay.capO), lay.capO);
     bool fo_g = false, uo_g = false;
     uint64_t fo_k = 0;  // best FO entry (exact)
     uint32_t fo_id = kSentinel, fo_ix = 0;
@@ -459,15 +495,31 @@ __global__ void __launch_bounds__(kPW * 32, 1)
     {
       const uint32_t entry = uint32_t(g.entry);
       cx = 0;
-      if (lane == 0) {
-        fence_proxy_async();
-        mbar_arrive_expect_tx(bar, uint32_t(D) * 4u);
-        bulk_g2s(tile, keys + size_t(entry) * D, uint32_t(D) * 4u, bar);
+      if constexpr (TP) {
+        if (lane == 0) {
+          const float4* r4 = reinterpret_cast<const float4*>(keys + size_t(entry) * D);
+          double acc = 0.0;
+#pragma unroll
+          for (int c = 0; c < D / 4; ++c) {
+            const float4 kk = __ldg(r4 + c);
+            acc = fma(qd[4 * c + 0], (double)kk.x, acc);
+            acc = fma(qd[4 * c + 1], (double)kk.y, acc);
+            acc = fma(qd[4 * c + 2], (double)kk.z, acc);
+            acc = fma(qd[4 * c + 3], (double)kk.w, acc);
+          }
+          cx = okey(acc);
+        }
+      } else {
+        if (lane == 0) {
+          fence_proxy_async();
+          mbar_arrive_expect_tx(bar, uint32_t(D) * 4u);
+          bulk_g2s(tile, keys + size_t(entry) * D, uint32_t(D) * 4u, bar);
+        }
+        __syncwarp();
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        if (lane == 0) cx = okey(row_dot<D>(qd, tile));
       }
-      __syncwarp();
-      mbar_wait(bar, phase);
-      phase ^= 1u;
-      if (lane == 0) cx = okey(row_dot<D>(qd, tile));
       cand = lane == 0;
       cv = entry;
       cm = masked_id(entry);
@@ -477,8 +529,10 @@ __global__ void __launch_bounds__(kPW * 32, 1)
     uint64_t tq = clock64();
     for (;;) {
       visit(cand, cx, cv, cm);
-      pub_k[lane] = fk[0];  // publish the lane heads (helpers' hint)
-      pub_id[lane] = fid[0];
+      if constexpr (!TP) {
+        pub_k[lane] = fk[0];  // publish the lane heads (helpers' hint)
+        pub_id[lane] = fid[0];
+      }
       PIPE_TICK(3)
       // frontier top (:387): lane heads vs the best overflow entry
       uint64_t tk = fk[0];
@@ -510,6 +564,12 @@ __global__ void __launch_bounds__(kPW * 32, 1)
       }
       ++expanded;
       PIPE_TICK(1)
+      if constexpr (TP) {
+        ++c_miss;
+        expand(tid, cv, cx, cand);
+        cm = cand && masked_id(cv);
+        continue;
+      }
       // the top's packet: hit (ready or in flight) or expand inline
       const uint32_t sl = slot_of(tid);
       uint64_t w = *reinterpret_cast<volatile unsigned long long*>(slotw + sl);
@@ -552,19 +612,24 @@ __global__ void __launch_bounds__(kPW * 32, 1)
         cm = cand && masked_id(cv);
       }
     }
-    ctrl[0] = 1;  // helpers stop
-    __syncwarp();
     // ---- result (:402-410): the pool's top min(k, |pool|), best-first ----
     uint32_t p2 = 32;
     while (p2 < nU) p2 <<= 1;
-    const bool fin_smem = size_t(p2) * 12 <= size_t(kPW) * lay.tile_bytes();
-    if (lane == 0) {
-      ctrl[4] = p2;
-      ctrl[5] = fin_smem;
+    bool fin_smem;
+    if constexpr (TP) {
+      fin_smem = p2 <= lay.capO;  // this warp's (dead) FO region
+    } else {
+      ctrl[0] = 1;  // helpers stop
+      __syncwarp();
+      fin_smem = size_t(p2) * 12 <= size_t(kPW) * lay.tile_bytes();
+      if (lane == 0) {
+        ctrl[4] = p2;
+        ctrl[5] = fin_smem;
+      }
+      __syncthreads();  // helpers are done with their tiles (and TMA)
     }
-    __syncthreads();  // helpers are done with their tiles (and TMA)
-    // A: shared tiles when it fits, else FO's (dead) half of the HBM slot
-    Arr A = fin_smem ? Arr::at(smem + lay.tiles_off(), p2) : Arr::at(spill_slot, p2);
+    // A: shared memory when it fits, else FO's (dead) half of the HBM slot
+    Arr A = fin_smem ? Arr::at(TP ? fo_base : smem + lay.tiles_off(), p2) : Arr::at(spill_slot, p2);
     uint32_t w = 0;
 #pragma unroll
     for (int i = 0; i < kUR; ++i) {
@@ -582,17 +647,52 @@ __global__ void __launch_bounds__(kPW * 32, 1)
     if (a.dbg && lane == 0) {
       uint64_t* d = a.dbg + size_t(b) * 12;
       d[0] = c_miss, d[1] = c_wait, d[2] = clock64() - t_begin, d[3] = expanded;
-      d[4] = c_hit, d[5] = ctrl[8], d[6] = c_comp;
+      d[4] = c_hit, d[5] = TP ? 0 : ctrl[8], d[6] = c_comp;
       d[7] = cy[0], d[8] = cy[1], d[9] = cy[2], d[10] = cy[3], d[11] = cyc_comp;
       (void)c_comp, (void)c_fopop, (void)c_fsp, (void)c_usp;
     }
+    const uint32_t pool = uint32_t(u_total < ef ? u_total : ef);
     if (lane == 0) {
       a.scanned[b] = scanned;
       if (a.expanded) a.expanded[b] = expanded;
-      ctrl[7] = uint32_t(u_total < ef ? u_total : ef);  // |pool|
     }
-    __syncthreads();
-  } else {
+    if constexpr (TP) {
+      __syncwarp();
+      for (uint32_t kk = 2; kk <= p2; kk <<= 1) {
+        for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+          for (uint32_t i = lane; i < p2; i += 32) {
+            const uint32_t pj = i ^ j;
+            if (pj > i) {
+              const bool desc = (i & kk) == 0;
+              const uint64_t xi = A.k[i], xp = A.k[pj];
+              const uint32_t ii = A.id[i], ip = A.id[pj];
+              if (desc ? better(xp, ip, xi, ii) : better(xi, ii, xp, ip)) {
+                A.k[i] = xp, A.k[pj] = xi;
+                A.id[i] = ip, A.id[pj] = ii;
+              }
+            }
+          }
+          __syncwarp();
+        }
+      }
+      const uint32_t take = pool < k ? pool : k;
+      for (uint32_t r = lane; r < k; r += 32) {
+        const bool have = r < take;
+        const double s = have ? okey_inv(A.k[r]) : __longlong_as_double(0x7ff8000000000000ll);
+        a.ids[size_t(b) * k + r] = have ? A.id[r] : kSentinel;
+        a.scores[size_t(b) * k + r] = have ? (float)s : __int_as_float(0x7fc00000);
+        if (a.scores64) a.scores64[size_t(b) * k + r] = s;
+      }
+      if (lane == 0) {
+        a.n_out[b] = take;
+        a.truncated[b] = take < k;
+      }
+      return;
+    } else {
+      if (lane == 0) ctrl[7] = pool;
+      __syncthreads();
+    }
+  } else if constexpr (!TP) {
     // =================== helper warps ===================
     uint32_t n_exp = 0, n_chain = 0, n_evict = 0;
     if (a.flags & 1u) ctrl[0] = 1;  // profiling: commit warp alone
@@ -692,6 +792,7 @@ __global__ void __launch_bounds__(kPW * 32, 1)
     __syncthreads();  // final array gathered
   }
 
+  if constexpr (TP) return;
   // ---- final: CTA bitonic sort of the gathered pool candidates ----
   const uint32_t p2 = ctrl[4];
   const bool fin_smem = ctrl[5];
@@ -729,14 +830,9 @@ __global__ void __launch_bounds__(kPW * 32, 1)
 }
 
 template <int D>
-bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* scratch) {
+bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* scratch,
+                   bool tp) {
   const size_t budget = ctx->smem_optin ? ctx->smem_optin : 227 * 1024;
-  PipeLayout lay{uint32_t(D), std::max<uint32_t>(a.max_M, 1), (max_n + 31) / 32, 1, 0};
-  if (lay.bytes() + PipeLayout::arr_bytes(512) * 2 > budget) lay.vis_smem = 0;
-  const size_t fixed = lay.bytes();
-  if (fixed + PipeLayout::arr_bytes(256) * 2 > budget) return false;
-  lay.capO = uint32_t(std::min<size_t>((budget - fixed - 64) / 24, 8192)) & ~31u;
-  if (lay.bytes() > budget) return false;
   uint32_t spill_cap = 32;
   while (spill_cap < max_n) spill_cap <<= 1;
   SearchArgs s = a;
@@ -745,7 +841,23 @@ bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* sc
   s.spill = cur;
   cur += (size_t(a.B) * 2 * PipeLayout::arr_bytes(spill_cap) + 255) & ~size_t(255);
   s.vis_global = reinterpret_cast<uint32_t*>(cur);
-  auto kern = lay.vis_smem ? k_graph_search_pipe<D, true> : k_graph_search_pipe<D, false>;
+  if (tp) {
+    PipeLayout lay{uint32_t(D), std::max<uint32_t>(a.max_M, 1), (max_n + 31) / 32, 0, 256};
+    const size_t bytes = kTW * lay.tp_warp_bytes();
+    auto kern = k_graph_search_pipe<D, false, true>;
+    RA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+    kern<<<(a.B + kTW - 1) / kTW, kTW * 32, bytes, ctx->stream>>>(s, lay, spill_cap);
+    RA_LAUNCH_CHECK();
+    return true;
+  }
+  PipeLayout lay{uint32_t(D), std::max<uint32_t>(a.max_M, 1), (max_n + 31) / 32, 1, 0};
+  if (lay.bytes() + PipeLayout::arr_bytes(512) * 2 > budget) lay.vis_smem = 0;
+  const size_t fixed = lay.bytes();
+  if (fixed + PipeLayout::arr_bytes(256) * 2 > budget) return false;
+  lay.capO = uint32_t(std::min<size_t>((budget - fixed - 64) / 24, 8192)) & ~31u;
+  if (lay.bytes() > budget) return false;
+  auto kern = lay.vis_smem ? k_graph_search_pipe<D, true, false>
+                           : k_graph_search_pipe<D, false, false>;
   RA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                int(lay.bytes())));
   kern<<<a.B, kPW * 32, lay.bytes(), ctx->stream>>>(s, lay, spill_cap);
@@ -762,15 +874,18 @@ size_t search_pipe_scratch_bytes(uint32_t B, uint32_t max_n) {
          size_t(B) * 2 * ((max_n + 31) / 32) * 4 + 256;
 }
 
+// Latency mode (one CTA of helpers per query) while the batch leaves SMs
+// idle; throughput mode (8 queries per CTA) once it fills the GPU.
 bool launch_graph_search_pipe(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n,
-                              uint8_t* scratch) {
+                              uint8_t* scratch, int mode) {
   if (a.max_M > 32 || a.max_M == 0) return false;
+  const bool tp = mode == 1 || (mode == 0 && a.B > 2u * uint32_t(ctx->num_sms));
   switch (a.d) {
-    case 128: return launch_pipe_d<128>(ctx, a, max_n, scratch);
-    case 64: return launch_pipe_d<64>(ctx, a, max_n, scratch);
-    case 32: return launch_pipe_d<32>(ctx, a, max_n, scratch);
-    case 16: return launch_pipe_d<16>(ctx, a, max_n, scratch);
-    case 8: return launch_pipe_d<8>(ctx, a, max_n, scratch);
+    case 128: return launch_pipe_d<128>(ctx, a, max_n, scratch, tp);
+    case 64: return launch_pipe_d<64>(ctx, a, max_n, scratch, tp);
+    case 32: return launch_pipe_d<32>(ctx, a, max_n, scratch, tp);
+    case 16: return launch_pipe_d<16>(ctx, a, max_n, scratch, tp);
+    case 8: return launch_pipe_d<8>(ctx, a, max_n, scratch, tp);
     default: return false;
   }
 }
