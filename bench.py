@@ -260,8 +260,8 @@ def main():
         "e2e": {"value": round(ms_e2e, 4), "unit": "ms/token",
                 "h2d_bytes_per_step": Hl * 128 * 4,
                 "d2h_bytes_per_step": Hl * 128 * 8 + Hl * max(eng.k, 1) * 4 + Hl * 8},
-        "gpu_launches": 4 * a.steps,
-        "roofline": {"bound": "hbm", "kernel": "k_graph_search",
+        "gpu_launches": 3 * a.steps,  # W partial, search, Omega partial + merge
+        "roofline": {"bound": "hbm", "kernel": "k_graph_search_pipe (latency mode)",
                      "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 5), "peak_source": peak_kind,
                      "traffic": ncu_traffic(),

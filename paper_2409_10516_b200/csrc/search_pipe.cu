@@ -757,7 +757,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
           pk_id[sl * 32 + o] = v;
           pk_k[sl * 32 + o] = x;
           // likely future tops: their adjacency rows go to L2 now
-          if ((M * 4) % 16 == 0) bulk_prefetch_l2(adj + size_t(v) * M, M * 4);
+          if ((M * 4) % 16 == 0 && !(a.flags & 2u)) bulk_prefetch_l2(adj + size_t(v) * M, M * 4);
         }
         const uint32_t mb = __reduce_or_sync(kFull, msk ? (1u << o) : 0u);
         if (lane == 0) {

@@ -40,11 +40,12 @@ def full(rep, out, cmd, alg=None):
     dur_ns = num("gpu__time_duration.sum")
     rd, wr = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
     # units of dram bytes may be in KB/MB depending on ncu scaling
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6,
+             "GB": 1e9}
     u_rd = units[hdr.index("dram__bytes_read.sum")] if "dram__bytes_read.sum" in hdr else "byte"
     u_wr = units[hdr.index("dram__bytes_write.sum")] if "dram__bytes_write.sum" in hdr else "byte"
     u_t = units[hdr.index("gpu__time_duration.sum")]
-    tscale = {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3}[u_t]
+    tscale = {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3, "ns": 1e-3, "us": 1, "ms": 1e3}[u_t]
     stalls = {}
     for k in hdr:
         if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
