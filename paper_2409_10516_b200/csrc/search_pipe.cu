@@ -54,7 +54,10 @@
 namespace ra {
 namespace {
 
-constexpr uint32_t kPW = 8;        // warps per CTA: 0 commits, 1.. pre-expand
+#ifndef RA_PIPE_WARPS
+#define RA_PIPE_WARPS 8
+#endif
+constexpr uint32_t kPW = RA_PIPE_WARPS;  // warps per CTA: 0 commits, 1.. pre-expand
 constexpr uint32_t kTW = 8;        // TP mode: queries (warps) per CTA
 #ifndef RA_TP_MINB
 #define RA_TP_MINB 2  // <= 128 registers: 16 query warps per SM
@@ -287,6 +290,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     uint64_t c_wait = 0, c_hit = 0, c_miss = 0, c_comp = 0, c_fopop = 0, c_fsp = 0, c_usp = 0;
     const uint64_t t_begin = clock64();
     uint64_t cyc_comp = 0;
+    const int bis_it = (a.flags >> 28) ? int(a.flags >> 28) * 4 : 8;  // thr bisection steps
 
     auto fo_rescan = [&]() {
       uint64_t bk = 0;
@@ -405,7 +409,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         lo = hi;
       } else {
 #pragma unroll 1
-        for (int it = 0; it < 24 && hi - lo > 1; ++it) {
+        for (int it = 0; it < bis_it && hi - lo > 1; ++it) {
           const uint64_t mid = lo + ((hi - lo) >> 1);
           if (count_gt(mid - 1) >= ef) lo = mid;
           else hi = mid;
@@ -458,7 +462,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
           plo = phi;
         } else {
 #pragma unroll 1
-          for (int it = 0; it < 24 && phi - plo > 1; ++it) {
+          for (int it = 0; it < bis_it && phi - plo > 1; ++it) {
             const uint64_t mid = plo + ((phi - plo) >> 1);
             if (count_gt(mid - 1) >= target) plo = mid;
             else phi = mid;
