@@ -336,30 +336,30 @@ def batched_throughput(a, ra, kvs, graphs, Q, cfg, flush, stream):
 
 
 def recall(eng, graphs, kvs, Q, a, ra):
-    """recall@100 on a sample: engine-level (masked, vs exact pool top-100,
-    acceptance.cpp:207-212) and unmasked vs FlatIndex (diagnostics.cpp:150-164)."""
-    import torch
+    """recall@100 on a sample against the GPU FlatIndex (exact, the
+    reference's recall ground truth, index_flat.hpp:9-22): engine-level
+    (masked by W, vs the exact pool top-100, acceptance.cpp:207-212) and
+    unmasked graph search vs FlatIndex (diagnostics.cpp:150-164)."""
     hpg = a.heads // a.groups
     W = ra.static_partition(a.n_ctx, 128, 512).static_set
-    mask = torch.zeros(a.n_ctx, dtype=torch.bool, device=Q.device)
-    mask[torch.from_numpy(W.astype(np.int64)).to(Q.device)] = True
+    flats = [ra.FlatIndex(kv) for kv in kvs]
     rec_m, rec_u = [], []
-    K64 = [kv.keys_tensor().double() for kv in kvs]
     for i in range(min(4, a.steps)):
         q = Q[a.warmup + i]
         out, om, sc = eng.decode_step_device(q)
         omega = om.cpu().numpy().view(np.uint32)
         un = ra.search_batch(graphs, q, 100, None, a.ef).host()
-        for h in range(len(graphs)):
-            s = K64[h // hpg] @ q[h].double()
-            top_u = torch.topk(s, 100).indices.cpu().numpy()
-            s[mask] = -float("inf")
-            top_m = torch.topk(s, 100).indices.cpu().numpy()
-            rec_m.append(len(set(top_m.tolist()) & set(omega[h].tolist())) / 100)
-            rec_u.append(len(set(top_u.tolist()) & set(un[h].ids.tolist())) / 100)
+        for g, flat in enumerate(flats):
+            qg = q[g * hpg:(g + 1) * hpg]
+            tm = flat.search_batch(qg, 100, W)
+            tu = flat.search_batch(qg, 100)
+            for j in range(hpg):
+                h = g * hpg + j
+                rec_m.append(len(set(tm[j].ids.tolist()) & set(omega[h].tolist())) / 100)
+                rec_u.append(len(set(tu[j].ids.tolist()) & set(un[h].ids.tolist())) / 100)
     return {"masked_engine": round(float(np.mean(rec_m)), 4),
             "unmasked_flat": round(float(np.mean(rec_u)), 4), "samples": len(rec_m),
-            "ef": a.ef}
+            "ef": a.ef, "ground_truth": "ra_flat_search_batch (GPU FlatIndex)"}
 
 
 def _ref_engine(keys_host, vals_host, graphs, cfg, threads):

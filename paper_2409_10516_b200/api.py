@@ -362,6 +362,58 @@ def search_batch(graphs: Sequence[OODGraph], queries, k: int, mask=None,
     return out
 
 
+class FlatIndex:
+    """Exact maximum-inner-product scan on the device (index_flat.hpp:9-22):
+    in-order f64 scores of every key, (score desc, id asc) top k, masked ids
+    skipped, scanned = n - |mask|. The recall ground truth."""
+
+    def __init__(self, keys: KVGroup):
+        if keys.n == 0:
+            raise InvalidArgument("empty keys")
+        self.keys = keys
+
+    def kind(self) -> str:
+        return "flat"
+
+    def size(self) -> int:
+        return self.keys.n
+
+    def memory_bytes(self) -> int:
+        return 0
+
+    def search_batch(self, queries, k: int, mask=None) -> list:
+        ctx = self.keys.ctx.bind_stream()
+        dev = torch.device("cuda", ctx.device)
+        q = _dev(queries, torch.float32, dev)
+        if q.dim() == 1:
+            q = q.view(1, -1)
+        if int(q.shape[1]) != self.keys.d:
+            raise InvalidArgument("query dimension mismatch")
+        B = int(q.shape[0])
+        m = None
+        if mask is not None and len(mask) > 0:
+            m = _dev(np.asarray(mask, np.uint32).view(np.int32) if not isinstance(mask, torch.Tensor)
+                     else mask, torch.int32, dev)
+        kk = max(int(k), 1)
+        ids = torch.empty((B, kk), dtype=torch.int32, device=dev)
+        sc = torch.empty((B, kk), dtype=torch.float32, device=dev)
+        scanned = torch.empty(B, dtype=torch.int64, device=dev)
+        _check(lib.ra_flat_search_batch(ctx.h, self.keys.h, B, _ptr(q), int(k), _ptr(m),
+                                        0 if m is None else int(m.numel()), _ptr(ids), _ptr(sc),
+                                        _ptr(scanned)))
+        ih, sh, nh = ids.cpu().numpy().view(np.uint32), sc.cpu().numpy(), scanned.cpu().numpy()
+        return [SearchResult(ih[b].copy(), sh[b].copy(), int(nh[b]), False) for b in range(B)]
+
+    def search(self, q, k: int, mask=None, param=None) -> SearchResult:
+        """SearchIndex::search (index.hpp:41-42); the flat scan has no knob."""
+        return self.search_batch(np.asarray(q, np.float32).reshape(1, -1), k, mask)[0]
+
+
+def flat_build(keys: KVGroup) -> FlatIndex:
+    """flat_build (index_flat.hpp:24)."""
+    return FlatIndex(keys)
+
+
 # ---------------------------------------------------------------------------
 # attention  (attention.hpp)
 # ---------------------------------------------------------------------------

@@ -111,7 +111,8 @@ __device__ uint32_t compact_query(double* bs, uint32_t* bi, uint32_t cnt, uint32
 __global__ void __launch_bounds__(KTHREADS)
     k_knn(const float* __restrict__ Q, uint64_t nq, const float* __restrict__ K, uint32_t n,
           uint32_t d, uint32_t kt, uint32_t cb, double* __restrict__ bufS,
-          uint32_t* __restrict__ bufI, uint32_t* __restrict__ knn, unsigned long long* widen_ctr) {
+          uint32_t* __restrict__ bufI, uint32_t* __restrict__ knn, unsigned long long* widen_ctr,
+          double* __restrict__ knn_s = nullptr) {
   __shared__ double Qs[KDC][KQ + 1];
   __shared__ double Ks[KDC][KK + 1];
   __shared__ double th_s[KQ];
@@ -206,7 +207,10 @@ __global__ void __launch_bounds__(KTHREADS)
     double* bs = bufS + (q0 + ql) * cb;
     uint32_t* bi = bufI + (q0 + ql) * cb;
     compact_query(bs, bi, cnt[ql], kt, lane);
-    for (uint32_t r = lane; r < kt; r += 32) knn[(q0 + ql) * kt + r] = bi[r];
+    for (uint32_t r = lane; r < kt; r += 32) {
+      knn[(q0 + ql) * kt + r] = bi[r];
+      if (knn_s) knn_s[(q0 + ql) * kt + r] = bs[r];
+    }
   }
 }
 
@@ -510,6 +514,28 @@ struct Timer {
   }
 };
 
+// FlatIndex: drop masked ids from each exact top-(k + |mask|) row, keep k
+__global__ void k_flat_pick(const uint32_t* __restrict__ ids, const double* __restrict__ sc,
+                            uint32_t B, uint32_t kt, uint32_t k, const uint32_t* __restrict__ bits,
+                            uint32_t* out_ids, float* out_sc, uint64_t* scanned, uint64_t nscan) {
+  const uint32_t b = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (b >= B) return;
+  uint32_t w = 0;
+  for (uint32_t c0 = 0; c0 < kt && w < k; c0 += 32) {
+    const uint32_t i = c0 + lane;
+    const uint32_t v = i < kt ? ids[size_t(b) * kt + i] : kSentinel;
+    const bool keep = v != kSentinel && !(bits && ((bits[v >> 5] >> (v & 31)) & 1u));
+    const uint32_t m = __ballot_sync(kFull, keep);
+    const uint32_t o = w + __popc(m & ((1u << lane) - 1u));
+    if (keep && o < k) {
+      out_ids[size_t(b) * k + o] = v;
+      out_sc[size_t(b) * k + o] = float(sc[size_t(b) * kt + i]);
+    }
+    w += __popc(m);
+  }
+  if (lane == 0) scanned[b] = nscan;
+}
+
 }  // namespace
 
 // host-orchestrated phase 4 on the host mirror; nearest-anchor on the GPU
@@ -810,5 +836,50 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
     g->kv = kv;
     if (stats) *stats = st;
     *out = g.release();
+  });
+}
+
+// FlatIndex::search (index_flat.cpp:22-43) for B queries on the device:
+// exact in-order f64 scores of every key and the (score desc, id asc) top
+// k + |mask| by the K1 exact kernel, then masked ids are dropped. Mask ids
+// must be sorted and unique (the reference's Mask contract, index.hpp:16-26).
+extern "C" ra_status ra_flat_search_batch(ra_ctx* ctx, ra_kv* kv, uint32_t B, const float* q,
+                                          uint32_t k, const uint32_t* mask, uint64_t mask_n,
+                                          uint32_t* ids, float* scores, uint64_t* scanned) {
+  using namespace ra;
+  return guard([&] {
+    if (!ctx) invalid("null context");
+    if (!kv || kv->n == 0) invalid("empty keys");
+    const uint64_t n = kv->n;
+    if (n < mask_n || k < 1 || k > n - mask_n) invalid("k out of range after masking");
+    if (B == 0) return;
+    DeviceGuard dg(ctx->device);
+    cudaStream_t s = ctx->stream;
+    const uint32_t d = kv->d;
+    const uint32_t kt = uint32_t(std::min<uint64_t>(n, uint64_t(k) + mask_n));
+    DevBuf<uint32_t> bits;
+    if (mask_n) {
+      const uint64_t words = (n + 31) / 32;
+      bits.alloc(words);
+      launch_mask_bitset(s, mask, mask_n, bits.p, words);
+    }
+    uint32_t cb = 1;
+    while (cb < 2 * kt + KK) cb <<= 1;
+    const uint64_t chunk = std::min<uint64_t>(
+        B, std::max<uint64_t>(KQ, (1ull << 30) / (uint64_t(cb) * 12ull)) / KQ * KQ);
+    DevBuf<double> bs(size_t((chunk + KQ - 1) / KQ * KQ) * cb);
+    DevBuf<uint32_t> bi(size_t((chunk + KQ - 1) / KQ * KQ) * cb);
+    DevBuf<uint32_t> tk(size_t(chunk) * kt);
+    DevBuf<double> ts(size_t(chunk) * kt);
+    for (uint64_t c0 = 0; c0 < B; c0 += chunk) {
+      const uint32_t cn = uint32_t(std::min<uint64_t>(chunk, B - c0));
+      k_knn<<<(cn + KQ - 1) / KQ, KTHREADS, 0, s>>>(q + c0 * d, cn, kv->keys.p, uint32_t(n), d, kt,
+                                                    cb, bs.p, bi.p, tk.p, nullptr, ts.p);
+      k_flat_pick<<<(cn + 7) / 8, 256, 0, s>>>(tk.p, ts.p, cn, kt, k, mask_n ? bits.p : nullptr,
+                                              ids + c0 * k, scores + c0 * k, scanned + c0,
+                                              n - mask_n);
+      RA_LAUNCH_CHECK();
+    }
+    RA_CUDA(cudaStreamSynchronize(s));
   });
 }

@@ -358,11 +358,6 @@ ra_status ra_graph_search_host(ra_ctx* ctx, const ra_graph* g, const float* q, u
   });
 }
 
-ra_status ra_flat_search_batch(ra_ctx*, ra_kv*, uint32_t, const float*, uint32_t,
-                               const uint32_t*, uint64_t, uint32_t*, float*, uint64_t*) {
-  return guard([&] { runtime("flat search is not part of this build yet"); });
-}
-
 // ---- attention ------------------------------------------------------------------------------
 ra_status ra_static_partition(uint64_t t, uint64_t s_init, uint64_t s_local,
                               uint32_t* static_ids, uint64_t* n_static, uint32_t* pool_ids,
