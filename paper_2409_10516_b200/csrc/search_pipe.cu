@@ -140,7 +140,8 @@ struct PipeLayout {
   static constexpr size_t kBars = 0, kCtrl = 64, kPubK = 128, kPubId = 384, kSlotW = 512,
                           kCnt = 1024, kMb = 1280, kNk = 1536, kPkId = 2048,
                           kPkK = kPkId + size_t(kSlots) * 32 * 4,
-                          kQd = kPkK + size_t(kSlots) * 32 * 8;
+                          kPubF = kPkK + size_t(kSlots) * 32 * 8,  // F: k u64[kFR][32], id u32[kFR][32]
+                          kQd = kPubF + size_t(kFR) * 32 * 12;
   __host__ __device__ size_t row_floats() const { return D + 4; }
   __host__ __device__ size_t tiles_off() const { return kQd + size_t(D) * 8; }
   __host__ __device__ size_t tile_bytes() const { return size_t(MT) * row_floats() * 4; }
@@ -190,6 +191,8 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
   volatile uint32_t* ctrl = reinterpret_cast<volatile uint32_t*>(smem + PipeLayout::kCtrl);
   volatile uint64_t* pub_k = reinterpret_cast<volatile uint64_t*>(smem + PipeLayout::kPubK);
   volatile uint32_t* pub_id = reinterpret_cast<volatile uint32_t*>(smem + PipeLayout::kPubId);
+  volatile uint64_t* pubf_k = reinterpret_cast<volatile uint64_t*>(smem + PipeLayout::kPubF);
+  volatile uint32_t* pubf_id = reinterpret_cast<volatile uint32_t*>(pubf_k + kFR * 32);
   unsigned long long* slotw = reinterpret_cast<unsigned long long*>(smem + PipeLayout::kSlotW);
   uint32_t* pk_cnt = reinterpret_cast<uint32_t*>(smem + PipeLayout::kCnt);
   uint32_t* pk_mb = reinterpret_cast<uint32_t*>(smem + PipeLayout::kMb);
@@ -216,6 +219,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     for (uint32_t i = threadIdx.x; i < kSlots; i += blockDim.x)
       slotw[i] = slotword(kSentinel, sFREE);
     if (threadIdx.x < 32) pub_k[threadIdx.x] = 0, pub_id[threadIdx.x] = kSentinel;
+    for (uint32_t i = threadIdx.x; i < kFR * 32; i += blockDim.x) pubf_k[i] = 0, pubf_id[i] = kSentinel;
     if (threadIdx.x < 16) ctrl[threadIdx.x] = 0;
     __syncthreads();
   }
@@ -534,8 +538,10 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     for (;;) {
       visit(cand, cx, cv, cm);
       if constexpr (!TP) {
-        pub_k[lane] = fk[0];  // publish the lane heads (helpers' hint)
-        pub_id[lane] = fid[0];
+        // publish the frontier (each lane's sorted column): the helpers'
+        // hint of the next tops; torn reads only misorder the hint
+#pragma unroll
+        for (int i = 0; i < kFR; ++i) pubf_k[i * 32 + lane] = fk[i], pubf_id[i * 32 + lane] = fid[i];
       }
       PIPE_TICK(3)
       // frontier top (:387): lane heads vs the best overflow entry
@@ -724,23 +730,35 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     };
     for (;;) {
       if (ctrl[0]) break;
-      uint64_t pk = pub_k[lane];
-      uint32_t pid = pub_id[lane];
-      if (pid >= n) pk = 0, pid = kSentinel;
-      sort32(pk, pid, lane);
-      const uint64_t floor_k = __shfl_sync(kFull, pk, pick - 1);
+      // the frontier's best `pick` nodes, best first: a tournament over the
+      // published per-lane sorted columns (winner lane advances)
+      uint64_t ck[kFR];
+      uint32_t ci[kFR];
+#pragma unroll
+      for (int i = 0; i < kFR; ++i) {
+        ck[i] = pubf_k[i * 32 + lane];
+        ci[i] = pubf_id[i * 32 + lane];
+        if (ci[i] >= n) ck[i] = 0, ci[i] = kSentinel;
+      }
       uint32_t got = kSentinel, sl = 0;
+      uint64_t gk = 0;
       for (uint32_t r = 0; r < pick; ++r) {
-        const uint32_t id = __shfl_sync(kFull, pid, r);
-        const uint64_t x = __shfl_sync(kFull, pk, r);
+        uint64_t x = ck[0];
+        uint32_t id = ci[0];
+        warp_best(x, id);
         if (id == kSentinel) break;
+        if (ci[0] == id) {  // winner lane advances
+#pragma unroll
+          for (int i = 0; i < kFR - 1; ++i) ck[i] = ck[i + 1], ci[i] = ci[i + 1];
+          ck[kFR - 1] = 0, ci[kFR - 1] = kSentinel;
+        }
         if (vbit(expd, id)) continue;
         {
           const uint64_t w = *reinterpret_cast<volatile unsigned long long*>(slotw + slot_of(id));
           if (uint32_t(w) == id) continue;  // in flight or ready
         }
         if (try_claim(id, x, sl)) {
-          got = id;
+          got = id, gk = x;
           break;
         }
       }
@@ -773,17 +791,17 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         if (lane == 0)
           *reinterpret_cast<volatile unsigned long long*>(slotw + sl) = slotword(got, sREADY);
         // greedy chain: the best new neighbour is the likely next top
-        uint64_t ck = isnew ? x : 0;
+        uint64_t ck2 = isnew ? x : 0;
         uint32_t cid = isnew ? v : kSentinel;
-        warp_best(ck, cid);
-        if (depth + 1 >= chain_max || cid == kSentinel || !(ck > floor_k) || ctrl[0]) break;
+        warp_best(ck2, cid);
+        if (depth + 1 >= chain_max || cid == kSentinel || !(ck2 > gk) || ctrl[0]) break;
         if (vbit(expd, cid)) break;
         {
           const uint64_t w = *reinterpret_cast<volatile unsigned long long*>(slotw + slot_of(cid));
           if (uint32_t(w) == cid) break;
         }
-        if (!try_claim(cid, ck, sl)) break;
-        got = cid;
+        if (!try_claim(cid, ck2, sl)) break;
+        got = cid, gk = ck2;
         ++n_chain;
       }
     }
