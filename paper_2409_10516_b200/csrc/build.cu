@@ -397,11 +397,26 @@ __global__ void __launch_bounds__(PWARPS * 32)
 
 // ---- K4 -------------------------------------------------------------------------
 // column mean, in row order per dimension (Eigen colwise().mean() as shimmed)
+// (rows stream through registers 32 at a time, double-buffered, so the
+// dependent f64 adds — not the load latency — set the pace)
 __global__ void k_colmean(const float* __restrict__ keys, uint32_t n, uint32_t d, double* mean) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= d) return;
+  constexpr uint32_t R = 32;
+  float cur[R], nxt[R];
+#pragma unroll
+  for (uint32_t r = 0; r < R; ++r) cur[r] = r < n ? __ldg(keys + size_t(r) * d + j) : 0.f;
   double acc = 0.0;
-  for (uint32_t i = 0; i < n; ++i) acc += (double)keys[size_t(i) * d + j];
+  for (uint32_t i = 0; i < n; i += R) {
+#pragma unroll
+    for (uint32_t r = 0; r < R; ++r)
+      nxt[r] = i + R + r < n ? __ldg(keys + size_t(i + R + r) * d + j) : 0.f;
+#pragma unroll
+    for (uint32_t r = 0; r < R; ++r)
+      if (i + r < n) acc += (double)cur[r];
+#pragma unroll
+    for (uint32_t r = 0; r < R; ++r) cur[r] = nxt[r];
+  }
   mean[j] = acc / (double)n;
 }
 
@@ -793,7 +808,7 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
     RA_CUDA(cudaMemsetAsync(covered.p, 0, 4, s));
     k_any_covered<<<(n + 255) / 256, 256, 0, s>>>(deg.p, n, covered.p);
     DevBuf<double> mean(d);
-    if (!p->entry_maxnorm) k_colmean<<<(d + 63) / 64, 64, 0, s>>>(K, n, d, mean.p);
+    if (!p->entry_maxnorm) k_colmean<<<(d + 31) / 32, 32, 0, s>>>(K, n, d, mean.p);
     uint32_t any = 0;
     RA_CUDA(cudaMemcpyAsync(&any, covered.p, 4, cudaMemcpyDeviceToHost, s));
     RA_CUDA(cudaStreamSynchronize(s));

@@ -197,3 +197,23 @@ def test_search_large_n_spills_and_global_visited(port):
         r = og.search(Q[qi], 100, None, n)
         assert r.scanned == n
         assert_same(res[qi], r)
+
+
+def test_search_throughput_mode_matches_oracle(port):
+    """A batch larger than 2 x SMs takes the throughput-mode kernel (one
+    query per warp): results must match the reference exactly too."""
+    ra = _ra()
+    rng = np.random.default_rng(23)
+    n, d = 4000, 64
+    keys = rng.standard_normal((n, d)).astype(np.float32)
+    blob = port.graph_build(keys, rng.standard_normal((800, d)).astype(np.float32),
+                            BuildParams(k_train=32, max_degree=24, ef_construction=64))
+    g = ra.OODGraph.from_blob(ra.KVGroup(keys), blob)
+    og = port.graph(keys, blob)
+    B = 400  # > 2 x 148 SMs
+    Q = rng.standard_normal((B, d)).astype(np.float32)
+    mask = np.sort(rng.choice(n, size=300, replace=False)).astype(np.uint32)
+    for m, ef, k in ((None, 64, 20), (mask, 128, 100)):
+        res = ra.search_batch([g], Q, k, m, ef).host()
+        for qi in range(0, B, 7):
+            assert_same(res[qi], og.search(Q[qi], k, m, ef), f"tp ef={ef} q={qi}")
