@@ -21,6 +21,7 @@
 #include "attnindex/index_flat.hpp"
 #include "attnindex/index_oodgraph.hpp"
 #include "attnindex/util.hpp"
+#include "attnindex/io.hpp"
 #include "attnindex/workload.hpp"
 
 using namespace attnindex;
@@ -110,6 +111,29 @@ int ref_generate_workload(uint64_t n_ctx, uint32_t d_model, uint32_t d_head,
                   per_ctx * sizeof(float));
     }
   });
+}
+
+// generate_workload + save_workloads (io.cpp:143-177) into dir: the KVD1
+// byte-format fixture for tests/test_kvd1.py
+int ref_save_workloads(uint64_t n_ctx, uint32_t d_model, uint32_t d_head, uint32_t n_heads,
+                       uint32_t n_kv_groups, uint64_t seed, uint64_t n_decode, const char* dir) {
+  return guard([&] {
+    WorkloadSpec s;
+    s.n_ctx = n_ctx;
+    s.d_model = d_model;
+    s.d_head = d_head;
+    s.n_heads = n_heads;
+    s.n_kv_groups = n_kv_groups;
+    s.seed = seed;
+    s.n_decode = n_decode;
+    auto heads = generate_workload(s, 1);
+    save_workloads(heads, n_kv_groups, dir);
+  });
+}
+
+// load_workloads + load_vectors error text for a file (empty on success)
+int ref_load_vectors_check(const char* path) {
+  return guard([&] { (void)load_vectors(path); });
 }
 
 int ref_graph_build(const float* keys, uint64_t n, uint32_t d, const float* train_q,

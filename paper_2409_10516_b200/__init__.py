@@ -10,6 +10,6 @@ from .api import (  # noqa: F401
     BatchResult, BuildStats, Context, CudaError, Engine, EngineConfig, FlatIndex, GraphError,
     InvalidArgument, KVGroup, KVPartition, OODGraph, OODGraphBuildParams, PartialAttention,
     SearchResult, default_context, empty_partial, merge, merge_gammas, ood_build,
-    partial_attention, search_batch, static_partition, flat_build)
+    partial_attention, search_batch, static_partition, flat_build, engine_init)
 
 __version__ = lib.ra_version().decode()

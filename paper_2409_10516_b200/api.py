@@ -362,6 +362,37 @@ def search_batch(graphs: Sequence[OODGraph], queries, k: int, mask=None,
     return out
 
 
+def engine_init(workloads, config: "EngineConfig" = None,
+                graph: "OODGraphBuildParams" = None) -> "Engine":
+    """engine_init (engine.cpp:23-65) for IndexKind::OODGraph: one KVGroup per
+    kv_group_id (uploaded once, shared by its heads), each head's graph built
+    on the GPU over its group's keys from its own prefill queries. `workloads`
+    are reference-style head bundles (kvd1.HeadWorkload or anything with
+    head_id, kv_group_id, prefill_queries, keys, values; vectors as .data or
+    arrays). Heads must be ordered by head id with groups contiguous."""
+    config = config or EngineConfig()
+    graph = graph or OODGraphBuildParams()
+    if not workloads:
+        raise InvalidArgument("no heads")
+    if config.top_k < 1:
+        raise InvalidArgument("top_k must be >= 1")
+    arr = lambda v: np.asarray(getattr(v, "data", v), np.float32)
+    t = arr(workloads[0].keys).shape[0]
+    if t == 0:
+        raise InvalidArgument("empty context")
+    for w in workloads:
+        if arr(w.keys).shape[0] != t or arr(w.values).shape[0] != t:
+            raise InvalidArgument("context length mismatch across heads")
+    groups, gid = [], {}
+    for w in workloads:
+        if w.kv_group_id not in gid:
+            gid[w.kv_group_id] = len(groups)
+            groups.append(KVGroup(arr(w.keys), arr(w.values)))
+    graphs = [ood_build(groups[gid[w.kv_group_id]], arr(w.prefill_queries), graph)
+              for w in workloads]
+    return Engine(groups, graphs, config)
+
+
 class FlatIndex:
     """Exact maximum-inner-product scan on the device (index_flat.hpp:9-22):
     in-order f64 scores of every key, (score desc, id asc) top k, masked ids

@@ -182,3 +182,35 @@ def test_engine_rejects_malformed_setups(port, small_workload):
     eng = ra.Engine([kv], [g], ra.EngineConfig())
     with pytest.raises(ra.InvalidArgument, match="one query per head required"):
         eng.decode_step(w["decode_q"][0][:2])
+
+
+def test_engine_init_from_kvd1_workloads_matches_reference_engine(tmp_path, port):
+    """Reference-style workloads (KVD1 round trip) -> engine_init on the GPU ->
+    decode_step equals the oracle's run_head (engine.cpp:69-101)."""
+    import paper_2409_10516_b200 as ra
+    from paper_2409_10516_b200 import kvd1
+    from oracle.ffi import BuildParams
+    w = port.generate_workload(1500, 64, 32, 4, 2, seed=11, n_decode=3)
+    keys = [kvd1.VectorSet(1, w["keys"][g]) for g in range(2)]
+    vals = [kvd1.VectorSet(2, w["values"][g]) for g in range(2)]
+    heads = [kvd1.HeadWorkload(h, h // 2, kvd1.VectorSet(0, w["prefill_q"][h]), keys[h // 2],
+                               vals[h // 2], kvd1.VectorSet(0, w["decode_q"][h]))
+             for h in range(4)]
+    kvd1.save_workloads(heads, 2, tmp_path)
+    loaded = kvd1.load_workloads(tmp_path / "manifest.json")
+    gp = ra.OODGraphBuildParams(32, 16, 64)
+    eng = ra.engine_init(loaded, ra.EngineConfig(128, 512, 100, 128), gp)
+    bp = BuildParams(k_train=32, max_degree=16, ef_construction=64)
+    W = ra.static_partition(1500, 128, 512).static_set
+    for step in range(3):
+        Q = np.stack([w["decode_q"][h][step] for h in range(4)])
+        out, omega, scanned = eng.decode_step(Q)
+        for h in range(4):
+            og = port.graph(w["keys"][h // 2], port.graph_build(w["keys"][h // 2],
+                                                               w["prefill_q"][h], bp))
+            r = og.search(Q[h], 100, W, 128)
+            assert np.array_equal(omega[h], r.ids) and int(scanned[h]) == r.scanned
+            pw = port.partial_attention(Q[h], w["keys"][h // 2], w["values"][h // 2], W)
+            po = port.partial_attention(Q[h], w["keys"][h // 2], w["values"][h // 2], r.ids)
+            ref = port.merge(pw, po, 32)[0]
+            assert np.linalg.norm(out[h] - ref) / np.linalg.norm(ref) <= 1e-9
