@@ -156,8 +156,9 @@ struct PipeLayout {
   __host__ __device__ size_t uo_off() const { return fo_off() + arr_bytes(capO); }
   __host__ __device__ size_t bytes() const { return uo_off() + arr_bytes(capO); }
   // TP mode: per warp q (f64) | FO | UO
+  __host__ __device__ size_t tp_flist_off() const { return size_t(D) * 8 + 2 * arr_bytes(capO); }
   __host__ __device__ size_t tp_warp_bytes() const {
-    return size_t(D) * 8 + 2 * arr_bytes(capO);
+    return tp_flist_off() + size_t(kFR) * 32 * 12;
   }
 };
 
@@ -270,10 +271,19 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
 
   if (TP || warp == 0) {
     // =================== commit warp ===================
-    uint64_t fk[kFR], uk[kUR];
-    uint32_t fid[kFR], uid[kUR];
+    // F: per-lane unsorted lists in shared memory (column layout, entry i of
+    // lane l at [i * 32 + l]; empty = (0, kSentinel)); the lane head (its
+    // best entry and slot) in registers. Helpers read these lists directly.
+    volatile uint64_t* Fl_k = TP ? reinterpret_cast<volatile uint64_t*>(
+                                       smem + warp * lay.tp_warp_bytes() + lay.tp_flist_off())
+                                 : pubf_k;
+    volatile uint32_t* Fl_i = reinterpret_cast<volatile uint32_t*>(Fl_k + kFR * 32);
+    if constexpr (TP) {
 #pragma unroll
-    for (int i = 0; i < kFR; ++i) fk[i] = 0, fid[i] = kSentinel;
+      for (int i = 0; i < kFR; ++i) Fl_k[i * 32 + lane] = 0, Fl_i[i * 32 + lane] = kSentinel;
+    }
+    uint64_t hk = 0, uk[kUR];
+    uint32_t hi = kSentinel, hpos = 0, uid[kUR];
 #pragma unroll
     for (int i = 0; i < kUR; ++i) uk[i] = 0, uid[i] = kSentinel;
     uint32_t fcnt = 0, ufree = (1u << kUR) - 1u;
@@ -316,23 +326,28 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
       __syncwarp();
       A = G;
     };
-    // sorted insertion of (x, v) into this lane's F; the lane's worst of
-    // kFR + 1 goes to FO when the lane is full
+    auto lane_head = [&]() {  // best entry of this lane's list
+      hk = 0, hi = kSentinel, hpos = 0;
+#pragma unroll
+      for (int i = 0; i < kFR; ++i) {
+        if (uint32_t(i) < fcnt) {
+          const uint64_t x = Fl_k[i * 32 + lane];
+          const uint32_t v = Fl_i[i * 32 + lane];
+          if (better(x, v, hk, hi)) hk = x, hi = v, hpos = i;
+        }
+      }
+    };
+    // (x, v) into this lane's list (one store, one head compare); a full
+    // lane hands the entry to FO, whose best competes with the lane heads
     auto insert_F = [&](bool ok, uint64_t x, uint32_t v) {
-      uint32_t pos = 0;
-#pragma unroll
-      for (int i = 0; i < kFR; ++i) pos += better(fk[i], fid[i], x, v);
       const bool sp = ok && fcnt == uint32_t(kFR);
-      const uint64_t sk = pos < uint32_t(kFR) ? fk[kFR - 1] : x;
-      const uint32_t si = pos < uint32_t(kFR) ? fid[kFR - 1] : v;
-      if (ok) {
-#pragma unroll
-        for (int i = kFR - 1; i > 0; --i)
-          if (uint32_t(i) > pos) fk[i] = fk[i - 1], fid[i] = fid[i - 1];
-#pragma unroll
-        for (int i = 0; i < kFR; ++i)
-          if (uint32_t(i) == pos) fk[i] = x, fid[i] = v;
-        fcnt += fcnt < uint32_t(kFR);
+      const uint64_t sk = x;
+      const uint32_t si = v;
+      if (ok && !sp) {
+        Fl_k[fcnt * 32 + lane] = x;
+        Fl_i[fcnt * 32 + lane] = v;
+        if (better(x, v, hk, hi)) hk = x, hi = v, hpos = fcnt;
+        ++fcnt;
       }
       const uint32_t sm = __ballot_sync(kFull, sp);
       if (sm) {
@@ -424,13 +439,26 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
 #pragma unroll
       for (int i = 0; i < kUR; ++i)
         if (uid[i] != kSentinel && uk[i] < thr) uk[i] = 0, uid[i] = kSentinel, ufree |= 1u << i;
-      // F is sorted per lane: the dropped entries are a tail
+      {  // drop this lane's list entries below thr (stable squeeze)
+        uint32_t w2 = 0;
 #pragma unroll
-      for (int i = 0; i < kFR; ++i)
-        if (fid[i] != kSentinel && fk[i] < thr) fk[i] = 0, fid[i] = kSentinel;
-      fcnt = 0;
+        for (int i = 0; i < kFR; ++i) {
+          if (uint32_t(i) < fcnt) {
+            const uint64_t x = Fl_k[i * 32 + lane];
+            const uint32_t v = Fl_i[i * 32 + lane];
+            if (x >= thr) {
+              Fl_k[w2 * 32 + lane] = x, Fl_i[w2 * 32 + lane] = v;
+              ++w2;
+            }
+          }
+        }
 #pragma unroll
-      for (int i = 0; i < kFR; ++i) fcnt += fid[i] != kSentinel;
+        for (int i = 0; i < kFR; ++i)
+          if (uint32_t(i) >= w2 && uint32_t(i) < fcnt)
+            Fl_k[i * 32 + lane] = 0, Fl_i[i * 32 + lane] = kSentinel;
+        fcnt = w2;
+        lane_head();
+      }
       auto squeeze = [&](Arr& A, uint32_t& cnt) {
         uint32_t w = 0;
 #pragma unroll 1
@@ -537,16 +565,10 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     uint64_t tq = clock64();
     for (;;) {
       visit(cand, cx, cv, cm);
-      if constexpr (!TP) {
-        // publish the frontier (each lane's sorted column): the helpers'
-        // hint of the next tops; torn reads only misorder the hint
-#pragma unroll
-        for (int i = 0; i < kFR; ++i) pubf_k[i * 32 + lane] = fk[i], pubf_id[i * 32 + lane] = fid[i];
-      }
       PIPE_TICK(3)
       // frontier top (:387): lane heads vs the best overflow entry
-      uint64_t tk = fk[0];
-      uint32_t tid = fid[0];
+      uint64_t tk = hk;
+      uint32_t tid = hi;
       warp_best(tk, tid);
       const bool from_fo = nFO && better(fo_k, fo_id, tk, tid);
       if (from_fo) tk = fo_k, tid = fo_id;
@@ -566,11 +588,14 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         nFO = __shfl_sync(kFull, nFO, 0);
         __syncwarp();
         fo_rescan();
-      } else if (fid[0] == tid) {
-#pragma unroll
-        for (int i = 0; i < kFR - 1; ++i) fk[i] = fk[i + 1], fid[i] = fid[i + 1];
-        fk[kFR - 1] = 0, fid[kFR - 1] = kSentinel;
+      } else if (hi == tid) {  // owner lane: last entry fills the hole
         --fcnt;
+        if (hpos != fcnt) {
+          Fl_k[hpos * 32 + lane] = Fl_k[fcnt * 32 + lane];
+          Fl_i[hpos * 32 + lane] = Fl_i[fcnt * 32 + lane];
+        }
+        Fl_k[fcnt * 32 + lane] = 0, Fl_i[fcnt * 32 + lane] = kSentinel;
+        lane_head();
       }
       ++expanded;
       PIPE_TICK(1)
@@ -739,6 +764,19 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         ck[i] = pubf_k[i * 32 + lane];
         ci[i] = pubf_id[i * 32 + lane];
         if (ci[i] >= n) ck[i] = 0, ci[i] = kSentinel;
+      }
+      // the commit warp's lists are unsorted: odd-even transposition sort
+#pragma unroll
+      for (int r = 0; r < kFR; ++r) {
+#pragma unroll
+        for (int i = r & 1; i + 1 < kFR; i += 2) {
+          if (better(ck[i + 1], ci[i + 1], ck[i], ci[i])) {
+            const uint64_t tk2 = ck[i];
+            const uint32_t ti2 = ci[i];
+            ck[i] = ck[i + 1], ci[i] = ci[i + 1];
+            ck[i + 1] = tk2, ci[i + 1] = ti2;
+          }
+        }
       }
       uint32_t got = kSentinel, sl = 0;
       uint64_t gk = 0;
