@@ -235,12 +235,14 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
   // Expansion of node c by this warp: lane l holds adjacency slot l; `isnew`
   // lanes hold an unvisited (at read time), first-occurrence neighbour v and
   // its exact score key. Key rows come through this warp's TMA tile.
-  auto expand = [&](uint32_t c, uint32_t& v, uint64_t& sk, bool& isnew) {
+  // The mask bit is fetched here too, so its load overlaps the row loads.
+  auto expand = [&](uint32_t c, uint32_t& v, uint64_t& sk, bool& isnew, bool& msk) {
     v = lane < M ? __ldg(adj + size_t(c) * M + lane) : kSentinel;
     const bool valid = v != kSentinel;
     const uint32_t grp = __match_any_sync(kFull, v);
     const bool first = uint32_t(__ffs(grp) - 1) == lane;
     isnew = valid && first && !vbit(vis, v);
+    msk = isnew && masked_id(v);
     const uint32_t newmask = __ballot_sync(kFull, isnew);
     sk = 0;
     if constexpr (TP) {
@@ -506,8 +508,10 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
       }
     };
     // visit lane-held candidates in commit order (:393-399)
-    auto visit = [&](bool cand, uint64_t x, uint32_t v, bool msk) {
-      const bool isnew = cand && !((vis[v >> 5] >> (v & 31)) & 1u);
+    // pre: candidates from this warp's own expansion were filtered against
+    // the visited set with nothing committed since, so the re-check is moot
+    auto visit = [&](bool cand, uint64_t x, uint32_t v, bool msk, bool pre) {
+      const bool isnew = cand && (pre || !((vis[v >> 5] >> (v & 31)) & 1u));
       if (isnew) atomicOr(vis + (v >> 5), 1u << (v & 31));
       const uint32_t nm = __ballot_sync(kFull, isnew);
       scanned += __popc(nm);
@@ -527,7 +531,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     bool cand;
     uint64_t cx;
     uint32_t cv;
-    bool cm;
+    bool cm, pre = true;  // the entry is unvisited
     {
       const uint32_t entry = uint32_t(g.entry);
       cx = 0;
@@ -564,7 +568,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     uint64_t cy[5] = {0, 0, 0, 0, 0};
     uint64_t tq = clock64();
     for (;;) {
-      visit(cand, cx, cv, cm);
+      visit(cand, cx, cv, cm, pre);
       PIPE_TICK(3)
       // frontier top (:387): lane heads vs the best overflow entry
       uint64_t tk = hk;
@@ -601,8 +605,8 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
       PIPE_TICK(1)
       if constexpr (TP) {
         ++c_miss;
-        expand(tid, cv, cx, cand);
-        cm = cand && masked_id(cv);
+        expand(tid, cv, cx, cand, cm);
+        pre = true;
         continue;
       }
       // the top's packet: hit (ready or in flight) or expand inline
@@ -635,6 +639,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         cv = cand ? pk_id[sl * 32 + j] : kSentinel;
         cx = cand ? pk_k[sl * 32 + j] : 0;
         cm = cand && ((mb >> j) & 1u);
+        pre = false;  // other packets may have visited these since
         __syncwarp();
         if (lane == 0) {
           __threadfence_block();
@@ -643,8 +648,8 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         rot += cnt;
       } else {
         ++c_miss;
-        expand(tid, cv, cx, cand);
-        cm = cand && masked_id(cv);
+        expand(tid, cv, cx, cand, cm);
+        pre = true;
       }
     }
     // ---- result (:402-410): the pool's top min(k, |pool|), best-first ----
@@ -808,11 +813,11 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         uint32_t v;
         uint64_t x;
         bool isnew;
-        expand(got, v, x, isnew);
+        bool msk;
+        expand(got, v, x, isnew, msk);
         ++n_exp;
         const uint32_t newmask = __ballot_sync(kFull, isnew);
         const uint32_t o = __popc(newmask & lanemask_lt(lane));
-        const bool msk = isnew && masked_id(v);
         if (isnew) {
           pk_id[sl * 32 + o] = v;
           pk_k[sl * 32 + o] = x;
