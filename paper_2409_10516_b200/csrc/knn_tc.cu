@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
       for (uint32_t t = 0; t < ntiles; ++t)
         for (uint32_t s = 0; s < nstages_k; ++s, ++it) {
           const uint32_t slot = it % NSTAGE, ph = (it / NSTAGE) & 1u;
-          mbar_wait(empty + slot, ph ^ 1u);
+          mbar_wait_sleep(empty + slot, ph ^ 1u);
           mbar_arrive_expect_tx(full + slot, b_stage);
           const uint8_t* gB = reinterpret_cast<const uint8_t*>(a.B) +
                               (size_t(t) * nstages_k + s) * b_stage;
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
     // ---- MMA issuer (one thread) ----
     if (lane == 0) {
       const uint32_t idesc = instr_desc(TM, TN);
-      mbar_wait(a_full, 0);
+      mbar_wait_sleep(a_full, 0);
       fence_after();
       const uint32_t a_base = smem_u32(sA), b_base0 = smem_u32(sB);
       // A: stage-major blocks of [KS/8 chunks][TM/8 groups][128 B]
@@ -235,12 +235,12 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
       uint32_t it = 0;
       for (uint32_t t = 0; t < ntiles; ++t) {
         const uint32_t buf = t & 1u, tph = (t >> 1) & 1u;
-        mbar_wait(t_empty + buf, tph ^ 1u);
+        mbar_wait_sleep(t_empty + buf, tph ^ 1u);
         fence_after();
         const uint32_t tc = tmem + buf * TN;
         for (uint32_t s = 0; s < nstages_k; ++s, ++it) {
           const uint32_t slot = it % NSTAGE, ph = (it / NSTAGE) & 1u;
-          mbar_wait(full + slot, ph);
+          mbar_wait_sleep(full + slot, ph);
           fence_after();
           const uint32_t b_base = b_base0 + slot * b_stage;
 #pragma unroll
@@ -266,20 +266,36 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
     uint32_t* bi = a.bufI + (valid_row ? q : 0) * size_t(a.cb);
     for (uint32_t t = 0; t < ntiles; ++t) {
       const uint32_t buf = t & 1u, tph = (t >> 1) & 1u;
-      mbar_wait(t_full + buf, tph);
+      mbar_wait_sleep(t_full + buf, tph);
       fence_after();
       for (uint32_t c0 = 0; c0 < TN; c0 += 32) {
         float v[32];
         tmem_ld32(tmem + ((warp * 32u) << 16) + buf * TN + c0, v);
         const uint32_t key0 = t * TN + c0;
+        // survivors are sparse (~0.5% of keys): max of each 8-column group,
+        // and the per-element append only inside a group that beats thr
+        float g8[4];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          if (valid_row && key0 + j < a.n && v[j] > thr) {
-            if (cnt < a.cb) {
-              bs[cnt] = v[j];
-              bi[cnt] = key0 + j;
+        for (int g = 0; g < 4; ++g) {
+          const float a0 = fmaxf(v[8 * g + 0], v[8 * g + 1]), a1 = fmaxf(v[8 * g + 2], v[8 * g + 3]);
+          const float a2 = fmaxf(v[8 * g + 4], v[8 * g + 5]), a3 = fmaxf(v[8 * g + 6], v[8 * g + 7]);
+          g8[g] = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
+        }
+        if (valid_row && fmaxf(fmaxf(g8[0], g8[1]), fmaxf(g8[2], g8[3])) > thr) {
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            if (g8[g] > thr) {
+#pragma unroll
+              for (int j = 8 * g; j < 8 * g + 8; ++j) {
+                if (key0 + j < a.n && v[j] > thr) {
+                  if (cnt < a.cb) {
+                    bs[cnt] = v[j];
+                    bi[cnt] = key0 + j;
+                  }
+                  cnt = min(cnt + 1, a.cb + 1);
+                }
+              }
             }
-            cnt = min(cnt + 1, a.cb + 1);
           }
         }
       }

@@ -31,6 +31,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         : "memory");
   } while (!ok);
 }
+// same, but the waiting thread may be suspended until the phase completes
+// (try_wait's suspend-time hint) instead of spinning on issue slots
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase), "r"(0x100000u)
+        : "memory");
+  } while (!ok);
+}
 // order prior generic-proxy shared accesses before async-proxy (TMA) writes
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
