@@ -372,25 +372,38 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
     double* qd = reinterpret_cast<double*>(hist);
     for (uint32_t j = lane; j < d; j += 32) qd[j] = (double)qr[j];
     __syncwarp();
-    for (uint32_t i = lane; i < cnt; i += 32) {  // the reference's in-order f64 dot
-      const uint32_t id = bufI[q * cb + i];
-      const float4* kr = reinterpret_cast<const float4*>(K + size_t(id) * d);
-      double acc = 0.0;
-      for (uint32_t c0 = 0; c0 < d / 4; c0 += 8) {  // 8 x 16 B loads in flight per lane
-        float4 b[8];
+    // the reference's in-order f64 dot; each lane runs two independent
+    // survivors' chains side by side (twice the loads in flight, DFMA
+    // latency hidden by the other chain)
+    for (uint32_t i0 = 0; i0 < cnt; i0 += 64) {
+      const uint32_t ia = i0 + lane, ib = i0 + 32 + lane;
+      const bool va = ia < cnt, vb = ib < cnt;
+      const uint32_t ida = va ? bufI[q * cb + ia] : 0, idb = vb ? bufI[q * cb + ib] : 0;
+      const float4* ka = reinterpret_cast<const float4*>(K + size_t(ida) * d);
+      const float4* kb = reinterpret_cast<const float4*>(K + size_t(idb) * d);
+      double acc_a = 0.0, acc_b = 0.0;
+      for (uint32_t c0 = 0; c0 < d / 4; c0 += 8) {
+        float4 xa[8], xb[8];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) b[c] = __ldg(kr + c0 + c);
+        for (int c = 0; c < 8; ++c) {
+          xa[c] = va ? __ldg(ka + c0 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+          xb[c] = vb ? __ldg(kb + c0 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const double* qq = qd + 4 * (c0 + c);
-          acc = fma(qq[0], (double)b[c].x, acc);
-          acc = fma(qq[1], (double)b[c].y, acc);
-          acc = fma(qq[2], (double)b[c].z, acc);
-          acc = fma(qq[3], (double)b[c].w, acc);
+          acc_a = fma(qq[0], (double)xa[c].x, acc_a);
+          acc_b = fma(qq[0], (double)xb[c].x, acc_b);
+          acc_a = fma(qq[1], (double)xa[c].y, acc_a);
+          acc_b = fma(qq[1], (double)xb[c].y, acc_b);
+          acc_a = fma(qq[2], (double)xa[c].z, acc_a);
+          acc_b = fma(qq[2], (double)xb[c].z, acc_b);
+          acc_a = fma(qq[3], (double)xa[c].w, acc_a);
+          acc_b = fma(qq[3], (double)xb[c].w, acc_b);
         }
       }
-      es[i] = acc;
-      ei[i] = id;
+      if (va) es[ia] = acc_a, ei[ia] = ida;
+      if (vb) es[ib] = acc_b, ei[ib] = idb;
     }
     __syncwarp();
     __syncwarp();
