@@ -397,27 +397,47 @@ __global__ void __launch_bounds__(PWARPS * 32)
 
 // ---- K4 -------------------------------------------------------------------------
 // column mean, in row order per dimension (Eigen colwise().mean() as shimmed)
-// (rows stream through registers 32 at a time, double-buffered, so the
-// dependent f64 adds — not the load latency — set the pace)
-__global__ void k_colmean(const float* __restrict__ keys, uint32_t n, uint32_t d, double* mean) {
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= d) return;
-  constexpr uint32_t R = 32;
-  float cur[R], nxt[R];
-#pragma unroll
-  for (uint32_t r = 0; r < R; ++r) cur[r] = r < n ? __ldg(keys + size_t(r) * d + j) : 0.f;
+// Block = 32 columns; its 8 warps stage 128-row chunks of those columns in
+// shared memory (double-buffered) while warp 0 runs the sequential f64 adds,
+// so the dependent add chain, not the load latency, sets the pace.
+__global__ void __launch_bounds__(256) k_colmean(const float* __restrict__ keys, uint32_t n,
+                                                 uint32_t d, double* mean) {
+  constexpr uint32_t CH = 128;
+  __shared__ float tile[2][CH][33];
+  const uint32_t c0 = blockIdx.x * 32, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t col = c0 + lane;
+  const uint32_t nch = (n + CH - 1) / CH;
+  auto stage = [&](uint32_t ch, uint32_t buf) {
+    for (uint32_t r = warp; r < CH; r += 8) {
+      const uint64_t row = uint64_t(ch) * CH + r;
+      tile[buf][r][lane] = (row < n && col < d) ? __ldg(keys + row * d + col) : 0.f;
+    }
+  };
   double acc = 0.0;
-  for (uint32_t i = 0; i < n; i += R) {
-#pragma unroll
-    for (uint32_t r = 0; r < R; ++r)
-      nxt[r] = i + R + r < n ? __ldg(keys + size_t(i + R + r) * d + j) : 0.f;
-#pragma unroll
-    for (uint32_t r = 0; r < R; ++r)
-      if (i + r < n) acc += (double)cur[r];
-#pragma unroll
-    for (uint32_t r = 0; r < R; ++r) cur[r] = nxt[r];
+  if (nch) stage(0, 0);
+  __syncthreads();
+  for (uint32_t ch = 0; ch < nch; ++ch) {
+    const uint32_t buf = ch & 1u;
+    if (ch + 1 < nch && warp != 0) stage(ch + 1, buf ^ 1u);
+    if (warp == 0) {
+      const uint32_t rows = min(CH, n - ch * CH);
+      if (rows == CH) {
+#pragma unroll 32
+        for (uint32_t r = 0; r < CH; ++r) acc += (double)tile[buf][r][lane];
+      } else {
+        for (uint32_t r = 0; r < rows; ++r) acc += (double)tile[buf][r][lane];
+      }
+    }
+    __syncthreads();
+    if (ch + 1 < nch && warp == 0) {  // warp 0's share of the next chunk
+      for (uint32_t r = 0; r < CH; r += 8) {
+        const uint64_t row = uint64_t(ch + 1) * CH + r;
+        tile[buf ^ 1u][r][lane] = (row < n && col < d) ? __ldg(keys + row * d + col) : 0.f;
+      }
+    }
+    __syncthreads();
   }
-  mean[j] = acc / (double)n;
+  if (warp == 0 && col < d) mean[col] = acc / (double)n;
 }
 
 // per-node key for the entry argmin: medoid distance (:222-230) or -norm (:218-220)
@@ -808,7 +828,7 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
     RA_CUDA(cudaMemsetAsync(covered.p, 0, 4, s));
     k_any_covered<<<(n + 255) / 256, 256, 0, s>>>(deg.p, n, covered.p);
     DevBuf<double> mean(d);
-    if (!p->entry_maxnorm) k_colmean<<<(d + 31) / 32, 32, 0, s>>>(K, n, d, mean.p);
+    if (!p->entry_maxnorm) k_colmean<<<(d + 31) / 32, 256, 0, s>>>(K, n, d, mean.p);
     uint32_t any = 0;
     RA_CUDA(cudaMemcpyAsync(&any, covered.p, 4, cudaMemcpyDeviceToHost, s));
     RA_CUDA(cudaStreamSynchronize(s));
