@@ -430,6 +430,18 @@ ra_status ra_merge(ra_ctx* ctx, uint32_t B, uint32_t d, const double* ow, const 
 
 // ---- decode engine (engine.cpp:23-115) -----------------------------------------------
 struct ra_engine {
+  // CUDA graph of one whole step (H2D, kernels on both streams, D2H) per
+  // (mode, buffer pointers); captured on the second call with the same
+  // pointers, replayed after that. Opt-in (RA_ENGINE_GRAPH=1): the step is
+  // one ~0.3 ms latency-bound search, launch overhead is a few microseconds,
+  // and replaying measured no faster on B200.
+  struct StepGraph {
+    const void* key[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    int seen = 0;
+    cudaGraphExec_t exec = nullptr;
+  } sg[2];
+  bool graphs_off = false;
+  cudaStream_t cap_stream = nullptr;  // capture happens here (the legacy stream can't capture)
   ra_ctx* ctx = nullptr;
   uint32_t H = 0, G = 0, d = 0, k = 0;
   uint64_t t = 0, n_pool = 0, n_static = 0;
@@ -573,11 +585,24 @@ void ra_engine_destroy(ra_engine* e) {
     if (e->aux) cudaStreamDestroy(e->aux);
     if (e->fork) cudaEventDestroy(e->fork);
     if (e->join) cudaEventDestroy(e->join);
+    for (auto& g : e->sg)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
   }
   delete e;
 }
 
 namespace {
+// timing event: a real event-record node when the step is being captured
+// into a CUDA graph (a plain record there would only be a dependency marker)
+void record_timing(cudaEvent_t ev, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  RA_CUDA(cudaStreamIsCapturing(s, &st));
+  if (st == cudaStreamCaptureStatusActive)
+    RA_CUDA(cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal));
+  else
+    RA_CUDA(cudaEventRecord(ev, s));
+}
 // run_head for every head (engine.cpp:69-101): search with Mask{W} ->
 // partial over W -> partial over Omega (scores reused) -> merge.
 void engine_enqueue(ra_engine* e, const float* q_dev) {
@@ -597,7 +622,7 @@ void engine_enqueue(ra_engine* e, const float* q_dev) {
     launch_engine_wpartial(e->aux, ea);
     RA_CUDA(cudaEventRecord(e->join, e->aux));
   }
-  RA_CUDA(cudaEventRecord(e->ev[0], s));
+  record_timing(e->ev[0], s);
   if (e->n_pool > 0) {
     SearchArgs sa{};
     sa.desc = e->desc.p;
@@ -621,11 +646,11 @@ void engine_enqueue(ra_engine* e, const float* q_dev) {
     RA_CUDA(cudaMemsetAsync(e->scanned.p, 0, H * 8, s));
     RA_CUDA(cudaMemsetAsync(e->expanded.p, 0, H * 4, s));
   }
-  RA_CUDA(cudaEventRecord(e->ev[1], s));
+  record_timing(e->ev[1], s);
   if (e->fast_attn) {
     RA_CUDA(cudaStreamWaitEvent(s, e->join, 0));
     launch_engine_omega_merge(s, ea);
-    RA_CUDA(cudaEventRecord(e->ev[2], s));
+    record_timing(e->ev[2], s);
     return;
   }
   launch_partial_attention_ex(s, e->kvrefs.p, d, H, q_dev, e->w_ids.p, 0, e->w_m.p, nullptr, 0,
@@ -635,9 +660,118 @@ void engine_enqueue(ra_engine* e, const float* q_dev) {
                               e->o_empty.p, e->flag.p);
   launch_merge(s, H, d, e->ow.p, e->zw.p, e->sw.p, e->w_empty.p, e->oo.p, e->zo.p, e->so.p,
                e->o_empty.p, e->out.p, nullptr, nullptr, e->flag.p);
-  RA_CUDA(cudaEventRecord(e->ev[2], s));
+  record_timing(e->ev[2], s);
 }
 }  // namespace
+
+}  // extern "C"
+
+namespace {
+void step_device_ops(ra_engine* e, const float* q, double* out, uint32_t* omega,
+                     uint64_t* scanned) {
+  cudaStream_t s = e->ctx->stream;
+  engine_enqueue(e, q);
+  if (out)
+    RA_CUDA(cudaMemcpyAsync(out, e->out.p, size_t(e->H) * e->d * 8, cudaMemcpyDeviceToDevice, s));
+  if (omega && e->k)
+    RA_CUDA(cudaMemcpyAsync(omega, e->ids.p, size_t(e->H) * e->k * 4, cudaMemcpyDeviceToDevice, s));
+  if (scanned)
+    RA_CUDA(cudaMemcpyAsync(scanned, e->scanned.p, size_t(e->H) * 8, cudaMemcpyDeviceToDevice, s));
+}
+
+void step_host_ops(ra_engine* e, const float* q, double* out, uint32_t* omega,
+                   uint64_t* scanned) {
+  cudaStream_t s = e->ctx->stream;
+  RA_CUDA(cudaMemcpyAsync(e->q.p, q, size_t(e->H) * e->d * 4, cudaMemcpyHostToDevice, s));
+  engine_enqueue(e, e->q.p);
+  if (out) RA_CUDA(cudaMemcpyAsync(out, e->out.p, size_t(e->H) * e->d * 8, cudaMemcpyDeviceToHost, s));
+  if (omega && e->k)
+    RA_CUDA(cudaMemcpyAsync(omega, e->ids.p, size_t(e->H) * e->k * 4, cudaMemcpyDeviceToHost, s));
+  if (scanned)
+    RA_CUDA(cudaMemcpyAsync(scanned, e->scanned.p, size_t(e->H) * 8, cudaMemcpyDeviceToHost, s));
+}
+
+bool engine_graphs_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("RA_ENGINE_GRAPH");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
+bool pinned_or_device(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeDevice ||
+         at.type == cudaMemoryTypeManaged;
+}
+
+// run `ops` through the step graph cache of slot `mode`
+template <typename Ops>
+void run_step(ra_engine* e, int mode, const void* k0, const void* k1, const void* k2,
+              const void* k3, Ops&& ops) {
+  static const bool env_off = !engine_graphs_enabled();
+  cudaStream_t s = e->ctx->stream;
+  auto& g = e->sg[mode];
+  const void* key[5] = {k0, k1, k2, k3, s};
+  const bool same = std::equal(key, key + 5, g.key);
+  if (env_off || e->graphs_off || !(pinned_or_device(k1) && pinned_or_device(k2) &&
+                                    pinned_or_device(k3) && pinned_or_device(k0))) {
+    ops();
+    return;
+  }
+  if (same && g.exec) {
+    RA_CUDA(cudaGraphLaunch(g.exec, s));
+    return;
+  }
+  if (!same) {
+    std::copy(key, key + 5, g.key);
+    g.seen = 0;
+    if (g.exec) cudaGraphExecDestroy(g.exec), g.exec = nullptr;
+  }
+  if (++g.seen < 2) {  // first call with these buffers: eager (sets kernel attributes)
+    ops();
+    return;
+  }
+  // capture on the engine's private stream (ops read ctx->stream), launch on s
+  cudaGraph_t graph = nullptr;
+  bool ok = true;
+  if (!e->cap_stream && cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
+    ok = false;
+  if (ok) {
+    RA_CUDA(cudaStreamSynchronize(s));  // the eager prefix (e.g. q staging) is done
+    e->ctx->stream = e->cap_stream;
+    if (cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      ok = false;
+    } else {
+      try {
+        ops();
+      } catch (...) {
+        ok = false;
+      }
+      if (cudaStreamEndCapture(e->cap_stream, &graph) != cudaSuccess) ok = false;
+      if (ok && cudaGraphInstantiate(&g.exec, graph, 0) != cudaSuccess) ok = false;
+    }
+    e->ctx->stream = s;
+  }
+  if (graph) cudaGraphDestroy(graph), graph = nullptr;
+  if (!ok) {
+    cudaGetLastError();
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g.exec = nullptr;
+    e->graphs_off = true;
+    ops();
+    return;
+  }
+  RA_CUDA(cudaGraphLaunch(g.exec, s));
+}
+}  // namespace
+
+extern "C" {
 
 ra_status ra_engine_step_device(ra_engine* e, const float* q, double* out, uint32_t* omega,
                                 uint64_t* scanned) {
@@ -645,14 +779,16 @@ ra_status ra_engine_step_device(ra_engine* e, const float* q, double* out, uint3
     if (!e) invalid("null engine");
     if (!e->step_error.empty()) invalid(e->step_error);
     DeviceGuard dg(e->ctx->device);
-    cudaStream_t s = e->ctx->stream;
-    engine_enqueue(e, q);
-    if (out)
-      RA_CUDA(cudaMemcpyAsync(out, e->out.p, size_t(e->H) * e->d * 8, cudaMemcpyDeviceToDevice, s));
-    if (omega && e->k)
-      RA_CUDA(cudaMemcpyAsync(omega, e->ids.p, size_t(e->H) * e->k * 4, cudaMemcpyDeviceToDevice, s));
-    if (scanned)
-      RA_CUDA(cudaMemcpyAsync(scanned, e->scanned.p, size_t(e->H) * 8, cudaMemcpyDeviceToDevice, s));
+    // q is staged into the engine's own buffer so the captured step does not
+    // depend on the caller's (often per-step) query pointer
+    if (!engine_graphs_enabled()) {
+      step_device_ops(e, q, out, omega, scanned);
+      return;
+    }
+    RA_CUDA(cudaMemcpyAsync(e->q.p, q, size_t(e->H) * e->d * 4, cudaMemcpyDeviceToDevice,
+                            e->ctx->stream));
+    run_step(e, 0, nullptr, out, omega, scanned,
+             [&] { step_device_ops(e, e->q.p, out, omega, scanned); });
   });
 }
 
@@ -662,15 +798,8 @@ ra_status ra_engine_step_host(ra_engine* e, const float* q, double* out, uint32_
     if (!e) invalid("null engine");
     if (!e->step_error.empty()) invalid(e->step_error);
     DeviceGuard dg(e->ctx->device);
-    cudaStream_t s = e->ctx->stream;
-    RA_CUDA(cudaMemcpyAsync(e->q.p, q, size_t(e->H) * e->d * 4, cudaMemcpyHostToDevice, s));
-    engine_enqueue(e, e->q.p);
-    if (out) RA_CUDA(cudaMemcpyAsync(out, e->out.p, size_t(e->H) * e->d * 8, cudaMemcpyDeviceToHost, s));
-    if (omega && e->k)
-      RA_CUDA(cudaMemcpyAsync(omega, e->ids.p, size_t(e->H) * e->k * 4, cudaMemcpyDeviceToHost, s));
-    if (scanned)
-      RA_CUDA(cudaMemcpyAsync(scanned, e->scanned.p, size_t(e->H) * 8, cudaMemcpyDeviceToHost, s));
-    RA_CUDA(cudaStreamSynchronize(s));
+    run_step(e, 1, q, out, omega, scanned, [&] { step_host_ops(e, q, out, omega, scanned); });
+    RA_CUDA(cudaStreamSynchronize(e->ctx->stream));
   });
 }
 
