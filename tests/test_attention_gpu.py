@@ -214,3 +214,42 @@ def test_engine_init_from_kvd1_workloads_matches_reference_engine(tmp_path, port
             po = port.partial_attention(Q[h], w["keys"][h // 2], w["values"][h // 2], r.ids)
             ref = port.merge(pw, po, 32)[0]
             assert np.linalg.norm(out[h] - ref) / np.linalg.norm(ref) <= 1e-9
+
+
+def test_engine_graph_replay_matches_eager(tmp_path):
+    """RA_ENGINE_GRAPH=1 (whole-step CUDA graph) gives the same outputs as the
+    eager launches, step after step (subprocess: the switch is read once)."""
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, sys
+sys.path.insert(0, ".")
+import paper_2409_10516_b200 as ra
+from oracle.ffi import Oracle, BuildParams
+port = Oracle("port")
+w = port.generate_workload(2048, 64, 32, 2, 1, seed=9, n_decode=6)
+bp = BuildParams(k_train=32, max_degree=16, ef_construction=64)
+kv = ra.KVGroup(w["keys"][0], w["values"][0])
+gs = [ra.OODGraph.from_blob(kv, port.graph_build(w["keys"][0], w["prefill_q"][h], bp)) for h in range(2)]
+eng = ra.Engine([kv], gs, ra.EngineConfig(128, 512, 100, 128))
+qh = torch.empty((2, 32), dtype=torch.float32, pin_memory=True)
+out = torch.empty((2, 32), dtype=torch.float64, pin_memory=True)
+om = torch.empty((2, 100), dtype=torch.int32, pin_memory=True)
+sc = torch.empty(2, dtype=torch.int64, pin_memory=True)
+res = []
+for s in range(6):
+    qh.copy_(torch.from_numpy(np.ascontiguousarray(w["decode_q"][:, s, :])))
+    eng.ctx.bind_stream()
+    ra.api._check(ra.lib.ra_engine_step_host(eng.h, qh.data_ptr(), out.data_ptr(), om.data_ptr(), sc.data_ptr()))
+    res.append((out.clone().numpy(), om.clone().numpy(), sc.clone().numpy()))
+np.save(sys.argv[1], np.array([np.concatenate([r[0].ravel(), r[1].ravel().astype(np.float64), r[2].astype(np.float64)]) for r in res]))
+'''
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("0", "1"):
+        f = tmp_path / f"r{flag}.npy"
+        env = dict(os.environ, RA_ENGINE_GRAPH=flag)
+        subprocess.run([sys.executable, "-c", code, str(f)], cwd=root, env=env, check=True)
+        outs.append(np.load(f))
+    np.testing.assert_array_equal(outs[0], outs[1])
