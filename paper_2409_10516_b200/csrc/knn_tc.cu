@@ -542,8 +542,30 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
     TcArgs t1{A.p, Bs.p, nq, msamp, K3, cb, nullptr, bufS.p, bufI.p, cnt.p};
     k_knn_tc<<<uint32_t(mt), KNN_THREADS, smem, s>>>(t1);
     const uint32_t r = std::max<uint32_t>(1, uint32_t((uint64_t(target) * msamp + n - 1) / n));
-    k_select_thr<<<uint32_t((nq + 7) / 8), 256, 0, s>>>(bufS.p, cnt.p, nq, cb, r, thr.p);
-    RA_LAUNCH_CHECK();
+    if (r >= 8 || n <= 8u * msamp) {
+      k_select_thr<<<uint32_t((nq + 7) / 8), 256, 0, s>>>(bufS.p, cnt.p, nq, cb, r, thr.p);
+      RA_LAUNCH_CHECK();
+    } else {
+      // large n: the r-th of 2048 samples is too noisy (r < 8). A coarse
+      // threshold (10th of 2048) filters a sample 8-64x larger, whose r2-th
+      // largest (r2 ~ 10) sets the final threshold.
+      k_select_thr<<<uint32_t((nq + 7) / 8), 256, 0, s>>>(bufS.p, cnt.p, nq, cb, 10, thr.p);
+      uint32_t m2 = msamp;
+      while (m2 < n / 64 && m2 < 65536) m2 *= 2;
+      m2 = (m2 / TN) * TN;
+      DevBuf<float> ks2(size_t(m2) * d);
+      DevBuf<uint16_t> Bs2(size_t(m2) * K3);
+      DevBuf<float> thr2(nq);
+      k_gather_sample<<<uint32_t((uint64_t(m2) * d + 255) / 256), 256, 0, s>>>(K, n, d, m2, ks2.p);
+      k_split<<<uint32_t((uint64_t(m2) * d + 255) / 256), 256, 0, s>>>(ks2.p, m2, d, TN, m2 / TN, 0,
+                                                                      Bs2.p);
+      TcArgs t1b{A.p, Bs2.p, nq, m2, K3, cb, thr.p, bufS.p, bufI.p, cnt.p};
+      k_knn_tc<<<uint32_t(mt), KNN_THREADS, smem, s>>>(t1b);
+      const uint32_t r2 = std::max<uint32_t>(1, uint32_t((uint64_t(target) * m2 + n - 1) / n));
+      k_select_thr<<<uint32_t((nq + 7) / 8), 256, 0, s>>>(bufS.p, cnt.p, nq, cb, r2, thr2.p);
+      RA_CUDA(cudaMemcpyAsync(thr.p, thr2.p, nq * 4, cudaMemcpyDeviceToDevice, s));
+      RA_LAUNCH_CHECK();
+    }
   }
   // pass 2: every key, keep S~ > threshold
   TcArgs t2{A.p, B.p, nq, n, K3, cb, sampled ? thr.p : nullptr, bufS.p, bufI.p, cnt.p};
