@@ -33,6 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "decode attention ms/token @128K (Llama-3-8B shape); search recall@100; HBM GB/s"
+TPUT_R = 128  # batched line: 128 decode queries per head x 32 heads = 4096 searches
 
 
 def parse():
@@ -167,7 +168,9 @@ def main():
     by_heads = a.shard == "heads" and n_world > 1
     my_groups = (groups_for_rank(G, n_world, rank) if by_heads else list(range(G)))
     layer = rank if (a.impl == "ours" and not by_heads) else 0
-    n_dec = a.warmup + 2 * a.steps + 2
+    # decode queries: the timed steps, the e2e steps, and one batched step of
+    # TPUT_R queries per head (the throughput line)
+    n_dec = max(a.warmup + 2 * a.steps + 2, TPUT_R)
     # synthetic layer l uses seed 7 + l (SURVEY §8 d; the reference has no layers)
     spec = WorkloadSpec(n_ctx=a.n_ctx, d_model=256, d_head=128, n_heads=H, n_kv_groups=G,
                         seed=7 + layer, n_decode=n_dec)
@@ -330,11 +333,12 @@ def batched_throughput(a, ra, kvs, graphs, Q, cfg, flush, stream):
     """Batched decode: R decode queries per head issued as ONE engine step
     over R x H heads (graphs and KV groups repeated R times, so every query
     walks its head's real graph and KV): search (throughput-mode kernel) +
-    static/retrieved partial attention + merge for R x H queries. A proxy for
-    the layer-batched step of configs[2] (32 layers x batch 1 on one GPU)
-    with the layer's KV shared by the R queries of a head."""
+    static/retrieved partial attention + merge for R x H queries (R = 128:
+    4096 searches, the per-GPU search count of configs[2] - 32 layers x batch
+    8 - sharded over 2 GPUs) with the layer's KV shared by the R queries of a
+    head."""
     import torch
-    R = min(32, Q.shape[0])
+    R = min(TPUT_R, Q.shape[0])
     Hl = len(graphs)
     eng = ra.Engine(list(kvs) * R, list(graphs) * R, cfg)
     qb = [Q[j:j + R].reshape(R * Hl, -1).contiguous()
