@@ -58,7 +58,10 @@ namespace {
 #define RA_PIPE_WARPS 8
 #endif
 constexpr uint32_t kPW = RA_PIPE_WARPS;  // warps per CTA: 0 commits, 1.. pre-expand
-constexpr uint32_t kTW = 8;        // TP mode: queries (warps) per CTA
+#ifndef RA_TP_WARPS
+#define RA_TP_WARPS 8
+#endif
+constexpr uint32_t kTW = RA_TP_WARPS;  // TP mode: queries (warps) per CTA
 #ifndef RA_TP_MINB
 #define RA_TP_MINB 2  // <= 128 registers: 16 query warps per SM
 #endif
