@@ -325,4 +325,29 @@ int ref_engine_step(void* e, const float* q, uint64_t step, double* out, uint32_
   });
 }
 
+// decode_run (engine.cpp:117-155) over stored decode queries
+// [n_heads][n_steps][d]: the trace JSONL (to_jsonl) and summary JSON (to_json)
+// copied into caller buffers (lengths returned; call with cap 0 to size).
+int ref_engine_run(void* e, const float* dq, uint64_t n_steps, int compute_reference,
+                   int include_omega, char* jsonl, uint64_t cap1, uint64_t* len1,
+                   char* summary, uint64_t cap2, uint64_t* len2, double* mse_out) {
+  return guard([&] {
+    auto& st = static_cast<RefEngine*>(e)->st;
+    const uint32_t d = st.heads[0].keys->d;
+    st.config.compute_reference = compute_reference != 0;
+    st.decode_queries.clear();
+    for (size_t h = 0; h < st.heads.size(); ++h)
+      st.decode_queries.push_back(*make_set(Role::Query, dq + h * n_steps * d, n_steps, d));
+    auto r = decode_run(st, n_steps);
+    const std::string a = r.trace.to_jsonl(include_omega != 0), b = r.summary.to_json();
+    *len1 = a.size();
+    *len2 = b.size();
+    if (jsonl && cap1 >= a.size()) std::memcpy(jsonl, a.data(), a.size());
+    if (summary && cap2 >= b.size()) std::memcpy(summary, b.data(), b.size());
+    if (mse_out)
+      for (size_t i = 0; i < r.trace.entries.size(); ++i)
+        mse_out[i] = r.trace.entries[i].mse ? *r.trace.entries[i].mse : -1.0;
+  });
+}
+
 }  // extern "C"

@@ -62,7 +62,7 @@ ra_status ra_ctx_create(int device, ra_ctx** out) {
 
 void ra_ctx_destroy(ra_ctx* ctx) {
   if (!ctx) return;
-  DeviceGuard dg(ctx->device);
+  DeviceGuard dg(ctx->device, true);
   cudaStreamSynchronize(ctx->stream);
   delete ctx;
 }
@@ -111,7 +111,7 @@ void ra_kv_retain(ra_kv* kv) {
 }
 void ra_kv_release(ra_kv* kv) {
   if (kv && kv->refs.fetch_sub(1) == 1) {
-    DeviceGuard dg(kv->device);
+    DeviceGuard dg(kv->device, true);
     delete kv;
   }
 }
@@ -212,7 +212,7 @@ ra_status ra_graph_serialize(const ra_graph* g, char* buf, uint64_t cap, uint64_
 void ra_graph_free(ra_graph* g) {
   if (!g) return;
   {
-    DeviceGuard dg(g->kv ? g->kv->device : 0);
+    DeviceGuard dg(g->kv ? g->kv->device : 0, true);
     g->adj.reset();
   }
   ra_kv_release(g->kv);
@@ -577,7 +577,7 @@ ra_status ra_engine_create(ra_ctx* ctx, ra_kv* const* groups, uint32_t n_groups,
 void ra_engine_destroy(ra_engine* e) {
   if (!e) return;
   {
-    DeviceGuard dg(e->ctx->device);
+    DeviceGuard dg(e->ctx->device, true);
     cudaStreamSynchronize(e->ctx->stream);
     for (ra_kv* g : e->groups) ra_kv_release(g);
     for (auto& ev : e->ev)

@@ -139,9 +139,17 @@ namespace ra {
 
 struct DeviceGuard {
   int prev = -1;
-  explicit DeviceGuard(int dev) {
+  // no_throw: for destroy/release paths (possibly at process teardown, when
+  // the runtime is already gone) - a failure there must not terminate
+  explicit DeviceGuard(int dev, bool no_throw = false) {
     cudaGetDevice(&prev);
-    if (prev != dev) RA_CUDA(cudaSetDevice(dev));
+    if (prev != dev) {
+      if (no_throw) {
+        if (cudaSetDevice(dev) != cudaSuccess) cudaGetLastError();
+      } else {
+        RA_CUDA(cudaSetDevice(dev));
+      }
+    }
   }
   ~DeviceGuard() {
     int cur;
