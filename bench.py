@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-bf16", action="store_true", help="skip the bf16-KV measurement")
     ap.add_argument("--flush-mb", type=int, default=512)
     ap.add_argument("--shard", default="layers", choices=["layers", "heads"],
                     help="N>1: layers = weak scaling, rank r decodes its own synthetic layer "
@@ -263,6 +264,9 @@ def main():
         e2e.append(e0.elapsed_time(e1))
 
     tput = batched_throughput(a, ra, kvs, graphs, Q, cfg, flush, stream)
+    out32 = eng.decode_step_device(Q[a.warmup])[0].cpu().numpy()
+    bf16 = (bf16_mode(a, ra, spec, my_groups, hpg, Q, cfg, flush, stream, out32, graphs)
+            if not a.no_bf16 else None)
 
     ms = statistics.mean(times)
     ms_search = statistics.mean(search_ms)
@@ -312,6 +316,7 @@ def main():
                    "scan_fraction": statistics.mean(scanned) / Hl / (a.n_ctx - 640)},
         "clocks": clk.summary(),
         "throughput": tput,
+        "bf16_kv": bf16,
         "setup_s": round(setup_s, 1),
         "build_ms_per_head": round(statistics.mean(build_ms), 1),
         "build_phase_ms_per_head": {
@@ -329,7 +334,7 @@ def main():
         dist.destroy_process_group()
 
 
-def batched_throughput(a, ra, kvs, graphs, Q, cfg, flush, stream):
+def batched_throughput(a, ra, kvs, graphs, Q, cfg, flush, stream, row_bytes=512):
     """Batched decode: R decode queries per head issued as ONE engine step
     over R x H heads (graphs and KV groups repeated R times, so every query
     walks its head's real graph and KV): search (throughput-mode kernel) +
@@ -361,7 +366,7 @@ def batched_throughput(a, ra, kvs, graphs, Q, cfg, flush, stream):
         sc.append(s)
         ex.append(e)
     ms, ms_s = statistics.mean(times), statistics.mean(s_ms)
-    by = statistics.mean([s * 128 * 4 + e * a.max_degree * 4 for s, e in zip(sc, ex)])
+    by = statistics.mean([s * row_bytes + e * a.max_degree * 4 for s, e in zip(sc, ex)])
     peak, kind = measured_peaks()
     gbs = by / (ms_s * 1e-3) / 1e9
     del eng
@@ -373,6 +378,66 @@ def batched_throughput(a, ra, kvs, graphs, Q, cfg, flush, stream):
             "search_GBps": round(gbs, 1), "search_frac": round(gbs / peak, 4),
             "peak_source": kind,
             "note": "one engine step over R x H heads; KV of each head shared by its R queries"}
+
+
+def bf16_mode(a, ra, spec, my_groups, hpg, Q, cfg, flush, stream, out32, graphs32):
+    """The same decode step on bf16 KV groups, two ways:
+    bf16      - K/V rounded to bf16 (nearest even), graphs rebuilt on the
+                rounded keys from the same prefill queries: exactly the
+                reference's results on the rounded inputs, half the bytes;
+    bf16_attn - the search keeps the exact f32 keys (ids identical to f32,
+                graphs reused), the sparse attention reads bf16 K/V.
+    Per mode: step time, the batched line, the output's distance from f32."""
+    import torch
+    from paper_2409_10516_b200.workload import generate_group
+    bp = ra.OODGraphBuildParams(a.k_train, a.max_degree, a.ef_construction, 8)
+    res = {}
+    for mode in ("bf16", "bf16_attn"):
+        kvs, graphs = [], []
+        for gi, g in enumerate(my_groups):
+            w = generate_group(spec, g, Q.device)
+            kv = ra.KVGroup(w["keys"], w["values"], dtype=mode)
+            kvs.append(kv)
+            if mode == "bf16":
+                graphs += [ra.ood_build(kv, w["prefill_q"][m], bp) for m in range(hpg)]
+            else:
+                graphs += [ra.OODGraph.from_blob(kv, graphs32[gi * hpg + m].serialize())
+                           for m in range(hpg)]
+            del w
+        eng = ra.Engine(kvs, graphs, cfg)
+        for i in range(a.warmup):
+            eng.decode_step_device(Q[i])
+        torch.cuda.synchronize()
+        times, s_ms, sc, ex = [], [], [], []
+        for i in range(a.warmup, a.warmup + a.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            eng.decode_step_device(Q[i])
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+            s_ms.append(eng.last_timing()[0])
+            s, e = eng.last_stats()
+            sc.append(s)
+            ex.append(e)
+        o = eng.decode_step_device(Q[a.warmup])[0].cpu().numpy()
+        rel = np.linalg.norm(o - out32, axis=1) / np.linalg.norm(out32, axis=1)
+        rb = 256 if mode == "bf16" else 512
+        by = statistics.mean([s_ * rb + e_ * a.max_degree * 4 for s_, e_ in zip(sc, ex)])
+        tput = batched_throughput(a, ra, kvs, graphs, Q, cfg, flush, stream, row_bytes=rb)
+        del eng
+        res[mode] = {"value": round(statistics.mean(times), 4), "unit": "ms/token",
+                     "search_ms": round(statistics.mean(s_ms), 4),
+                     "search_GBps": round(by / (statistics.mean(s_ms) * 1e-3) / 1e9, 1),
+                     "out_rel_vs_f32": {"max": float(rel.max()), "mean": float(rel.mean())},
+                     "throughput_us_per_query": tput["us_per_query"],
+                     "throughput_search_GBps": tput["search_GBps"]}
+    res["note"] = ("bf16: K/V rounded in HBM, graphs rebuilt on the rounded keys (= the "
+                   "reference on the rounded inputs); bf16_attn: exact f32 search (same ids), "
+                   "bf16 K/V in the attention; north-star bf16 tolerance 1e-2")
+    return res
 
 
 def recall(eng, graphs, kvs, Q, a, ra):

@@ -89,6 +89,15 @@ ra_status ra_ctx_synchronize(ra_ctx* ctx);
  * GQA group (refcount), mirroring the shared_ptr<const VectorSet>. */
 ra_status ra_kv_create(ra_ctx* ctx, const float* keys, const float* values, uint64_t n,
                        uint32_t d, int on_device, ra_kv** out);
+/* bf16 KV group: keys and values also kept rounded to bf16 (nearest even).
+ * attention_only = 0: search and attention read the bf16 rows - exactly the
+ *   reference's arithmetic on the rounded inputs (half the decode bytes);
+ * attention_only = 1: the search keeps the exact f32 keys (retrieved ids
+ *   identical to f32), the sparse attention reads bf16 K/V.
+ * ra_kv_is_bf16: 0 = f32, 1 = bf16, 2 = bf16 attention only. */
+ra_status ra_kv_create_bf16(ra_ctx* ctx, const float* keys, const float* values, uint64_t n,
+                            uint32_t d, int on_device, int attention_only, ra_kv** out);
+int ra_kv_is_bf16(const ra_kv* kv);
 void ra_kv_retain(ra_kv* kv);
 void ra_kv_release(ra_kv* kv);
 uint64_t ra_kv_size(const ra_kv* kv);

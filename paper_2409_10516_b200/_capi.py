@@ -51,6 +51,9 @@ _SIGS = {
     "ra_ctx_synchronize": (C.c_int, [c_vp]),
     "ra_kv_create": (C.c_int, [c_vp, c_vp, c_vp, C.c_uint64, C.c_uint32, C.c_int,
                                C.POINTER(c_vp)]),
+    "ra_kv_create_bf16": (C.c_int, [c_vp, c_vp, c_vp, C.c_uint64, C.c_uint32, C.c_int,
+                                    C.c_int, C.POINTER(c_vp)]),
+    "ra_kv_is_bf16": (C.c_int, [c_vp]),
     "ra_kv_retain": (None, [c_vp]),
     "ra_kv_release": (None, [c_vp]),
     "ra_kv_size": (C.c_uint64, [c_vp]),

@@ -113,7 +113,15 @@ class KVGroup:
     """One GQA group's keys (and values) resident in HBM; shared by its heads
     the way HeadWorkload shares shared_ptr<const VectorSet> (types.hpp:54-61)."""
 
-    def __init__(self, keys, values=None, ctx: Optional[Context] = None):
+    def __init__(self, keys, values=None, ctx: Optional[Context] = None, dtype: str = "f32"):
+        """dtype "bf16": K and V are rounded to bf16 (nearest even) and the
+        decode path reads bf16 rows (half the HBM bytes); results equal the
+        reference's on the rounded inputs (keys_tensor() holds them as f32).
+        dtype "bf16_attn": the search keeps the exact f32 keys (retrieved ids
+        identical to f32) and only the sparse attention reads bf16 K/V."""
+        if dtype not in ("f32", "bf16", "bf16_attn"):
+            raise InvalidArgument("dtype must be f32, bf16 or bf16_attn")
+        self.dtype = dtype
         self.ctx = ctx or default_context()
         dev = torch.device("cuda", self.ctx.device)
         k = _dev(keys, torch.float32, dev)
@@ -124,7 +132,11 @@ class KVGroup:
             raise InvalidArgument("keys and values must have equal n")
         self.n, self.d = int(k.shape[0]), int(k.shape[1])
         h = C.c_void_p()
-        _check(lib.ra_kv_create(self.ctx.h, _ptr(k), _ptr(v), self.n, self.d, 1, C.byref(h)))
+        if dtype == "f32":
+            _check(lib.ra_kv_create(self.ctx.h, _ptr(k), _ptr(v), self.n, self.d, 1, C.byref(h)))
+        else:
+            _check(lib.ra_kv_create_bf16(self.ctx.h, _ptr(k), _ptr(v), self.n, self.d, 1,
+                                         int(dtype == "bf16_attn"), C.byref(h)))
         self.h = h
 
     def __del__(self):

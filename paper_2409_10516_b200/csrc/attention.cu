@@ -160,7 +160,57 @@ __global__ void k_merge(uint32_t B, uint32_t d, const double* ow, const double* 
 // chunks with the same log-sum-exp rescaling merge() uses.
 constexpr uint32_t kWC = 64;  // W rows per CTA
 
+// K/V element access for f32 or bf16 groups (bf16 -> f32 -> f64 is exact)
+__device__ __forceinline__ double elem(const float* p, uint32_t i) { return (double)p[i]; }
+__device__ __forceinline__ double elem(const uint16_t* p, uint32_t i) {
+  return (double)__uint_as_float(uint32_t(p[i]) << 16);
+}
+template <typename T> __device__ __forceinline__ const T* kv_keys(const KVRef& r);
+template <> __device__ __forceinline__ const float* kv_keys<float>(const KVRef& r) { return r.keys; }
+template <> __device__ __forceinline__ const uint16_t* kv_keys<uint16_t>(const KVRef& r) {
+  return r.keys16;
+}
+template <typename T> __device__ __forceinline__ const T* kv_vals(const KVRef& r);
+template <> __device__ __forceinline__ const float* kv_vals<float>(const KVRef& r) { return r.values; }
+template <> __device__ __forceinline__ const uint16_t* kv_vals<uint16_t>(const KVRef& r) {
+  return r.values16;
+}
+// tile row stride in elements: rows stay 16-B aligned for the TMA copies
+template <typename T> constexpr uint32_t kpad() { return 16 / sizeof(T); }
+
+// in-order f64 dot of q (f64) with a staged key row
 template <int D>
+__device__ __forceinline__ double tile_dot(const double* qh, const float* row) {
+  double acc = 0.0;
+  const float4* r4 = reinterpret_cast<const float4*>(row);
+#pragma unroll 8
+  for (int cc = 0; cc < D / 4; ++cc) {
+    const float4 kv = r4[cc];
+    acc = fma(qh[4 * cc + 0], (double)kv.x, acc);
+    acc = fma(qh[4 * cc + 1], (double)kv.y, acc);
+    acc = fma(qh[4 * cc + 2], (double)kv.z, acc);
+    acc = fma(qh[4 * cc + 3], (double)kv.w, acc);
+  }
+  return acc;
+}
+template <int D>
+__device__ __forceinline__ double tile_dot(const double* qh, const uint16_t* row) {
+  double acc = 0.0;
+  const uint4* r4 = reinterpret_cast<const uint4*>(row);
+#pragma unroll 4
+  for (int cc = 0; cc < D / 8; ++cc) {
+    const uint4 w = r4[cc];
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      acc = fma(qh[8 * cc + 2 * t], (double)__uint_as_float(ws[t] << 16), acc);
+      acc = fma(qh[8 * cc + 2 * t + 1], (double)__uint_as_float(ws[t] & 0xFFFF0000u), acc);
+    }
+  }
+  return acc;
+}
+
+template <int D, typename T>
 __global__ void __launch_bounds__(256)
     k_wpartial(const KVRef* __restrict__ gkv, const float* __restrict__ q,
                const uint32_t* __restrict__ W, uint32_t nW, uint32_t hpg, double inv_sqrt_d,
@@ -170,22 +220,23 @@ __global__ void __launch_bounds__(256)
   const uint32_t c = blockIdx.x, g = blockIdx.y, C = gridDim.x;
   const uint32_t tid = threadIdx.x;
   const uint32_t i0 = c * kWC, rows = min(kWC, nW - i0);
+  constexpr uint32_t KS = D + kpad<T>();
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-  float* Kt = reinterpret_cast<float*>(smem + 16);                 // [kWC][D+4]
-  float* Vt = Kt + kWC * (D + 4);                                   // [kWC][D]
+  T* Kt = reinterpret_cast<T*>(smem + 16);                          // [kWC][KS]
+  T* Vt = Kt + kWC * KS;                                            // [kWC][D]
   double* qs = reinterpret_cast<double*>(Vt + kWC * D);             // [hpg][D]
   double* z = qs + size_t(hpg) * D;                                 // [hpg][kWC]
-  const float* K = gkv[g].keys;
-  const float* V = gkv[g].values;
+  const T* K = kv_keys<T>(gkv[g]);
+  const T* V = kv_vals<T>(gkv[g]);
   if (tid == 0) {
     mbar_init(bar);
-    mbar_arrive_expect_tx(bar, rows * D * 8u);
+    mbar_arrive_expect_tx(bar, rows * D * uint32_t(2 * sizeof(T)));
   }
   __syncthreads();
   if (tid < rows) {
     const uint32_t id = W[i0 + tid];
-    bulk_g2s(Kt + tid * (D + 4), K + size_t(id) * D, D * 4u, bar);
-    bulk_g2s(Vt + tid * D, V + size_t(id) * D, D * 4u, bar);
+    bulk_g2s(Kt + tid * KS, K + size_t(id) * D, D * uint32_t(sizeof(T)), bar);
+    bulk_g2s(Vt + tid * D, V + size_t(id) * D, D * uint32_t(sizeof(T)), bar);
   }
   for (uint32_t e = tid; e < hpg * D; e += blockDim.x)
     qs[e] = (double)q[size_t(g) * hpg * D + e];
@@ -194,20 +245,7 @@ __global__ void __launch_bounds__(256)
   for (uint32_t t = tid; t < hpg * kWC; t += blockDim.x) {
     const uint32_t h = t / kWC, i = t % kWC;
     double acc = -DBL_MAX;
-    if (i < rows) {
-      acc = 0.0;
-      const float4* r4 = reinterpret_cast<const float4*>(Kt + i * (D + 4));
-      const double* qh = qs + h * D;
-#pragma unroll 8
-      for (int cc = 0; cc < D / 4; ++cc) {
-        const float4 kv = r4[cc];
-        acc = fma(qh[4 * cc + 0], (double)kv.x, acc);
-        acc = fma(qh[4 * cc + 1], (double)kv.y, acc);
-        acc = fma(qh[4 * cc + 2], (double)kv.z, acc);
-        acc = fma(qh[4 * cc + 3], (double)kv.w, acc);
-      }
-      acc *= inv_sqrt_d;
-    }
+    if (i < rows) acc = tile_dot<D>(qs + h * D, Kt + i * KS) * inv_sqrt_d;
     z[h * kWC + i] = acc;
   }
   __syncthreads();
@@ -233,13 +271,13 @@ __global__ void __launch_bounds__(256)
   for (uint32_t t = tid; t < hpg * D; t += blockDim.x) {
     const uint32_t h = t / D, j = t % D;
     double acc = 0.0;
-    for (uint32_t i = 0; i < rows; ++i) acc = fma(z[h * kWC + i], (double)Vt[i * D + j], acc);
+    for (uint32_t i = 0; i < rows; ++i) acc = fma(z[h * kWC + i], elem(Vt, i * D + j), acc);
     part_out[((size_t(g) * C + c) * hpg + h) * D + j] = acc;
   }
 }
 
 // ---- engine path: Omega partial (search scores reused) + merge per head --------
-template <int D>
+template <int D, typename T>
 __global__ void __launch_bounds__(128)
     k_omega_merge(const KVRef* __restrict__ hkv, const uint32_t* __restrict__ ids,
                   const double* __restrict__ s64, const uint32_t* __restrict__ n_out,
@@ -249,11 +287,11 @@ __global__ void __launch_bounds__(128)
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t h = blockIdx.x, g = h / hpg, hl = h % hpg, tid = threadIdx.x;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-  float* Vt = reinterpret_cast<float*>(smem + 16);                  // [kWC][D]
+  T* Vt = reinterpret_cast<T*>(smem + 16);                          // [kWC][D]
   double* e = reinterpret_cast<double*>(Vt + kWC * D);              // [kWC]
   __shared__ double red[4];
   const uint32_t m = n_out[h];
-  const float* V = hkv[h].values;
+  const T* V = kv_vals<T>(hkv[h]);
   if (tid == 0) mbar_init(bar);
   // Omega max (scores are exact f64 search scores; z = s / sqrt(d))
   double zo = -DBL_MAX;
@@ -270,11 +308,12 @@ __global__ void __launch_bounds__(128)
     __syncthreads();  // previous tile fully consumed
     if (tid == 0) {
       fence_proxy_async();
-      mbar_arrive_expect_tx(bar, rows * D * 4u);
+      mbar_arrive_expect_tx(bar, rows * D * uint32_t(sizeof(T)));
     }
     __syncthreads();
     if (tid < rows) {
-      bulk_g2s(Vt + tid * D, V + size_t(ids[size_t(h) * k + t0 + tid]) * D, D * 4u, bar);
+      bulk_g2s(Vt + tid * D, V + size_t(ids[size_t(h) * k + t0 + tid]) * D,
+               D * uint32_t(sizeof(T)), bar);
       e[tid] = exp(s64[size_t(h) * k + t0 + tid] * inv_sqrt_d - zo);
     }
     mbar_wait(bar, phase);
@@ -286,7 +325,7 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
       for (uint32_t r = 0; r < (D + 127) / 128; ++r) {
         const uint32_t j = tid + r * 128;
-        if (j < D) acc[r] = fma(ei, (double)Vt[i * D + j], acc[r]);
+        if (j < D) acc[r] = fma(ei, elem(Vt, i * D + j), acc[r]);
       }
     }
   }
@@ -322,27 +361,27 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-template <int D>
+template <int D, typename T>
 void launch_engine_attention_d(cudaStream_t st, const EngineAttn& a, int part) {
   const uint32_t C = (a.nW + kWC - 1) / kWC;
   if (part == 0) {
     if (!C) return;
-    const size_t smem_w = 16 + kWC * (D + 4) * 4 + kWC * D * 4 + size_t(a.hpg) * D * 8 +
-                          size_t(a.hpg) * kWC * 8;
-    RA_CUDA(cudaFuncSetAttribute(k_wpartial<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const size_t smem_w = 16 + kWC * (D + kpad<T>()) * sizeof(T) + kWC * D * sizeof(T) +
+                          size_t(a.hpg) * D * 8 + size_t(a.hpg) * kWC * 8;
+    RA_CUDA(cudaFuncSetAttribute(k_wpartial<D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_w));
-    k_wpartial<D><<<dim3(C, a.G), 256, smem_w, st>>>(a.gkv, a.q, a.W, a.nW, a.hpg,
-                                                      a.inv_sqrt_d, a.part_out, a.part_m,
-                                                      a.part_s);
+    k_wpartial<D, T><<<dim3(C, a.G), 256, smem_w, st>>>(a.gkv, a.q, a.W, a.nW, a.hpg,
+                                                         a.inv_sqrt_d, a.part_out, a.part_m,
+                                                         a.part_s);
     RA_LAUNCH_CHECK();
     return;
   }
-  const size_t smem_o = 16 + kWC * D * 4 + kWC * 8;
-  RA_CUDA(cudaFuncSetAttribute(k_omega_merge<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem_o = 16 + kWC * D * sizeof(T) + kWC * 8;
+  RA_CUDA(cudaFuncSetAttribute(k_omega_merge<D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem_o));
-  k_omega_merge<D><<<a.H, 128, smem_o, st>>>(a.hkv, a.ids, a.s64, a.n_out, a.k, a.hpg, C, a.nW,
-                                             a.inv_sqrt_d, a.part_out, a.part_m, a.part_s,
-                                             a.out);
+  k_omega_merge<D, T><<<a.H, 128, smem_o, st>>>(a.hkv, a.ids, a.s64, a.n_out, a.k, a.hpg, C,
+                                                a.nW, a.inv_sqrt_d, a.part_out, a.part_m,
+                                                a.part_s, a.out);
   RA_LAUNCH_CHECK();
 }
 
@@ -392,13 +431,18 @@ size_t engine_attention_part_doubles(uint32_t G, uint32_t hpg, uint32_t nW, uint
   return size_t(G) * std::max<uint32_t>(C, 1) * hpg * (d + 2);
 }
 
-static void engine_attention(cudaStream_t st, const EngineAttn& a, int part) {
+template <typename T>
+static void engine_attention_t(cudaStream_t st, const EngineAttn& a, int part) {
   switch (a.d) {
-    case 128: launch_engine_attention_d<128>(st, a, part); break;
-    case 64: launch_engine_attention_d<64>(st, a, part); break;
-    case 32: launch_engine_attention_d<32>(st, a, part); break;
+    case 128: launch_engine_attention_d<128, T>(st, a, part); break;
+    case 64: launch_engine_attention_d<64, T>(st, a, part); break;
+    case 32: launch_engine_attention_d<32, T>(st, a, part); break;
     default: throw Error(RA_ERR_RUNTIME, "engine attention: unsupported head dim");
   }
+}
+static void engine_attention(cudaStream_t st, const EngineAttn& a, int part) {
+  if (a.bf16) engine_attention_t<uint16_t>(st, a, part);
+  else engine_attention_t<float>(st, a, part);
 }
 void launch_engine_wpartial(cudaStream_t st, const EngineAttn& a) { engine_attention(st, a, 0); }
 void launch_engine_omega_merge(cudaStream_t st, const EngineAttn& a) {

@@ -106,6 +106,44 @@ ra_status ra_kv_create(ra_ctx* ctx, const float* keys, const float* values, uint
   });
 }
 
+namespace {
+__global__ void k_to_bf16(float* x, uint16_t* y, uint64_t n, int round_f32) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t u = __float_as_uint(x[i]);
+    u += 0x7FFFu + ((u >> 16) & 1u);  // round to nearest even (finite inputs)
+    y[i] = uint16_t(u >> 16);
+    if (round_f32) x[i] = __uint_as_float(uint32_t(y[i]) << 16);
+  }
+}
+}  // namespace
+
+ra_status ra_kv_create_bf16(ra_ctx* ctx, const float* keys, const float* values, uint64_t n,
+                            uint32_t d, int on_device, int attention_only, ra_kv** out) {
+  return guard([&] {
+    ra_kv* kv = nullptr;
+    if (ra_kv_create(ctx, keys, values, n, d, on_device, &kv) != RA_OK)
+      throw Error(RA_ERR_INVALID_ARGUMENT, ra_last_error());
+    std::unique_ptr<ra_kv, void (*)(ra_kv*)> hold(kv, ra_kv_release);
+    DeviceGuard dg(ctx->device);
+    kv->bf16 = !attention_only;
+    kv->bf16_attn = true;
+    const uint64_t m = n * d;
+    const int rnd = attention_only ? 0 : 1;
+    kv->keys16.alloc(std::max<uint64_t>(m, 1));
+    if (m) k_to_bf16<<<1024, 256, 0, ctx->stream>>>(kv->keys.p, kv->keys16.p, m, rnd);
+    if (kv->values.p) {
+      kv->values16.alloc(std::max<uint64_t>(m, 1));
+      if (m) k_to_bf16<<<1024, 256, 0, ctx->stream>>>(kv->values.p, kv->values16.p, m, rnd);
+    }
+    RA_LAUNCH_CHECK();
+    RA_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = hold.release();
+  });
+}
+
+int ra_kv_is_bf16(const ra_kv* kv) { return !kv ? 0 : kv->bf16 ? 1 : kv->bf16_attn ? 2 : 0; }
+
 void ra_kv_retain(ra_kv* kv) {
   if (kv) kv->refs.fetch_add(1);
 }
@@ -273,16 +311,18 @@ ra_status ra_graph_search_batch(ra_ctx* ctx, const ra_graph* const* graphs, uint
   return guard([&] {
     check_ctx(ctx);
     if (B == 0) return;
-    uint32_t max_n = 0, max_M = 0;
+    uint32_t max_n = 0, max_M = 0, n_bf16 = 0;
     std::vector<GraphDesc> desc(B);
     for (uint32_t b = 0; b < B; ++b) {
       const ra_graph* g = graphs[b];
       if (!g) invalid("null graph");
+      n_bf16 += g->kv->bf16;
       if (q_dim != g->kv->d) invalid("query dimension mismatch");  // :359
       if (k < 1) invalid("k must be >= 1");                         // :360
       const uint64_t e = ef >= 0 ? uint64_t(ef) : g->default_ef;
       if (e < k) invalid("ef must be >= k");                        // :362
-      desc[b] = GraphDesc{g->adj.p, g->kv->keys.p, g->entry, uint32_t(g->n), g->max_degree,
+      desc[b] = GraphDesc{g->adj.p, g->kv->keys.p, g->kv->bf16 ? g->kv->keys16.p : nullptr,
+                          g->entry, uint32_t(g->n), g->max_degree,
                           uint32_t(std::min<uint64_t>(e, 0xFFFFFFFFu)), 0};
       max_n = std::max<uint32_t>(max_n, uint32_t(g->n));
       max_M = std::max<uint32_t>(max_M, g->max_degree);
@@ -296,6 +336,7 @@ ra_status ra_graph_search_batch(ra_ctx* ctx, const ra_graph* const* graphs, uint
     RA_CUDA(cudaMemcpyAsync(d_desc, desc.data(), B * sizeof(GraphDesc), cudaMemcpyHostToDevice,
                             ctx->stream));
     if (mask_n) launch_mask_bitset(ctx->stream, mask, mask_n, bits, words);
+    if (n_bf16 && n_bf16 != B) invalid("mixed f32 and bf16 key groups in one batch");
     SearchArgs sa{};
     sa.desc = d_desc;
     sa.q = q;
@@ -304,6 +345,7 @@ ra_status ra_graph_search_batch(ra_ctx* ctx, const ra_graph* const* graphs, uint
     sa.d = q_dim;
     sa.k = k;
     sa.max_M = max_M;
+    sa.bf16 = n_bf16 == B;
     sa.ids = ids;
     sa.scores = scores;
     sa.scores64 = nullptr;
@@ -399,7 +441,7 @@ ra_status ra_partial_attention(ra_ctx* ctx, ra_kv* kv, uint32_t B, const float* 
     uint8_t* a = arena<uint8_t>(ctx->scratch_a, refs_bytes + 256);
     KVRef* refs = reinterpret_cast<KVRef*>(a);
     uint32_t* flag = reinterpret_cast<uint32_t*>(a + refs_bytes);
-    std::vector<KVRef> h(B, KVRef{kv->keys.p, kv->values.p, kv->n});
+    std::vector<KVRef> h(B, KVRef{kv->keys.p, kv->values.p, kv->n, nullptr, nullptr});
     RA_CUDA(cudaMemcpyAsync(refs, h.data(), B * sizeof(KVRef), cudaMemcpyHostToDevice,
                             ctx->stream));
     RA_CUDA(cudaMemsetAsync(flag, 0, 4, ctx->stream));
@@ -493,6 +535,9 @@ ra_status ra_engine_create(ra_ctx* ctx, ra_kv* const* groups, uint32_t n_groups,
     for (uint32_t h = 0; h < n_heads; ++h)
       if (!head_graphs[h] || head_graphs[h]->kv != groups[h / per])
         invalid("head graph is not built over its group's keys");
+    for (uint32_t gi = 1; gi < n_groups; ++gi)
+      if (groups[gi]->bf16 != groups[0]->bf16 || groups[gi]->bf16_attn != groups[0]->bf16_attn)
+        invalid("mixed f32 and bf16 key groups");
     DeviceGuard dg(ctx->device);
     auto e = std::make_unique<ra_engine>();
     e->ctx = ctx;
@@ -521,9 +566,11 @@ ra_status ra_engine_create(ra_ctx* ctx, ra_kv* const* groups, uint32_t n_groups,
       const ra_graph* g = head_graphs[h];
       const uint64_t ef = cfg->ef >= 0 ? uint64_t(cfg->ef) : g->default_ef;
       if (np > 0 && ef < e->k) e->step_error = "ef must be >= k";
-      desc[h] = GraphDesc{g->adj.p, g->kv->keys.p, g->entry, uint32_t(g->n), g->max_degree,
+      desc[h] = GraphDesc{g->adj.p, g->kv->keys.p, g->kv->bf16 ? g->kv->keys16.p : nullptr,
+                          g->entry, uint32_t(g->n), g->max_degree,
                           uint32_t(std::min<uint64_t>(ef, 0xFFFFFFFFu)), 0};
-      refs[h] = KVRef{g->kv->keys.p, g->kv->values.p, g->kv->n};
+      refs[h] = KVRef{g->kv->keys.p, g->kv->values.p, g->kv->n, g->kv->keys16.p,
+                      g->kv->values16.p};
       e->max_n = std::max<uint32_t>(e->max_n, uint32_t(g->n));
       e->max_M = std::max<uint32_t>(e->max_M, g->max_degree);
     }
@@ -537,7 +584,8 @@ ra_status ra_engine_create(ra_ctx* ctx, ra_kv* const* groups, uint32_t n_groups,
     up(e->kvrefs, refs);
     std::vector<KVRef> grefs(n_groups);
     for (uint32_t gi = 0; gi < n_groups; ++gi)
-      grefs[gi] = KVRef{groups[gi]->keys.p, groups[gi]->values.p, groups[gi]->n};
+      grefs[gi] = KVRef{groups[gi]->keys.p, groups[gi]->values.p, groups[gi]->n,
+                        groups[gi]->keys16.p, groups[gi]->values16.p};
     up(e->gkv, grefs);
     e->hpg = per;
     e->fast_attn = engine_attention_supported(d);
@@ -615,7 +663,8 @@ void engine_enqueue(ra_engine* e, const float* q_dev) {
     ea = EngineAttn{e->gkv.p, e->kvrefs.p, q_dev, e->w_ids.p, uint32_t(e->n_static), e->G, H,
                     e->hpg, d, e->k, 1.0 / std::sqrt(double(d)), e->ids.p, e->scores64.p,
                     e->n_out.p, e->part.p, e->part.p + size_t(e->G) * std::max(C, 1u) * e->hpg * d,
-                    e->part.p + size_t(e->G) * std::max(C, 1u) * e->hpg * (d + 1), e->out.p};
+                    e->part.p + size_t(e->G) * std::max(C, 1u) * e->hpg * (d + 1), e->out.p,
+                    uint32_t(e->groups[0]->bf16_attn)};
     // fork: the W partials depend only on q, so they run beside the search
     RA_CUDA(cudaEventRecord(e->fork, s));
     RA_CUDA(cudaStreamWaitEvent(e->aux, e->fork, 0));
@@ -632,6 +681,7 @@ void engine_enqueue(ra_engine* e, const float* q_dev) {
     sa.d = d;
     sa.k = e->k;
     sa.max_M = e->max_M;
+    sa.bf16 = e->groups[0]->bf16;
     sa.ids = e->ids.p;
     sa.scores = e->scores.p;
     sa.scores64 = e->scores64.p;

@@ -91,6 +91,7 @@ struct DevBuf {
 struct GraphDesc {
   const uint32_t* adj;  // [n][M], kSentinel-padded rows
   const float* keys;    // [n][d]
+  const uint16_t* keys16;  // [n][d] bf16 copy (bf16 KV groups), else nullptr
   uint64_t entry;
   uint32_t n, M;
   uint32_t ef;          // resolved ef for this query
@@ -118,6 +119,14 @@ struct ra_kv {
   uint32_t d = 0;
   ra::DevBuf<float> keys;    // n x d row-major (f32, the reference's VectorSet layout)
   ra::DevBuf<float> values;  // n x d row-major (may be empty)
+  // bf16 KV groups (ra_kv_create_bf16): K and V also stored rounded to bf16
+  // (RNE). bf16: the search reads bf16 key rows too, and the f32 arrays above
+  // hold the same rounded values (builder, generic paths) - the reference's
+  // results on the rounded inputs. bf16_attn only: the search keeps the exact
+  // f32 keys (retrieved ids identical to f32), attention reads bf16 K/V.
+  bool bf16 = false;
+  bool bf16_attn = false;
+  ra::DevBuf<uint16_t> keys16, values16;
 };
 
 struct ra_graph {
@@ -188,6 +197,7 @@ struct SearchArgs {
   uint8_t* spill;
   uint32_t* vis_global;
   uint32_t flags;  // profiling switches (RA_PIPE_FLAGS): 1 = helpers idle
+  uint32_t bf16;   // every desc[b].keys16 is set: score from the bf16 rows
 };
 
 // Returns bytes of scratch needed for (B, max_n, d); then launches.
@@ -208,6 +218,8 @@ struct KVRef {
   const float* keys;
   const float* values;
   uint64_t n;
+  const uint16_t* keys16;    // bf16 groups only
+  const uint16_t* values16;
 };
 void launch_partial_attention_ex(cudaStream_t s, const KVRef* kvs, uint32_t d, uint32_t B, const float* q,
                                  const uint32_t* idx, uint32_t m_stride, const uint32_t* m,
@@ -236,6 +248,7 @@ struct EngineAttn {
   double* part_m;        // [G][C][hpg]
   double* part_s;
   double* out;           // [H][d]
+  uint32_t bf16;         // K/V read from the groups' bf16 copies
 };
 bool engine_attention_supported(uint32_t d);
 size_t engine_attention_part_doubles(uint32_t G, uint32_t hpg, uint32_t nW, uint32_t d);

@@ -1094,10 +1094,12 @@ int search_variant() {
 void launch_graph_search(ra_ctx* ctx, SearchArgs a, uint32_t max_n, uint8_t* scratch) {
   if (a.B == 0) return;
   const int variant = search_variant();
-  if ((variant == 0 || variant >= 3) &&
+  if ((variant == 0 || variant >= 3 || a.bf16) &&
       launch_graph_search_pipe(ctx, a, max_n, scratch,
                                variant == 3 ? 1 : variant == 4 ? 2 : 0))
     return;
+  // the older kernels read f32 rows; the f32 copy of a bf16 group holds the
+  // same rounded values, so they stay exact for shapes the pipe kernel skips
   // v3 (CTA per query, speculative pre-expansion) for the common shapes
   if (a.max_M <= 32 && variant <= 1) {
     bool done = false;

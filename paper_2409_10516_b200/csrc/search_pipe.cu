@@ -112,6 +112,31 @@ __device__ __forceinline__ double row_dot(const double* __restrict__ qd,
   return acc;
 }
 
+__device__ __forceinline__ double bf_lo(uint32_t w) { return (double)__uint_as_float(w << 16); }
+__device__ __forceinline__ double bf_hi(uint32_t w) { return (double)__uint_as_float(w & 0xFFFF0000u); }
+
+// in-order f64 dot of q and a bf16 row (8 elements per 16-B word; bf16 ->
+// f32 -> f64 is exact, so this is dot_f64 on the rounded key)
+template <int D>
+__device__ __forceinline__ double row_dot_bf(const double* __restrict__ qd,
+                                             const uint4* __restrict__ r4, bool global) {
+  double acc = 0.0;
+#pragma unroll 4
+  for (int c = 0; c < D / 8; ++c) {
+    const uint4 w = global ? __ldg(r4 + c) : r4[c];
+    const double* q8 = qd + 8 * c;
+    acc = fma(q8[0], bf_lo(w.x), acc);
+    acc = fma(q8[1], bf_hi(w.x), acc);
+    acc = fma(q8[2], bf_lo(w.y), acc);
+    acc = fma(q8[3], bf_hi(w.y), acc);
+    acc = fma(q8[4], bf_lo(w.z), acc);
+    acc = fma(q8[5], bf_hi(w.z), acc);
+    acc = fma(q8[6], bf_lo(w.w), acc);
+    acc = fma(q8[7], bf_hi(w.w), acc);
+  }
+  return acc;
+}
+
 // 32-lane bitonic sort, best-first
 __device__ __forceinline__ void sort32(uint64_t& k, uint32_t& id, uint32_t lane) {
 #pragma unroll
@@ -178,7 +203,8 @@ struct Arr {  // (key, id) array: k u64[cap] then id u32[cap]
 // TP (throughput mode): every warp is a commit warp running its own query
 // with inline expansions (key rows straight into registers), kTW queries
 // per CTA, visited set in HBM/L2; for batches that fill the GPU many times.
-template <int D, bool VS, bool TP>
+// BF: key rows are read from the group's bf16 copy (half the bytes)
+template <int D, bool VS, bool TP, bool BF>
 __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     k_graph_search_pipe(SearchArgs a, PipeLayout lay, uint32_t spill_cap) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -188,6 +214,8 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
   const GraphDesc g = a.desc[b];
   const uint32_t M = g.M, ef = g.ef, k = a.k, n = g.n;
   const float* __restrict__ keys = g.keys;
+  const uint16_t* __restrict__ keys16 = g.keys16;
+  constexpr uint32_t kRowBytes = uint32_t(D) * (BF ? 2u : 4u);
   const uint32_t* __restrict__ adj = g.adj;
   constexpr uint32_t RS = D + 4;
 
@@ -250,27 +278,37 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     sk = 0;
     if constexpr (TP) {
       if (isnew) {
-        const float4* r4 = reinterpret_cast<const float4*>(keys + size_t(v) * D);
         double acc = 0.0;
+        if constexpr (BF) {
+          acc = row_dot_bf<D>(qd, reinterpret_cast<const uint4*>(keys16 + size_t(v) * D), true);
+        } else {
+          const float4* r4 = reinterpret_cast<const float4*>(keys + size_t(v) * D);
 #pragma unroll
-        for (int c = 0; c < D / 4; ++c) {
-          const float4 kk = __ldg(r4 + c);
-          acc = fma(qd[4 * c + 0], (double)kk.x, acc);
-          acc = fma(qd[4 * c + 1], (double)kk.y, acc);
-          acc = fma(qd[4 * c + 2], (double)kk.z, acc);
-          acc = fma(qd[4 * c + 3], (double)kk.w, acc);
+          for (int c = 0; c < D / 4; ++c) {
+            const float4 kk = __ldg(r4 + c);
+            acc = fma(qd[4 * c + 0], (double)kk.x, acc);
+            acc = fma(qd[4 * c + 1], (double)kk.y, acc);
+            acc = fma(qd[4 * c + 2], (double)kk.z, acc);
+            acc = fma(qd[4 * c + 3], (double)kk.w, acc);
+          }
         }
         sk = okey(acc);
       }
     } else if (newmask) {
       float* row = tile + size_t(__popc(newmask & lanemask_lt(lane))) * RS;
       fence_proxy_async();
-      if (lane == 0) mbar_arrive_expect_tx(bar, __popc(newmask) * uint32_t(D) * 4u);
+      if (lane == 0) mbar_arrive_expect_tx(bar, __popc(newmask) * kRowBytes);
       __syncwarp();
-      if (isnew) bulk_g2s(row, keys + size_t(v) * D, uint32_t(D) * 4u, bar);
+      if (isnew) {
+        if constexpr (BF) bulk_g2s(row, keys16 + size_t(v) * D, kRowBytes, bar);
+        else bulk_g2s(row, keys + size_t(v) * D, kRowBytes, bar);
+      }
       mbar_wait(bar, phase);
       phase ^= 1u;
-      if (isnew) sk = okey(row_dot<D>(qd, row));
+      if (isnew) {
+        if constexpr (BF) sk = okey(row_dot_bf<D>(qd, reinterpret_cast<const uint4*>(row), false));
+        else sk = okey(row_dot<D>(qd, row));
+      }
     }
   };
 
@@ -897,7 +935,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
   }
 }
 
-template <int D>
+template <int D, bool BF>
 bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* scratch,
                    bool tp) {
   const size_t budget = ctx->smem_optin ? ctx->smem_optin : 227 * 1024;
@@ -912,7 +950,7 @@ bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* sc
   if (tp) {
     PipeLayout lay{uint32_t(D), std::max<uint32_t>(a.max_M, 1), (max_n + 31) / 32, 0, 256};
     const size_t bytes = kTW * lay.tp_warp_bytes();
-    auto kern = k_graph_search_pipe<D, false, true>;
+    auto kern = k_graph_search_pipe<D, false, true, BF>;
     RA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
     kern<<<(a.B + kTW - 1) / kTW, kTW * 32, bytes, ctx->stream>>>(s, lay, spill_cap);
     RA_LAUNCH_CHECK();
@@ -924,8 +962,8 @@ bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* sc
   if (fixed + PipeLayout::arr_bytes(256) * 2 > budget) return false;
   lay.capO = uint32_t(std::min<size_t>((budget - fixed - 64) / 24, 8192)) & ~31u;
   if (lay.bytes() > budget) return false;
-  auto kern = lay.vis_smem ? k_graph_search_pipe<D, true, false>
-                           : k_graph_search_pipe<D, false, false>;
+  auto kern = lay.vis_smem ? k_graph_search_pipe<D, true, false, BF>
+                           : k_graph_search_pipe<D, false, false, BF>;
   RA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                int(lay.bytes())));
   kern<<<a.B, kPW * 32, lay.bytes(), ctx->stream>>>(s, lay, spill_cap);
@@ -948,12 +986,20 @@ bool launch_graph_search_pipe(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n,
                               uint8_t* scratch, int mode) {
   if (a.max_M > 32 || a.max_M == 0) return false;
   const bool tp = mode == 1 || (mode == 0 && a.B > 2u * uint32_t(ctx->num_sms));
+  if (a.bf16) {  // bf16 rows: d in {32, 64, 128} (16-B multiples)
+    switch (a.d) {
+      case 128: return launch_pipe_d<128, true>(ctx, a, max_n, scratch, tp);
+      case 64: return launch_pipe_d<64, true>(ctx, a, max_n, scratch, tp);
+      case 32: return launch_pipe_d<32, true>(ctx, a, max_n, scratch, tp);
+      default: return false;
+    }
+  }
   switch (a.d) {
-    case 128: return launch_pipe_d<128>(ctx, a, max_n, scratch, tp);
-    case 64: return launch_pipe_d<64>(ctx, a, max_n, scratch, tp);
-    case 32: return launch_pipe_d<32>(ctx, a, max_n, scratch, tp);
-    case 16: return launch_pipe_d<16>(ctx, a, max_n, scratch, tp);
-    case 8: return launch_pipe_d<8>(ctx, a, max_n, scratch, tp);
+    case 128: return launch_pipe_d<128, false>(ctx, a, max_n, scratch, tp);
+    case 64: return launch_pipe_d<64, false>(ctx, a, max_n, scratch, tp);
+    case 32: return launch_pipe_d<32, false>(ctx, a, max_n, scratch, tp);
+    case 16: return launch_pipe_d<16, false>(ctx, a, max_n, scratch, tp);
+    case 8: return launch_pipe_d<8, false>(ctx, a, max_n, scratch, tp);
     default: return false;
   }
 }
