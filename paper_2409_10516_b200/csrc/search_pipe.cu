@@ -942,7 +942,11 @@ bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* sc
   uint32_t spill_cap = 32;
   while (spill_cap < max_n) spill_cap <<= 1;
   SearchArgs s = a;
-  if (const char* f = std::getenv("RA_PIPE_FLAGS")) s.flags = uint32_t(std::atoi(f));
+  static const uint32_t env_flags = [] {  // profiling switches, read once
+    const char* f = std::getenv("RA_PIPE_FLAGS");
+    return f ? uint32_t(std::atoi(f)) : 0u;
+  }();
+  s.flags = env_flags;
   uint8_t* cur = scratch;
   s.spill = cur;
   cur += (size_t(a.B) * 2 * PipeLayout::arr_bytes(spill_cap) + 255) & ~size_t(255);
