@@ -14,6 +14,7 @@
  *   ra_graph_* accessors    <- entry_point/degree/neighbors/...    include/attnindex/index_oodgraph.hpp:49-59
  *   ra_graph_search_batch   <- SearchIndex::search (OODGraph)      include/attnindex/index.hpp:41-42
  *   ra_flat_search_batch    <- FlatIndex::search                   include/attnindex/index_flat.hpp:14-15
+ *   ra_ivf_build / _search_batch <- IVFIndex / IVFIndex::search     include/attnindex/index_ivf.hpp:17-37
  *   ra_partial_attention    <- partial_attention                   include/attnindex/attention.hpp:47-50
  *   ra_merge                <- merge_gammas + merge                include/attnindex/attention.hpp:52-60
  *   ra_static_partition     <- static_partition                    include/attnindex/attention.hpp:44-45
@@ -164,6 +165,27 @@ ra_status ra_graph_search_host(ra_ctx* ctx, const ra_graph* g, const float* q, u
 ra_status ra_flat_search_batch(ra_ctx* ctx, ra_kv* keys, uint32_t B, const float* q,
                                uint32_t k, const uint32_t* mask, uint64_t mask_n,
                                uint32_t* ids, float* scores, uint64_t* scanned);
+
+/* ---- IVF index (index_ivf.cpp; contrast baseline) --------
+ * IVFIndex ctor / ivf_build (index_ivf.cpp:56-151): nlist 0 = ceil(sqrt(n));
+ * errors "empty keys", "nlist out of range". Arithmetic in the reference's
+ * Eigen expression order (fma chains from 0.0, sums in id order). */
+typedef struct ra_ivf ra_ivf;
+ra_status ra_ivf_build(ra_ctx* ctx, ra_kv* keys, uint32_t nlist, uint64_t seed, uint32_t iters,
+                       uint32_t default_nprobe, ra_ivf** out);
+void ra_ivf_free(ra_ivf* ivf);
+uint32_t ra_ivf_nlist(const ra_ivf* ivf);
+uint32_t ra_ivf_default_nprobe(const ra_ivf* ivf);
+/* host copies: centroids nlist x d f32, offsets nlist + 1, ids n (ascending per list) */
+ra_status ra_ivf_export(const ra_ivf* ivf, float* centroids, uint32_t* offsets, uint32_t* ids);
+uint64_t ra_ivf_memory_bytes(const ra_ivf* ivf);
+/* IVFIndex::search (index_ivf.cpp:153-181), B queries, device pointers;
+ * nprobe < 0 = the index default. Errors "query dimension mismatch",
+ * "nprobe out of range", "k out of range". */
+ra_status ra_ivf_search_batch(ra_ctx* ctx, const ra_ivf* ivf, uint32_t B, const float* q,
+                              uint32_t q_dim, uint32_t k, int64_t nprobe, const uint32_t* mask,
+                              uint64_t mask_n, uint32_t* ids, float* scores, uint32_t* n_out,
+                              uint64_t* scanned, uint8_t* truncated);
 
 /* ---- attention (attention.cpp:87-157) ------------------------------------- */
 /* static_partition into host arrays (either may be NULL to just count). */

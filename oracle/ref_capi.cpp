@@ -21,6 +21,7 @@
 #include "attnindex/index_flat.hpp"
 #include "attnindex/index_oodgraph.hpp"
 #include "attnindex/util.hpp"
+#include "attnindex/index_ivf.hpp"
 #include "attnindex/io.hpp"
 #include "attnindex/workload.hpp"
 
@@ -347,6 +348,52 @@ int ref_engine_run(void* e, const float* dq, uint64_t n_steps, int compute_refer
     if (mse_out)
       for (size_t i = 0; i < r.trace.entries.size(); ++i)
         mse_out[i] = r.trace.entries[i].mse ? *r.trace.entries[i].mse : -1.0;
+  });
+}
+
+// IVFIndex (index_ivf.cpp): build, export (centroids, offsets, ids), search
+int ref_ivf_build(const float* keys, uint64_t n, uint32_t d, uint32_t nlist, uint64_t seed,
+                  uint32_t iters, uint32_t default_nprobe, void** out) {
+  return guard([&] {
+    IVFBuildParams p;
+    p.nlist = nlist;
+    p.seed = seed;
+    p.iters = iters;
+    p.default_nprobe = default_nprobe;
+    auto ks = make_set(Role::Key, keys, n, d);
+    *out = ivf_build(ks, p).release();
+  });
+}
+void ref_ivf_free(void* h) { delete static_cast<IVFIndex*>(h); }
+uint32_t ref_ivf_nlist(void* h) { return static_cast<IVFIndex*>(h)->nlist(); }
+int ref_ivf_export(void* h, float* cent, uint32_t* offsets, uint32_t* ids) {
+  return guard([&] {
+    auto* ix = static_cast<IVFIndex*>(h);
+    const uint32_t d = ix->keys()->d;
+    uint32_t o = 0;
+    for (uint32_t c = 0; c < ix->nlist(); ++c) {
+      auto cr = ix->centroid(c);
+      std::copy(cr.begin(), cr.end(), cent + size_t(c) * d);
+      offsets[c] = o;
+      for (uint32_t id : ix->list(c)) ids[o++] = id;
+    }
+    offsets[ix->nlist()] = o;
+  });
+}
+int ref_ivf_search(void* h, const float* q, uint32_t d, uint64_t k, const uint32_t* mask,
+                   uint64_t mask_n, int64_t nprobe, uint32_t* ids, float* scores,
+                   uint64_t* n_out, uint64_t* scanned, uint8_t* truncated) {
+  return guard([&] {
+    auto* ix = static_cast<IVFIndex*>(h);
+    std::optional<uint32_t> np;
+    if (nprobe >= 0) np = uint32_t(nprobe);
+    auto r = ix->search(std::span<const float>(q, d), k,
+                        Mask{std::span<const uint32_t>(mask, mask_n)}, np);
+    std::copy(r.ids.begin(), r.ids.end(), ids);
+    std::copy(r.scores.begin(), r.scores.end(), scores);
+    *n_out = r.ids.size();
+    *scanned = r.scanned;
+    *truncated = r.truncated;
   });
 }
 

@@ -8,6 +8,7 @@ loads (building if necessary) that library; there is no CPU fallback.
 from ._capi import EXPORTED, lib  # noqa: F401  (loads libra_b200.so, loudly)
 from .api import (  # noqa: F401
     BatchResult, BuildStats, Context, CudaError, Engine, EngineConfig, FlatIndex, GraphError,
+    IVFBuildParams, IVFIndex, ivf_build,
     InvalidArgument, KVGroup, KVPartition, OODGraph, OODGraphBuildParams, PartialAttention,
     SearchResult, default_context, empty_partial, merge, merge_gammas, ood_build,
     partial_attention, search_batch, static_partition, flat_build, engine_init)

@@ -90,6 +90,15 @@ _SIGS = {
                                        c_vp, c_vp, c_vp]),
     "ra_merge": (C.c_int, [c_vp, C.c_uint32, C.c_uint32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                            c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "ra_ivf_build": (C.c_int, [c_vp, c_vp, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32,
+                               C.POINTER(c_vp)]),
+    "ra_ivf_free": (None, [c_vp]),
+    "ra_ivf_nlist": (C.c_uint32, [c_vp]),
+    "ra_ivf_default_nprobe": (C.c_uint32, [c_vp]),
+    "ra_ivf_export": (C.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "ra_ivf_memory_bytes": (C.c_uint64, [c_vp]),
+    "ra_ivf_search_batch": (C.c_int, [c_vp, c_vp, C.c_uint32, c_vp, C.c_uint32, C.c_uint32,
+                                      C.c_int64, c_vp, C.c_uint64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "ra_engine_create": (C.c_int, [c_vp, C.POINTER(c_vp), C.c_uint32, C.POINTER(c_vp),
                                    C.c_uint32, C.POINTER(EngineConfigC), C.POINTER(c_vp)]),
     "ra_engine_destroy": (None, [c_vp]),

@@ -452,6 +452,93 @@ class FlatIndex:
         return self.search_batch(np.asarray(q, np.float32).reshape(1, -1), k, mask)[0]
 
 
+@dataclass
+class IVFBuildParams:
+    """index_ivf.hpp:7-12 (defaults identical)."""
+
+    nlist: int = 0          # 0 = ceil(sqrt(n))
+    seed: int = 0
+    iters: int = 20
+    default_nprobe: int = 8
+
+
+class IVFIndex:
+    """k-means IVF baseline on the device (index_ivf.hpp:17-37)."""
+
+    def __init__(self, keys: KVGroup, params: IVFBuildParams = IVFBuildParams()):
+        self.keys = keys
+        h = C.c_void_p()
+        _check(lib.ra_ivf_build(keys.ctx.h, keys.h, params.nlist, params.seed, params.iters,
+                                params.default_nprobe, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib.ra_ivf_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def kind(self) -> str:
+        return "ivf"
+
+    def size(self) -> int:
+        return self.keys.n
+
+    def nlist(self) -> int:
+        return int(lib.ra_ivf_nlist(self.h))
+
+    def memory_bytes(self) -> int:
+        return int(lib.ra_ivf_memory_bytes(self.h))
+
+    def export(self):
+        """(centroids [nlist, d] f32, offsets [nlist+1], ids [n]) host copies."""
+        nl, d = self.nlist(), self.keys.d
+        cent = np.empty((nl, d), np.float32)
+        off = np.empty(nl + 1, np.uint32)
+        ids = np.empty(self.keys.n, np.uint32)
+        _check(lib.ra_ivf_export(self.h, cent.ctypes.data, off.ctypes.data, ids.ctypes.data))
+        return cent, off, ids
+
+    def list(self, c: int) -> np.ndarray:
+        _, off, ids = self.export()
+        return ids[off[c]:off[c + 1]].copy()
+
+    def search_batch(self, queries, k: int, mask=None, nprobe: Optional[int] = None) -> list:
+        ctx = self.keys.ctx.bind_stream()
+        dev = torch.device("cuda", ctx.device)
+        q = _dev(queries, torch.float32, dev)
+        if q.dim() == 1:
+            q = q.view(1, -1)
+        B = int(q.shape[0])
+        m = None
+        if mask is not None and len(mask) > 0:
+            m = _dev(np.asarray(mask, np.uint32).view(np.int32), torch.int32, dev)
+        kk = max(int(k), 1)
+        ids = torch.empty((B, kk), dtype=torch.int32, device=dev)
+        sc = torch.empty((B, kk), dtype=torch.float32, device=dev)
+        n_out = torch.empty(B, dtype=torch.int32, device=dev)
+        scanned = torch.empty(B, dtype=torch.int64, device=dev)
+        tr = torch.empty(B, dtype=torch.uint8, device=dev)
+        _check(lib.ra_ivf_search_batch(ctx.h, self.h, B, _ptr(q), int(q.shape[1]), int(k),
+                                       -1 if nprobe is None else int(nprobe), _ptr(m),
+                                       0 if m is None else int(m.numel()), _ptr(ids), _ptr(sc),
+                                       _ptr(n_out), _ptr(scanned), _ptr(tr)))
+        ih, sh = ids.cpu().numpy().view(np.uint32), sc.cpu().numpy()
+        nh, snh, th = n_out.cpu().numpy(), scanned.cpu().numpy(), tr.cpu().numpy()
+        return [SearchResult(ih[b, : nh[b]].copy(), sh[b, : nh[b]].copy(), int(snh[b]), bool(th[b]))
+                for b in range(B)]
+
+    def search(self, q, k: int, mask=None, nprobe: Optional[int] = None) -> SearchResult:
+        return self.search_batch(np.asarray(q, np.float32).reshape(1, -1), k, mask, nprobe)[0]
+
+
+def ivf_build(keys: KVGroup, params: IVFBuildParams = IVFBuildParams()) -> IVFIndex:
+    """ivf_build (index_ivf.hpp:39-40)."""
+    return IVFIndex(keys, params)
+
+
 def flat_build(keys: KVGroup) -> FlatIndex:
     """flat_build (index_flat.hpp:24)."""
     return FlatIndex(keys)
