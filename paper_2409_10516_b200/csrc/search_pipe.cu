@@ -71,7 +71,10 @@ constexpr uint32_t kSlots = 64;    // packet table, direct-mapped by node id
 constexpr uint32_t kSlotBits = 6;
 constexpr uint32_t kPick = 12;     // helpers consider the best kPick heads
 constexpr uint32_t kChain = 3;     // greedy chain depth after a pre-expansion
-constexpr uint32_t kSlackU = 64;   // U grows to ef + slack before thr is raised
+#ifndef RA_PIPE_SLACK
+#define RA_PIPE_SLACK 64
+#endif
+constexpr uint32_t kSlackU = RA_PIPE_SLACK;  // U grows to ef + slack before thr is raised
 constexpr uint32_t sFREE = 0, sBUSY = 1, sREADY = 2, sTAKEN = 3;
 
 // order-preserving key of a double; -0.0 and +0.0 share a key
