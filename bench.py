@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-bf16", action="store_true", help="skip the bf16-KV measurement")
+    ap.add_argument("--no-multilayer", action="store_true",
+                    help="skip the 4-distinct-layer batched measurement")
     ap.add_argument("--flush-mb", type=int, default=512)
     ap.add_argument("--shard", default="layers", choices=["layers", "heads"],
                     help="N>1: layers = weak scaling, rank r decodes its own synthetic layer "
@@ -264,6 +266,8 @@ def main():
         e2e.append(e0.elapsed_time(e1))
 
     tput = batched_throughput(a, ra, kvs, graphs, Q, cfg, flush, stream)
+    tput_ml = (multilayer_throughput(a, ra, spec, my_groups, hpg, kvs, graphs, Q, cfg, flush,
+                                     stream, layer) if not a.no_multilayer else None)
     out32 = eng.decode_step_device(Q[a.warmup])[0].cpu().numpy()
     bf16 = (bf16_mode(a, ra, spec, my_groups, hpg, Q, cfg, flush, stream, out32, graphs)
             if not a.no_bf16 else None)
@@ -316,6 +320,7 @@ def main():
                    "scan_fraction": statistics.mean(scanned) / Hl / (a.n_ctx - 640)},
         "clocks": clk.summary(),
         "throughput": tput,
+        "throughput_multilayer": tput_ml,
         "bf16_kv": bf16,
         "setup_s": round(setup_s, 1),
         "build_ms_per_head": round(statistics.mean(build_ms), 1),
@@ -378,6 +383,64 @@ def batched_throughput(a, ra, kvs, graphs, Q, cfg, flush, stream, row_bytes=512)
             "search_GBps": round(gbs, 1), "search_frac": round(gbs / peak, 4),
             "peak_source": kind,
             "note": "one engine step over R x H heads; KV of each head shared by its R queries"}
+
+
+def multilayer_throughput(a, ra, spec, my_groups, hpg, kvs0, graphs0, Q0, cfg, flush, stream,
+                          layer0, n_layers=4, R=32):
+    """Layer-batched decode with DISTINCT layers: this layer plus 3 more
+    synthetic layers (seeds 7 + l, their own K/V and graphs), 32 decode
+    queries per head per layer, all 4096 searches + attention in one engine
+    step (configs[2]'s per-GPU shape with 4 layers x batch 32)."""
+    import dataclasses
+    import torch
+    from paper_2409_10516_b200.workload import generate_group
+    bp = ra.OODGraphBuildParams(a.k_train, a.max_degree, a.ef_construction, 8)
+    layers = [(list(kvs0), list(graphs0), Q0[:R])]
+    for l in range(1, n_layers):
+        sp = dataclasses.replace(spec, seed=7 + layer0 * n_layers + l, n_decode=R)
+        kvs, graphs, dq = [], [], []
+        for g in my_groups:
+            w = generate_group(sp, g, Q0.device)
+            kv = ra.KVGroup(w["keys"], w["values"])
+            kvs.append(kv)
+            for m in range(hpg):
+                graphs.append(ra.ood_build(kv, w["prefill_q"][m], bp))
+                dq.append(w["decode_q"][m])
+            del w
+        layers.append((kvs, graphs, torch.stack(dq, dim=1)))
+    G_all = [kv for kvs, _, _ in layers for _ in range(R) for kv in kvs]
+    H_all = [g for _, gr, _ in layers for _ in range(R) for g in gr]
+    eng = ra.Engine(G_all, H_all, cfg)
+    q = torch.cat([dq[:R].reshape(R * dq.shape[1], -1) for _, _, dq in layers]).contiguous()
+    for _ in range(3):
+        eng.decode_step_device(q)
+    torch.cuda.synchronize()
+    times, s_ms, sc, ex = [], [], [], []
+    for _ in range(max(3, min(a.steps, 10))):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.decode_step_device(q)
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+        s_ms.append(eng.last_timing()[0])
+        s, e = eng.last_stats()
+        sc.append(s)
+        ex.append(e)
+    ms, ms_s = statistics.mean(times), statistics.mean(s_ms)
+    nq = len(H_all)
+    by = statistics.mean([s * 512 + e * a.max_degree * 4 for s, e in zip(sc, ex)])
+    peak, kind = measured_peaks()
+    gbs = by / (ms_s * 1e-3) / 1e9
+    del eng
+    return {"layers": n_layers, "decode_queries_per_head_per_layer": R, "queries_per_step": nq,
+            "ms_per_step": round(ms, 4), "us_per_query": round(ms * 1e3 / nq, 3),
+            "queries_per_s": round(nq / (ms * 1e-3), 1), "search_ms": round(ms_s, 4),
+            "search_GBps": round(gbs, 1), "search_frac": round(gbs / peak, 4),
+            "peak_source": kind,
+            "note": "distinct synthetic layers (own K/V and graphs); one engine step"}
 
 
 def bf16_mode(a, ra, spec, my_groups, hpg, Q, cfg, flush, stream, out32, graphs32):
