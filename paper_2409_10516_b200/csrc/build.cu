@@ -573,23 +573,32 @@ __global__ void k_flat_pick(const uint32_t* __restrict__ ids, const double* __re
 
 }  // namespace
 
-// host-orchestrated phase 4 on the host mirror; nearest-anchor on the GPU
+// host-orchestrated phase 4 on the fixed-stride host mirror (row u =
+// adj[u*M .. u*M+deg[u]); appends stay within M by construction);
+// nearest-anchor on the GPU
 static void repair(ra_ctx* ctx, ra_kv* kv, const double* norms_dev, uint64_t entry,
-                   uint32_t M, std::vector<std::vector<uint32_t>>& adj, ra_build_stats* st) {
+                   uint32_t M, std::vector<uint32_t>& adj, std::vector<uint32_t>& deg,
+                   ra_build_stats* st) {
   const uint32_t n = uint32_t(kv->n), d = kv->d;
   std::vector<uint8_t> reached(n);
+  std::vector<uint32_t> stack;
+  stack.reserve(n);
   auto sweep = [&] {
     std::fill(reached.begin(), reached.end(), 0);
-    std::vector<uint32_t> stack{uint32_t(entry)};
+    stack.clear();
+    stack.push_back(uint32_t(entry));
     reached[entry] = 1;
     while (!stack.empty()) {
       const uint32_t u = stack.back();
       stack.pop_back();
-      for (uint32_t v : adj[u])
+      const uint32_t* row = adj.data() + size_t(u) * M;
+      for (uint32_t e = 0; e < deg[u]; ++e) {
+        const uint32_t v = row[e];
         if (!reached[v]) {
           reached[v] = 1;
           stack.push_back(v);
         }
+      }
     }
   };
   sweep();
@@ -603,7 +612,7 @@ static void repair(ra_ctx* ctx, ra_kv* kv, const double* norms_dev, uint64_t ent
     st->repaired_nodes += pending.size();
     std::vector<uint32_t> anchors;
     for (uint32_t v = 0; v < n; ++v)
-      if (reached[v] && adj[v].size() < M) anchors.push_back(v);
+      if (reached[v] && deg[v] < M) anchors.push_back(v);
     if (anchors.empty()) {
       std::vector<uint32_t> depth(n, UINT32_MAX), queue{uint32_t(entry)};
       depth[entry] = 0;
@@ -611,13 +620,15 @@ static void repair(ra_ctx* ctx, ra_kv* kv, const double* norms_dev, uint64_t ent
       for (size_t h = 0; h < queue.size(); ++h) {
         const uint32_t u = queue[h];
         if (depth[u] > depth[deepest] || (depth[u] == depth[deepest] && u < deepest)) deepest = u;
-        for (uint32_t v : adj[u])
+        for (uint32_t e = 0; e < deg[u]; ++e) {
+          const uint32_t v = adj[size_t(u) * M + e];
           if (depth[v] == UINT32_MAX) {
             depth[v] = depth[u] + 1;
             queue.push_back(v);
           }
+        }
       }
-      adj[deepest].pop_back();
+      --deg[deepest];  // drop its last edge
       anchors.push_back(deepest);
     }
     d_pend.ensure(pending.size());
@@ -648,7 +659,7 @@ static void repair(ra_ctx* ctx, ra_kv* kv, const double* norms_dev, uint64_t ent
       bool deferred = false;
       for (size_t i = g0; i < g1; ++i) {
         const uint32_t u = by_anchor[i].second;
-        while (adj[t].size() >= M) {
+        while (deg[t] >= M) {
           if (next_t >= attached.size()) {
             deferred = true;
             break;
@@ -656,9 +667,9 @@ static void repair(ra_ctx* ctx, ra_kv* kv, const double* norms_dev, uint64_t ent
           t = attached[next_t++];
         }
         if (deferred) break;
-        adj[t].push_back(u);
+        adj[size_t(t) * M + deg[t]++] = u;
         attached.push_back(u);
-        if (adj[u].size() < M) t = u;
+        if (deg[u] < M) t = u;
       }
       g0 = g1;
     }
@@ -855,16 +866,15 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
     st.ms_entry = tm.lap();
 
     // ---- phase 4 + CSR ----
-    std::vector<std::vector<uint32_t>> adj(n);
-    for (uint32_t u = 0; u < n; ++u)
-      adj[u].assign(h_adj.begin() + size_t(u) * M, h_adj.begin() + size_t(u) * M + h_deg[u]);
-    repair(ctx, kv, norms.p, g->entry, M, adj, &st);
+    const uint32_t rounds0 = st.repair_rounds;
+    repair(ctx, kv, norms.p, g->entry, M, h_adj, h_deg, &st);
     g->offsets.assign(size_t(n) + 1, 0);
-    for (uint32_t u = 0; u < n; ++u) g->offsets[u + 1] = g->offsets[u] + adj[u].size();
+    for (uint32_t u = 0; u < n; ++u) g->offsets[u + 1] = g->offsets[u] + h_deg[u];
     g->adjacency.resize(g->offsets[n]);
     for (uint32_t u = 0; u < n; ++u)
-      std::copy(adj[u].begin(), adj[u].end(), g->adjacency.begin() + g->offsets[u]);
-    graph_upload(ctx, g.get());
+      std::copy(h_adj.begin() + size_t(u) * M, h_adj.begin() + size_t(u) * M + h_deg[u],
+                g->adjacency.begin() + g->offsets[u]);
+    if (st.repair_rounds != rounds0) graph_upload(ctx, g.get());  // else the device rows stand
     st.ms_repair = tm.lap();
 
     ra_kv_retain(kv);
