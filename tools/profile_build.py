@@ -20,6 +20,7 @@ def main():
     t = time.time()
     g = ra.ood_build(kv, w["prefill_q"][0], ra.OODGraphBuildParams(128, 24, 256, 8))
     print(f"n={a.n} build {1e3 * (time.time() - t):.1f} ms phases {g.build_stats.ms} "
+          f"repair rounds {g.build_stats.repair_rounds} nodes {g.build_stats.repaired_nodes} "
           f"fallback_rows {g.build_stats.knn_rows_widened}")
 
 
