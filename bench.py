@@ -36,6 +36,16 @@ METRIC = "decode attention ms/token @128K (Llama-3-8B shape); search recall@100;
 TPUT_R = 128  # batched line: 128 decode queries per head x 32 heads = 4096 searches
 
 
+def workload_config(a, H, G):
+    """The workload both arms run (BASELINE.json configs[1])."""
+    return {"workload": "configs[1]: Llama-3-8B shape single layer, 32 Q heads / 8 KV "
+                        "groups, d=128, 128K ctx, top-100 + 640 static, ef 128",
+            "n_ctx": a.n_ctx, "heads": H, "kv_groups": G, "top_k": a.top_k, "ef": a.ef,
+            "graph": {"k_train": a.k_train, "max_degree": a.max_degree,
+                      "ef_construction": a.ef_construction, "edge_window": 8},
+            "l2": f"flushed between timed steps ({a.flush_mb} MiB write)"}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -293,17 +303,12 @@ def main():
         "higher_is_better": False, "scaling": "strong" if by_heads else "weak",
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference OOD generator algorithm, seed 7, GPU-synthesized)",
-        "config": {"workload": "configs[1]: Llama-3-8B shape single layer, 32 Q heads / 8 KV "
-                               "groups, d=128, 128K ctx, top-100 + 640 static, ef 128",
-                   "n_ctx": a.n_ctx, "heads": H, "kv_groups": G, "top_k": a.top_k, "ef": a.ef,
-                   "graph": {"k_train": a.k_train, "max_degree": M,
-                             "ef_construction": a.ef_construction, "edge_window": 8},
-                   "l2": f"flushed between timed steps ({a.flush_mb} MiB write)",
-                   "parallelism": (f"heads sharded by KV group over {world} GPU(s) + NCCL "
-                                   "all_gather of outputs" if by_heads else
-                                   f"layer-sharded: {world} GPU(s), rank r decodes synthetic "
-                                   "layer r (all 32 heads), no data-path collective; value = "
-                                   "step time / layers")},
+        "config": dict(workload_config(a, H, G),
+                       parallelism=(f"heads sharded by KV group over {world} GPU(s) + NCCL "
+                                    "all_gather of outputs" if by_heads else
+                                    f"layer-sharded: {world} GPU(s), rank r decodes synthetic "
+                                    "layer r (all 32 heads), no data-path collective; value = "
+                                    "step time / layers")),
         "e2e": {"value": round(ms_e2e, 4), "unit": "ms/token",
                 "h2d_bytes_per_step": Hl * 128 * 4,
                 "d2h_bytes_per_step": Hl * 128 * 8 + Hl * max(eng.k, 1) * 4 + Hl * 8},
@@ -599,8 +604,8 @@ def run_reference(a, keys_host, vals_host, graphs, Q, cfg, H, G, setup_s):
         "n_gpus": 1, "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 3),
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference OOD generator algorithm, seed 7)",
-        "config": {"workload": "configs[1]", "n_ctx": a.n_ctx, "heads": H, "kv_groups": G,
-                   "top_k": a.top_k, "ef": a.ef},
+        "config": dict(workload_config(a, H, G),
+                       parallelism="reference decode_step on the host cores (rank 0)"),
         "cpu_baseline": {"value": round(ms, 3), "unit": "ms/token", "cores": threads,
                          "kind": "reference", "sample": sample},
         "e2e": {"value": round(ms, 3), "unit": "ms/token", "h2d_bytes_per_step": 0,
