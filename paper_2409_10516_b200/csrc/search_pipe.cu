@@ -636,14 +636,27 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         nFO = __shfl_sync(kFull, nFO, 0);
         __syncwarp();
         fo_rescan();
-      } else if (hi == tid) {  // owner lane: last entry fills the hole
-        --fcnt;
-        if (hpos != fcnt) {
-          Fl_k[hpos * 32 + lane] = Fl_k[fcnt * 32 + lane];
-          Fl_i[hpos * 32 + lane] = Fl_i[fcnt * 32 + lane];
+      } else {
+        // owner lane: its last entry fills the hole; then the owner's new
+        // head is found by kFR lanes at once (one entry each, 3 REDUX)
+        const uint32_t owner = __ffs(__ballot_sync(kFull, hi == tid)) - 1;
+        if (lane == owner) {
+          --fcnt;
+          if (hpos != fcnt) {
+            Fl_k[hpos * 32 + lane] = Fl_k[fcnt * 32 + lane];
+            Fl_i[hpos * 32 + lane] = Fl_i[fcnt * 32 + lane];
+          }
+          Fl_k[fcnt * 32 + lane] = 0, Fl_i[fcnt * 32 + lane] = kSentinel;
         }
-        Fl_k[fcnt * 32 + lane] = 0, Fl_i[fcnt * 32 + lane] = kSentinel;
-        lane_head();
+        __syncwarp();
+        const uint32_t fc = __shfl_sync(kFull, fcnt, owner);
+        uint64_t x = 0;
+        uint32_t v = kSentinel;
+        if (lane < fc) x = Fl_k[lane * 32 + owner], v = Fl_i[lane * 32 + owner];
+        const uint32_t mine = v;
+        warp_best(x, v);
+        const uint32_t pos = __ffs(__ballot_sync(kFull, lane < fc && mine == v)) - 1;
+        if (lane == owner) hk = x, hi = v, hpos = fc ? pos : 0;
       }
       ++expanded;
       PIPE_TICK(1)
