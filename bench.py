@@ -289,6 +289,16 @@ def main():
         t = torch.tensor([ms, ms_e2e, ms_search], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, ms_e2e, ms_search = (float(x) for x in t)
+        # shard balance: per-rank mean scanned per head, max vs mean
+        sc_local = torch.tensor([statistics.mean(scanned) / max(Hl, 1)], dtype=torch.float64,
+                                device=dev)
+        all_sc = [torch.zeros_like(sc_local) for _ in range(world)]
+        dist.all_gather(all_sc, sc_local)
+        per_rank = [float(x) for x in all_sc]
+        shard_balance = {"mean_scanned_per_head_by_rank": [round(x, 1) for x in per_rank],
+                         "max_over_mean": round(max(per_rank) / statistics.mean(per_rank), 4)}
+    else:
+        shard_balance = None
     # whole-job aggregate: layer-sharded ranks each decode one layer per step,
     # so N layer-tokens complete in the (max-over-ranks) step time
     units = world if (dist is not None and not by_heads) else 1
@@ -326,6 +336,7 @@ def main():
         "clocks": clk.summary(),
         "throughput": tput,
         "throughput_multilayer": tput_ml,
+        "shard_balance": shard_balance,
         "bf16_kv": bf16,
         "setup_s": round(setup_s, 1),
         "build_ms_per_head": round(statistics.mean(build_ms), 1),
