@@ -172,7 +172,8 @@ struct PipeLayout {
                           kCnt = 1024, kMb = 1280, kNk = 1536, kPkId = 2048,
                           kPkK = kPkId + size_t(kSlots) * 32 * 4,
                           kPubF = kPkK + size_t(kSlots) * 32 * 8,  // F: k u64[kFR][32], id u32[kFR][32]
-                          kQd = kPubF + size_t(kFR) * 32 * 12;
+                          kHint = kPubF + size_t(kFR) * 32 * 12,   // hints: k u64[32], id u32[32]
+                          kQd = kHint + 32 * 12;
   __host__ __device__ size_t row_floats() const { return D + 4; }
   __host__ __device__ size_t tiles_off() const { return kQd + size_t(D) * 8; }
   __host__ __device__ size_t tile_bytes() const { return size_t(MT) * row_floats() * 4; }
@@ -228,6 +229,10 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
   volatile uint32_t* pub_id = reinterpret_cast<volatile uint32_t*>(smem + PipeLayout::kPubId);
   volatile uint64_t* pubf_k = reinterpret_cast<volatile uint64_t*>(smem + PipeLayout::kPubF);
   volatile uint32_t* pubf_id = reinterpret_cast<volatile uint32_t*>(pubf_k + kFR * 32);
+  // hint ring: the runner-up children of recent pre-expansions (likely tops
+  // right after their parent commits), written by helpers, read by helpers
+  volatile uint64_t* hint_k = reinterpret_cast<volatile uint64_t*>(smem + PipeLayout::kHint);
+  volatile uint32_t* hint_id = reinterpret_cast<volatile uint32_t*>(hint_k + 32);
   unsigned long long* slotw = reinterpret_cast<unsigned long long*>(smem + PipeLayout::kSlotW);
   uint32_t* pk_cnt = reinterpret_cast<uint32_t*>(smem + PipeLayout::kCnt);
   uint32_t* pk_mb = reinterpret_cast<uint32_t*>(smem + PipeLayout::kMb);
@@ -255,6 +260,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
       slotw[i] = slotword(kSentinel, sFREE);
     if (threadIdx.x < 32) pub_k[threadIdx.x] = 0, pub_id[threadIdx.x] = kSentinel;
     for (uint32_t i = threadIdx.x; i < kFR * 32; i += blockDim.x) pubf_k[i] = 0, pubf_id[i] = kSentinel;
+    if (threadIdx.x < 32) hint_k[threadIdx.x] = 0, hint_id[threadIdx.x] = kSentinel;
     if (threadIdx.x < 16) ctrl[threadIdx.x] = 0;
     __syncthreads();
   }
@@ -840,23 +846,39 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
           }
         }
       }
+      auto claimable = [&](uint32_t id) -> bool {
+        if (id >= n || vbit(expd, id)) return false;
+        const uint64_t w = *reinterpret_cast<volatile unsigned long long*>(slotw + slot_of(id));
+        return uint32_t(w) != id;  // not in flight / ready already
+      };
+      // best claimable hint (one per lane)
+      uint64_t hx = hint_k[lane];
+      uint32_t hid = hint_id[lane];
+      if (!(a.flags & 8u) && hid != kSentinel && claimable(hid)) {
+      } else {
+        hx = 0, hid = kSentinel;
+      }
+      warp_best(hx, hid);
       uint32_t got = kSentinel, sl = 0;
       uint64_t gk = 0;
       for (uint32_t r = 0; r < pick; ++r) {
         uint64_t x = ck[0];
         uint32_t id = ci[0];
         warp_best(x, id);
+        if (hid != kSentinel && !better(x, id, hx, hid)) {  // the hint ranks first
+          if (try_claim(hid, hx, sl)) {
+            got = hid, gk = hx;
+            break;
+          }
+          hid = kSentinel, hx = 0;
+        }
         if (id == kSentinel) break;
         if (ci[0] == id) {  // winner lane advances
 #pragma unroll
           for (int i = 0; i < kFR - 1; ++i) ck[i] = ck[i + 1], ci[i] = ci[i + 1];
           ck[kFR - 1] = 0, ci[kFR - 1] = kSentinel;
         }
-        if (vbit(expd, id)) continue;
-        {
-          const uint64_t w = *reinterpret_cast<volatile unsigned long long*>(slotw + slot_of(id));
-          if (uint32_t(w) == id) continue;  // in flight or ready
-        }
+        if (!claimable(id)) continue;
         if (try_claim(id, x, sl)) {
           got = id, gk = x;
           break;
@@ -894,6 +916,17 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         uint64_t ck2 = isnew ? x : 0;
         uint32_t cid = isnew ? v : kSentinel;
         warp_best(ck2, cid);
+        {  // the runner-up beating the parent becomes a hint for idle helpers
+          uint64_t k2 = (isnew && v != cid) ? x : 0;
+          uint32_t i2 = (isnew && v != cid) ? v : kSentinel;
+          warp_best(k2, i2);
+          if (lane == 0 && i2 != kSentinel && k2 > gk && !(a.flags & 8u)) {
+            const uint32_t h = atomicAdd(const_cast<uint32_t*>(ctrl) + 12, 1u) & 31u;
+            hint_id[h] = kSentinel;
+            hint_k[h] = k2;
+            hint_id[h] = i2;
+          }
+        }
         if (depth + 1 >= chain_max || cid == kSentinel || !(ck2 > gk) || ctrl[0]) break;
         if (vbit(expd, cid)) break;
         {
