@@ -67,7 +67,7 @@ constexpr uint32_t kTW = RA_TP_WARPS;  // TP mode: queries (warps) per CTA
 #endif
 constexpr int kFR = 8;             // frontier entries per lane (sorted)
 constexpr int kUR = 8;             // pool-candidate entries per lane
-constexpr uint32_t kSlots = 64;    // packet table, direct-mapped by node id
+constexpr uint32_t kSlots = 64;    // packet table, 2-way set-associative by node id
 constexpr uint32_t kSlotBits = 6;
 constexpr uint32_t kPick = 12;     // helpers consider the best kPick heads
 constexpr uint32_t kChain = 3;     // greedy chain depth after a pre-expansion
@@ -92,8 +92,9 @@ __device__ __forceinline__ bool better(uint64_t ka, uint32_t ia, uint64_t kb, ui
 __device__ __forceinline__ uint64_t slotword(uint32_t key, uint32_t st) {
   return (uint64_t(st) << 32) | key;
 }
+// first slot of id's set (a node's packet lives in slot_of(id) or slot_of(id) + 1)
 __device__ __forceinline__ uint32_t slot_of(uint32_t id) {
-  return (id * 2654435761u) >> (32 - kSlotBits);
+  return ((id * 2654435761u) >> (33 - kSlotBits)) << 1;
 }
 __device__ __forceinline__ uint32_t lanemask_lt(uint32_t lane) { return (1u << lane) - 1u; }
 
@@ -673,8 +674,12 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         continue;
       }
       // the top's packet: hit (ready or in flight) or expand inline
-      const uint32_t sl = slot_of(tid);
+      uint32_t sl = slot_of(tid);
       uint64_t w = *reinterpret_cast<volatile unsigned long long*>(slotw + sl);
+      {
+        const uint64_t w1 = *reinterpret_cast<volatile unsigned long long*>(slotw + sl + 1);
+        if (uint32_t(w) != tid && uint32_t(w1) == tid) w = w1, ++sl;
+      }
       bool hit = false;
       if (uint32_t(w) == tid) {
         if (uint32_t(w >> 32) == sBUSY) {
@@ -711,6 +716,12 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         rot += cnt;
       } else {
         ++c_miss;
+#ifdef RA_PIPE_MISSCLASS
+        // 1: slot held another live packet, 2: empty slot, 3: own id (taken race)
+        if (uint32_t(w) != tid && uint32_t(w >> 32) != sFREE) cy[4] += 1;
+        else if (uint32_t(w) != tid) cy[4] += 1ull << 20;
+        else cy[4] += 1ull << 40;
+#endif
         expand(tid, cv, cx, cand, cm);
         pre = true;
       }
@@ -752,6 +763,9 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
       d[0] = c_miss, d[1] = c_wait, d[2] = clock64() - t_begin, d[3] = expanded;
       d[4] = c_hit, d[5] = TP ? 0 : ctrl[8], d[6] = c_comp;
       d[7] = cy[0], d[8] = cy[1], d[9] = cy[2], d[10] = cy[3], d[11] = cyc_comp;
+#ifdef RA_PIPE_MISSCLASS
+      d[9] = cy[4];
+#endif
       (void)c_comp, (void)c_fopop, (void)c_fsp, (void)c_usp;
     }
     const uint32_t pool = uint32_t(u_total < ef ? u_total : ef);
@@ -805,20 +819,34 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     // expanded already or ranks below x
     auto try_claim = [&](uint32_t id, uint64_t x, uint32_t& sl) -> bool {
       bool ok = false;
-      sl = slot_of(id);
+      const uint32_t s0 = slot_of(id);
+      sl = s0;
       if (lane == 0) {
-        const uint64_t w = *reinterpret_cast<volatile unsigned long long*>(slotw + sl);
-        const uint32_t key = uint32_t(w), st = uint32_t(w >> 32);
-        if (key != id) {
-          if (st == sFREE) {
+        const uint64_t w0 = *reinterpret_cast<volatile unsigned long long*>(slotw + s0);
+        const uint64_t w1 = *reinterpret_cast<volatile unsigned long long*>(slotw + s0 + 1);
+        if (uint32_t(w0) != id && uint32_t(w1) != id) {
+          // a free way first, else the way whose ready packet may be evicted
+          // (node expanded already, or ranking below x; the lower rank goes)
+          auto rank = [&](uint64_t w, uint32_t s) -> uint64_t {  // 0: unusable
+            const uint32_t st = uint32_t(w >> 32);
+            if (st == sFREE) return ~0ull;
+            if (st != sREADY) return 0;
+            if (vbit(expd, uint32_t(w))) return ~0ull - 1;
+            const uint64_t nk = pk_nk[s];
+            return nk < x ? ~nk : 0;
+          };
+          const uint64_t r0 = rank(w0, s0), r1 = rank(w1, s0 + 1);
+          if (r0 | r1) {
+            const bool second = r1 > r0;
+            const uint64_t w = second ? w1 : w0;
+            sl = s0 + second;
             ok = atomicCAS(slotw + sl, w, slotword(id, sBUSY)) == w;
-          } else if (st == sREADY && (vbit(expd, key) || pk_nk[sl] < x)) {
-            ok = atomicCAS(slotw + sl, w, slotword(id, sBUSY)) == w;
-            n_evict += ok;
+            n_evict += ok && uint32_t(w >> 32) != sFREE;
           }
         }
         if (ok) pk_nk[sl] = x;
       }
+      sl = __shfl_sync(kFull, sl, 0);
       return __shfl_sync(kFull, ok, 0);
     };
     for (;;) {
@@ -848,8 +876,10 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
       }
       auto claimable = [&](uint32_t id) -> bool {
         if (id >= n || vbit(expd, id)) return false;
-        const uint64_t w = *reinterpret_cast<volatile unsigned long long*>(slotw + slot_of(id));
-        return uint32_t(w) != id;  // not in flight / ready already
+        const uint32_t s0 = slot_of(id);
+        const uint64_t w0 = *reinterpret_cast<volatile unsigned long long*>(slotw + s0);
+        const uint64_t w1 = *reinterpret_cast<volatile unsigned long long*>(slotw + s0 + 1);
+        return uint32_t(w0) != id && uint32_t(w1) != id;  // not in flight / ready already
       };
       // best claimable hint (one per lane)
       uint64_t hx = hint_k[lane];
@@ -930,8 +960,10 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         if (depth + 1 >= chain_max || cid == kSentinel || !(ck2 > gk) || ctrl[0]) break;
         if (vbit(expd, cid)) break;
         {
-          const uint64_t w = *reinterpret_cast<volatile unsigned long long*>(slotw + slot_of(cid));
-          if (uint32_t(w) == cid) break;
+          const uint32_t s0 = slot_of(cid);
+          const uint64_t w0 = *reinterpret_cast<volatile unsigned long long*>(slotw + s0);
+          const uint64_t w1 = *reinterpret_cast<volatile unsigned long long*>(slotw + s0 + 1);
+          if (uint32_t(w0) == cid || uint32_t(w1) == cid) break;
         }
         if (!try_claim(cid, ck2, sl)) break;
         got = cid, gk = ck2;
