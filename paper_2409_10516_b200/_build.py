@@ -41,7 +41,7 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, jobs: int = 8) -> str:
-    if not force and not stale():
+    if not force and not stale() and not os.environ.get("RA_NVCC_EXTRA"):
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
     objdir = os.path.join(PKG, "_obj")
