@@ -287,6 +287,14 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     const uint32_t newmask = __ballot_sync(kFull, isnew);
     sk = 0;
     if constexpr (TP) {
+      // every new row's lines in flight at once (the dot's loads then merge
+      // with these misses instead of paying one L2 round trip per few lines)
+      if (isnew && !(a.flags & 8192u)) {
+        const char* r = BF ? reinterpret_cast<const char*>(keys16 + size_t(v) * D)
+                           : reinterpret_cast<const char*>(keys + size_t(v) * D);
+#pragma unroll
+        for (int l = 0; l < D * (BF ? 2 : 4) / 128; ++l) prefetch_l1(r + 128 * l);
+      }
       if (isnew) {
         double acc = 0.0;
         if constexpr (BF) {

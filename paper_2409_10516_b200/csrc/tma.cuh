@@ -57,6 +57,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// one 128-B line into L1 (CCTL-style prefetch; a later load of the line merges
+// with the pending miss)
+__device__ __forceinline__ void prefetch_l1(const void* src) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(src));
+}
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
