@@ -98,6 +98,49 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t id) {
 }
 __device__ __forceinline__ uint32_t lanemask_lt(uint32_t lane) { return (1u << lane) - 1u; }
 
+// Best-first bitonic sort of 256 (key, id) entries held by one warp, entry
+// lane * 8 + i in register i: distances < 8 inside a lane, the rest by
+// shuffles (15 of the 36 stages).
+__device__ __forceinline__ void warp_sort256(uint64_t (&k)[8], uint32_t (&id)[8], uint32_t lane) {
+#pragma unroll
+  for (uint32_t kk = 2; kk <= 256; kk <<= 1) {
+#pragma unroll
+    for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= 8) {
+        const uint32_t lj = j >> 3;
+        const bool lower = (lane & lj) == 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t e = lane * 8 + i;
+          const bool desc = (e & kk) == 0;
+          const uint64_t pk = __shfl_xor_sync(0xffffffffu, k[i], lj);
+          const uint32_t pi = __shfl_xor_sync(0xffffffffu, id[i], lj);
+          // the lower index keeps the better entry in a descending block
+          const bool pb = better(pk, pi, k[i], id[i]);
+          if (pb == (lower == desc)) k[i] = pk, id[i] = pi;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int pj = i ^ int(j);
+          if (pj > i) {
+            const uint32_t e = lane * 8 + i;
+            const bool desc = (e & kk) == 0;
+            const bool sw = desc ? better(k[pj], id[pj], k[i], id[i])
+                                 : better(k[i], id[i], k[pj], id[pj]);
+            if (sw) {
+              const uint64_t tk = k[i];
+              const uint32_t ti = id[i];
+              k[i] = k[pj], id[i] = id[pj];
+              k[pj] = tk, id[pj] = ti;
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
 // in-order f64 dot of q (f64, smem) and a key row staged in shared memory
 // (dot_f64, index_oodgraph.cpp:40-44; f32 x f32 products are exact in f64)
 template <int D>
@@ -783,6 +826,40 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     }
     if constexpr (TP) {
       __syncwarp();
+      if (fin_smem && p2 <= 256) {
+        // pool in registers (element lane * 8 + i), warp bitonic sort
+        uint64_t sk8[8];
+        uint32_t si8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t e = lane * 8 + i;
+          sk8[i] = e < p2 ? A.k[e] : 0;
+          si8[i] = e < p2 ? A.id[e] : kSentinel;
+        }
+        warp_sort256(sk8, si8, lane);
+        const uint32_t take = pool < k ? pool : k;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t r = lane * 8 + i;
+          if (r < k) {
+            const bool have = r < take;
+            const double sc = have ? okey_inv(sk8[i]) : __longlong_as_double(0x7ff8000000000000ll);
+            a.ids[size_t(b) * k + r] = have ? si8[i] : kSentinel;
+            a.scores[size_t(b) * k + r] = have ? (float)sc : __int_as_float(0x7fc00000);
+            if (a.scores64) a.scores64[size_t(b) * k + r] = sc;
+          }
+        }
+        for (uint32_t r = 256 + lane; r < k; r += 32) {  // k beyond the pool
+          a.ids[size_t(b) * k + r] = kSentinel;
+          a.scores[size_t(b) * k + r] = __int_as_float(0x7fc00000);
+          if (a.scores64) a.scores64[size_t(b) * k + r] = __longlong_as_double(0x7ff8000000000000ll);
+        }
+        if (lane == 0) {
+          a.n_out[b] = take;
+          a.truncated[b] = take < k;
+        }
+        return;
+      }
       for (uint32_t kk = 2; kk <= p2; kk <<= 1) {
         for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
           for (uint32_t i = lane; i < p2; i += 32) {
