@@ -1042,7 +1042,8 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
             hint_id[h] = i2;
           }
         }
-        if (depth + 1 >= chain_max || cid == kSentinel || !(ck2 > gk) || ctrl[0]) break;
+        if (depth + 1 >= chain_max || cid == kSentinel || ctrl[0]) break;
+        if (!(a.flags & 16384u) && !(ck2 > gk)) break;
         if (vbit(expd, cid)) break;
         {
           const uint32_t s0 = slot_of(cid);
