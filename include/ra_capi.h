@@ -135,7 +135,7 @@ uint64_t ra_graph_memory_bytes(const ra_graph* g);
 uint64_t ra_graph_device_bytes(const ra_graph* g);
 /* Copies the reference CSR (offsets_[n+1] u64, adjacency_ u32) into host
  * arrays sized from ra_graph_size / ra_graph_memory_bytes
- * (index_oodgraph.hpp:74-75). */
+ * (index_oodgraph.hpp:74-75); either pointer may be NULL (not copied). */
 ra_status ra_graph_csr(const ra_graph* g, uint64_t* offsets, uint32_t* adjacency);
 
 /* ---- search (OODGraph::search, index_oodgraph.cpp:357-411) -----------------

@@ -10,6 +10,9 @@
 // assert (e.g. test_index_oodgraph.cpp:384-400).
 #include <chrono>
 #include <cstdint>
+#include <filesystem>
+#include <fstream>
+#include <set>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -24,6 +27,8 @@
 #include "attnindex/index_ivf.hpp"
 #include "attnindex/io.hpp"
 #include "attnindex/workload.hpp"
+
+#include <json.hpp>
 
 using namespace attnindex;
 
@@ -394,6 +399,109 @@ int ref_ivf_search(void* h, const float* q, uint32_t d, uint64_t k, const uint32
     *n_out = r.ids.size();
     *scanned = r.scanned;
     *truncated = r.truncated;
+  });
+}
+
+// cmd_build (tools/main.cpp:401-480) restated over the reference library:
+// the workload comes from manifest_path (acquire_workloads' manifest branch,
+// main.cpp:344-358), every head's index is built with the reference's own
+// builders (build_index, main.cpp:360-374), artifacts and build_report.json
+// go to out_dir. kind: 0 flat, 1 ivf, 2 oodgraph. Verify counters are the
+// VerifyLog's (main.cpp:308-321): checks made, checks failed.
+int ref_build_report(const char* manifest_path, const char* out_dir, int kind, uint32_t k_train,
+                     uint32_t max_degree, uint32_t ef_construction, uint32_t edge_window,
+                     uint32_t nlist, uint64_t seed, uint32_t iters, uint32_t default_nprobe,
+                     int n_threads, int verify, uint64_t* checks, uint64_t* failures) {
+  namespace fs = std::filesystem;
+  using nlohmann::json;
+  return guard([&] {
+    uint64_t n_checks = 0, n_fail = 0;
+    auto check = [&](bool ok) {
+      if (!verify) return;
+      ++n_checks;
+      n_fail += !ok;
+    };
+    auto heads = load_workloads(manifest_path);
+    if (heads.empty()) throw std::runtime_error("workload has no heads");
+    fs::path dir(out_dir);
+    fs::create_directories(dir);
+    const IndexKind ik = kind == 0 ? IndexKind::Flat : kind == 1 ? IndexKind::IVF : IndexKind::OODGraph;
+    json report;
+    report["kind"] = std::string(index_kind_name(ik));
+    report["n_heads"] = heads.size();
+    report["n_keys"] = heads[0].keys->n;
+    json per_head = json::array();
+    std::set<const VectorSet*> counted;
+    size_t kv_bytes = 0, index_bytes = 0;
+    for (const auto& h : heads) {
+      std::unique_ptr<SearchIndex> idx;
+      if (ik == IndexKind::Flat) {
+        idx = flat_build(h.keys);
+      } else if (ik == IndexKind::IVF) {
+        IVFBuildParams p;
+        p.nlist = nlist;
+        p.seed = seed;
+        p.iters = iters;
+        p.default_nprobe = default_nprobe;
+        idx = ivf_build(h.keys, p);
+      } else {
+        OODGraphBuildParams p;
+        p.k_train = k_train;
+        p.max_degree = max_degree;
+        p.ef_construction = ef_construction;
+        p.edge_window = edge_window;
+        idx = ood_build(h.keys, h.prefill_queries, p, n_threads);
+      }
+      json entry;
+      entry["head"] = h.head_id;
+      entry["kv_group"] = h.kv_group_id;
+      if (const auto* g = dynamic_cast<const OODGraph*>(idx.get())) {
+        std::string name = "head" + std::to_string(h.head_id) + ".oodg";
+        g->save(dir / name);
+        entry["artifact"] = name;
+        uint64_t edges = 0;
+        std::vector<uint64_t> hist(g->max_degree_bound() + 1, 0);
+        for (uint64_t u = 0; u < g->size(); ++u) {
+          edges += g->degree(u);
+          hist[g->degree(u)] += 1;
+        }
+        entry["edges"] = edges;
+        entry["degree_histogram"] = hist;
+        entry["entry_point"] = g->entry_point();
+        check(g->reachable_count() == g->size());
+        auto back = OODGraph::load(h.keys, dir / name);
+        check(back->serialize() == g->serialize());
+      } else if (const auto* ivf = dynamic_cast<const IVFIndex*>(idx.get())) {
+        entry["artifact"] = nullptr;
+        entry["nlist"] = ivf->nlist();
+        std::vector<char> seen(ivf->size(), 0);
+        uint64_t total = 0;
+        bool ok = true;
+        for (uint32_t c = 0; c < ivf->nlist(); ++c)
+          for (uint32_t id : ivf->list(c)) {
+            if (id >= ivf->size() || seen[id]) ok = false;
+            else seen[id] = 1;
+            ++total;
+          }
+        check(ok && total == ivf->size());
+      } else {
+        entry["artifact"] = nullptr;
+        entry["note"] = "no preprocessing";
+      }
+      entry["memory_bytes"] = idx->memory_bytes();
+      index_bytes += idx->memory_bytes();
+      if (counted.insert(h.keys.get()).second) kv_bytes += h.keys->data.size() * sizeof(float);
+      if (counted.insert(h.values.get()).second) kv_bytes += h.values->data.size() * sizeof(float);
+      per_head.push_back(std::move(entry));
+    }
+    report["heads"] = std::move(per_head);
+    report["kv_bytes"] = kv_bytes;
+    report["index_bytes"] = index_bytes;
+    std::ofstream out(dir / "build_report.json", std::ios::binary | std::ios::trunc);
+    out << report.dump(2) + "\n";
+    if (!out) throw std::runtime_error("write failed");
+    *checks = n_checks;
+    *failures = n_fail;
   });
 }
 

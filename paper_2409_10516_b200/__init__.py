@@ -12,5 +12,6 @@ from .api import (  # noqa: F401
     InvalidArgument, KVGroup, KVPartition, OODGraph, OODGraphBuildParams, PartialAttention,
     SearchResult, default_context, empty_partial, merge, merge_gammas, ood_build,
     partial_attention, search_batch, static_partition, flat_build, engine_init)
+from .report import VerifyLog, build_run  # noqa: F401
 
 __version__ = lib.ra_version().decode()

@@ -297,8 +297,8 @@ uint64_t ra_graph_device_bytes(const ra_graph* g) { return g->adj.bytes(); }
 ra_status ra_graph_csr(const ra_graph* g, uint64_t* offsets, uint32_t* adjacency) {
   return guard([&] {
     if (!g) invalid("null graph");
-    std::copy(g->offsets.begin(), g->offsets.end(), offsets);
-    std::copy(g->adjacency.begin(), g->adjacency.end(), adjacency);
+    if (offsets) std::copy(g->offsets.begin(), g->offsets.end(), offsets);
+    if (adjacency) std::copy(g->adjacency.begin(), g->adjacency.end(), adjacency);
   });
 }
 
