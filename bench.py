@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-bf16", action="store_true", help="skip the bf16-KV measurement")
+    ap.add_argument("--no-throughput", action="store_true",
+                    help="skip the batched (throughput-mode) line (launch-list profiling)")
     ap.add_argument("--no-multilayer", action="store_true",
                     help="skip the 4-distinct-layer batched measurement")
     ap.add_argument("--flush-mb", type=int, default=512)
@@ -275,7 +277,8 @@ def main():
         e1.synchronize()
         e2e.append(e0.elapsed_time(e1))
 
-    tput = batched_throughput(a, ra, kvs, graphs, Q, cfg, flush, stream)
+    tput = (batched_throughput(a, ra, kvs, graphs, Q, cfg, flush, stream)
+            if not a.no_throughput else None)
     tput_ml = (multilayer_throughput(a, ra, spec, my_groups, hpg, kvs, graphs, Q, cfg, flush,
                                      stream, layer) if not a.no_multilayer else None)
     out32 = eng.decode_step_device(Q[a.warmup])[0].cpu().numpy()

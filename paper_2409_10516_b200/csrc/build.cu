@@ -112,7 +112,15 @@ __global__ void __launch_bounds__(KTHREADS)
     k_knn(const float* __restrict__ Q, uint64_t nq, const float* __restrict__ K, uint32_t n,
           uint32_t d, uint32_t kt, uint32_t cb, double* __restrict__ bufS,
           uint32_t* __restrict__ bufI, uint32_t* __restrict__ knn, unsigned long long* widen_ctr,
-          double* __restrict__ knn_s = nullptr) {
+          double* __restrict__ knn_s = nullptr, uint32_t kchunk = 0) {
+  // key split (few rows): block y scans keys [y * kchunk, +kchunk) into its
+  // own buffers and writes that range's top kt (ids absolute, with scores)
+  // at row y * nq + q; k_knn_merge then ranks the union
+  const uint32_t kbeg = kchunk ? blockIdx.y * kchunk : 0;
+  const uint32_t kend = kchunk ? min(n, kbeg + kchunk) : n;
+  const uint64_t rbase = uint64_t(blockIdx.y) * nq;
+  bufS += rbase * cb, bufI += rbase * cb, knn += rbase * kt;
+  if (knn_s) knn_s += rbase * kt;
   __shared__ double Qs[KDC][KQ + 1];
   __shared__ double Ks[KDC][KK + 1];
   __shared__ double th_s[KQ];
@@ -129,7 +137,7 @@ __global__ void __launch_bounds__(KTHREADS)
   }
   __syncthreads();
 
-  for (uint32_t k0 = 0; k0 < n; k0 += KK) {
+  for (uint32_t k0 = kbeg; k0 < kend; k0 += KK) {
     double acc[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -142,7 +150,7 @@ __global__ void __launch_bounds__(KTHREADS)
         const uint64_t qi = q0 + r;
         const uint32_t ki = k0 + r;
         Qs[c][r] = (qi < nq && c0 + c < d) ? (double)Q[qi * d + c0 + c] : 0.0;
-        Ks[c][r] = (ki < n && c0 + c < d) ? (double)K[size_t(ki) * d + c0 + c] : 0.0;
+        Ks[c][r] = (ki < kend && c0 + c < d) ? (double)K[size_t(ki) * d + c0 + c] : 0.0;
       }
       __syncthreads();
       const uint32_t cmax = min(KDC, d - c0);
@@ -169,7 +177,7 @@ __global__ void __launch_bounds__(KTHREADS)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const uint32_t key = k0 + tx + 16 * j;
-        if (key < n && better(acc[i][j], key, ts, ti)) {
+        if (key < kend && better(acc[i][j], key, ts, ti)) {
           const uint32_t pos = atomicAdd(&cnt[ql], 1u);
           bufS[(q0 + ql) * cb + pos] = acc[i][j];
           bufI[(q0 + ql) * cb + pos] = key;
@@ -206,12 +214,32 @@ __global__ void __launch_bounds__(KTHREADS)
     if (q0 + ql >= nq) continue;
     double* bs = bufS + (q0 + ql) * cb;
     uint32_t* bi = bufI + (q0 + ql) * cb;
-    compact_query(bs, bi, cnt[ql], kt, lane);
-    for (uint32_t r = lane; r < kt; r += 32) {
-      knn[(q0 + ql) * kt + r] = bi[r];
-      if (knn_s) knn_s[(q0 + ql) * kt + r] = bs[r];
+    const uint32_t c = compact_query(bs, bi, cnt[ql], kt, lane);
+    for (uint32_t r = lane; r < kt; r += 32) {  // r >= c only for a short key range
+      knn[(q0 + ql) * kt + r] = r < c ? bi[r] : kSentinel;
+      if (knn_s) knn_s[(q0 + ql) * kt + r] = r < c ? bs[r] : -DBL_MAX;
     }
   }
+}
+
+// union of the key-split partial lists of each row (C ranges x kt, exact
+// scores) -> the row's top kt; warp per row, sorted in its bufS/bufI slot
+__global__ void k_knn_merge(const uint32_t* __restrict__ pid, const double* __restrict__ ps,
+                            uint32_t nq, uint32_t C, uint32_t kt, uint32_t cb,
+                            double* __restrict__ bufS, uint32_t* __restrict__ bufI,
+                            uint32_t* __restrict__ knn) {
+  const uint32_t row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= nq) return;
+  double* bs = bufS + size_t(row) * cb;
+  uint32_t* bi = bufI + size_t(row) * cb;
+  for (uint32_t e = lane; e < C * kt; e += 32) {
+    const uint32_t c = e / kt, r = e % kt;
+    bs[e] = ps[(size_t(c) * nq + row) * kt + r];
+    bi[e] = pid[(size_t(c) * nq + row) * kt + r];
+  }
+  __syncwarp();
+  compact_query(bs, bi, C * kt, kt, lane);
+  for (uint32_t r = lane; r < kt; r += 32) knn[size_t(row) * kt + r] = bi[r];
 }
 
 __global__ void k_gather_rows(const float* __restrict__ Q, uint32_t d,
@@ -601,9 +629,15 @@ static void repair(ra_ctx* ctx, ra_kv* kv, const double* norms_dev, uint64_t ent
       }
     }
   };
+  static const bool trace = std::getenv("RA_REPAIR_TRACE") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  auto t0 = now();
   sweep();
+  if (trace) fprintf(stderr, "repair: sweep %.2f ms\n", ms(t0, now()));
   DevBuf<uint32_t> d_pend, d_anch, d_near;
   for (;;) {
+    auto t1 = now();
     std::vector<uint32_t> pending;
     for (uint32_t u = 0; u < n; ++u)
       if (!reached[u]) pending.push_back(u);
@@ -646,6 +680,7 @@ static void repair(ra_ctx* ctx, ra_kv* kv, const double* norms_dev, uint64_t ent
     RA_CUDA(cudaMemcpyAsync(nearest.data(), d_near.p, pending.size() * 4,
                             cudaMemcpyDeviceToHost, ctx->stream));
     RA_CUDA(cudaStreamSynchronize(ctx->stream));
+    auto t2 = now();
     std::vector<std::pair<uint32_t, uint32_t>> by_anchor(pending.size());
     for (size_t i = 0; i < pending.size(); ++i) by_anchor[i] = {nearest[i], pending[i]};
     std::sort(by_anchor.begin(), by_anchor.end());
@@ -673,7 +708,11 @@ static void repair(ra_ctx* ctx, ra_kv* kv, const double* norms_dev, uint64_t ent
       }
       g0 = g1;
     }
+    auto t3 = now();
     sweep();
+    if (trace)
+      fprintf(stderr, "repair: pending %zu anchors %zu  nearest %.2f ms  attach %.2f ms  sweep %.2f ms\n",
+              pending.size(), anchors.size(), ms(t1, t2), ms(t2, t3), ms(t3, now()));
   }
 }
 
@@ -700,7 +739,7 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
     const float* K = kv->keys.p;
     Timer tm(s);
 
-    DevBuf<double> norms(n);
+    DevBuf<double> norms(n, s);
     k_norms<<<(n + 255) / 256, 256, 0, s>>>(K, n, d, norms.p);
     RA_LAUNCH_CHECK();
 
@@ -709,11 +748,11 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
     DevBuf<float> tq_own;
     const float* TQ = train_q;
     if (nq && !on_device) {
-      tq_own.alloc(size_t(nq) * d);
+      tq_own.alloc(size_t(nq) * d, s);
       RA_CUDA(cudaMemcpyAsync(tq_own.p, train_q, size_t(nq) * d * 4, cudaMemcpyHostToDevice, s));
       TQ = tq_own.p;
     }
-    DevBuf<uint32_t> knn(std::max<size_t>(size_t(nq) * kt, 1));
+    DevBuf<uint32_t> knn(std::max<size_t>(size_t(nq) * kt, 1), s);
     const char* force_exact = std::getenv("RA_KNN_EXACT");
     const bool use_tc = nq && !(force_exact && force_exact[0] == '1') &&
                         knn_tc_supported(d, nq, n, kt);
@@ -726,15 +765,27 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
       st.knn_rows = nq;
       st.knn_rows_widened = nf;
       if (nf) {
-        DevBuf<float> qf(size_t(nf) * d);
-        DevBuf<uint32_t> kf(size_t(nf) * kt);
+        DevBuf<float> qf(size_t(nf) * d, s);
+        DevBuf<uint32_t> kf(size_t(nf) * kt, s);
         k_gather_rows<<<(nf * d + 255) / 256, 256, 0, s>>>(TQ, d, fail.p, nf, qf.p);
+        // few rows: split the keys over C blocks per row tile so the exact
+        // pass fills the GPU, then merge the C partial top-kt lists per row
+        const uint32_t tiles = (nf + KQ - 1) / KQ;
+        uint32_t C = std::max<uint32_t>(1, std::min<uint32_t>(64, 2 * ctx->num_sms / tiles));
+        uint32_t kchunk = (n + C - 1) / C;
+        kchunk = std::max<uint32_t>((kchunk + KK - 1) / KK * KK, (kt + KK - 1) / KK * KK);
+        C = (n + kchunk - 1) / kchunk;
         uint32_t cb = 1;
-        while (cb < 2 * kt + KK) cb <<= 1;
-        DevBuf<double> bs(size_t((nf + KQ - 1) / KQ * KQ) * cb);
-        DevBuf<uint32_t> bi(size_t((nf + KQ - 1) / KQ * KQ) * cb);
-        k_knn<<<(nf + KQ - 1) / KQ, KTHREADS, 0, s>>>(qf.p, nf, K, n, d, kt, cb, bs.p, bi.p,
-                                                      kf.p, nullptr);
+        while (cb < std::max<uint32_t>(2 * kt + KK, C * kt)) cb <<= 1;
+        const size_t rows_pad = size_t(tiles) * KQ;
+        DevBuf<double> bs(size_t(C) * rows_pad * cb, s);
+        DevBuf<uint32_t> bi(size_t(C) * rows_pad * cb, s);
+        DevBuf<uint32_t> pid(size_t(C) * nf * kt, s);
+        DevBuf<double> pscore(size_t(C) * nf * kt, s);
+        k_knn<<<dim3(tiles, C), KTHREADS, 0, s>>>(qf.p, nf, K, n, d, kt, cb, bs.p, bi.p, pid.p,
+                                                   nullptr, pscore.p, C > 1 ? kchunk : 0);
+        k_knn_merge<<<(nf + 7) / 8, 256, 0, s>>>(pid.p, pscore.p, nf, C, kt, cb, bs.p, bi.p,
+                                                 kf.p);
         k_scatter_knn<<<(nf * kt + 255) / 256, 256, 0, s>>>(kf.p, fail.p, nf, kt, knn.p);
         RA_LAUNCH_CHECK();
       }
@@ -742,9 +793,9 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
       uint32_t cb = 1;
       while (cb < 2 * kt + KK) cb <<= 1;
       const uint64_t chunk = std::min<uint64_t>(nq, std::max<uint64_t>(KQ, (1ull << 30) / (cb * 12ull)) / KQ * KQ);
-      DevBuf<double> bs(size_t(chunk) * cb);
-      DevBuf<uint32_t> bi(size_t(chunk) * cb);
-      DevBuf<unsigned long long> ctr(1);
+      DevBuf<double> bs(size_t(chunk) * cb, s);
+      DevBuf<uint32_t> bi(size_t(chunk) * cb, s);
+      DevBuf<unsigned long long> ctr(1, s);
       RA_CUDA(cudaMemsetAsync(ctr.p, 0, 8, s));
       for (uint64_t c0 = 0; c0 < nq; c0 += chunk) {
         const uint64_t cn = std::min<uint64_t>(chunk, nq - c0);
@@ -765,10 +816,10 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
     for (uint32_t b = 1; b < kt; ++b) b_off[b + 1] = b_off[b] + prop_count(b, p->edge_window);
     const uint32_t per_row = kt > 1 ? b_off[kt] : 0;
     const uint64_t total = uint64_t(nq) * per_row;
-    DevBuf<uint64_t> edges(std::max<uint64_t>(total, 1)), edges2(std::max<uint64_t>(total, 1));
+    DevBuf<uint64_t> edges(std::max<uint64_t>(total, 1), s), edges2(std::max<uint64_t>(total, 1), s);
     uint64_t ne = 0;
     if (total) {
-      DevBuf<uint32_t> d_boff(b_off.size());
+      DevBuf<uint32_t> d_boff(b_off.size(), s);
       RA_CUDA(cudaMemcpyAsync(d_boff.p, b_off.data(), b_off.size() * 4, cudaMemcpyHostToDevice, s));
       const uint64_t threads = uint64_t(nq) * (kt - 1);
       k_proposals<<<uint32_t((threads + 255) / 256), 256, 0, s>>>(knn.p, nq, kt, p->edge_window,
@@ -778,20 +829,20 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
       while (end_bit < 64 && (uint64_t(n - 1) >> (end_bit - 32)) != 0) ++end_bit;
       size_t tb = 0;
       cub::DeviceRadixSort::SortKeys(nullptr, tb, edges.p, edges2.p, (int64_t)total, 0, end_bit, s);
-      DevBuf<uint8_t> tmp(tb);
+      DevBuf<uint8_t> tmp(tb, s);
       RA_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, edges.p, edges2.p, (int64_t)total, 0,
                                              end_bit, s));
-      DevBuf<uint64_t> nsel(1);
+      DevBuf<uint64_t> nsel(1, s);
       size_t tb2 = 0;
       cub::DeviceSelect::Unique(nullptr, tb2, edges2.p, edges.p, nsel.p, (int64_t)total, s);
-      DevBuf<uint8_t> tmp2(tb2);
+      DevBuf<uint8_t> tmp2(tb2, s);
       RA_CUDA(cub::DeviceSelect::Unique(tmp2.p, tb2, edges2.p, edges.p, nsel.p, (int64_t)total, s));
       RA_CUDA(cudaMemcpyAsync(&ne, nsel.p, 8, cudaMemcpyDeviceToHost, s));
       RA_CUDA(cudaStreamSynchronize(s));
     }
     edges2.reset();
     st.candidate_edges = ne;
-    DevBuf<uint64_t> off(size_t(n) + 1);
+    DevBuf<uint64_t> off(size_t(n) + 1, s);
     k_src_offsets<<<(n + 1 + 255) / 256, 256, 0, s>>>(edges.p, ne, n, off.p);
     RA_LAUNCH_CHECK();
     st.ms_edges = tm.lap();
@@ -802,7 +853,7 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
     g->max_degree = M;
     g->default_ef = p->default_ef;
     g->adj.alloc(size_t(n) * M);
-    DevBuf<uint32_t> deg(n), big(n), big_cnt(1);
+    DevBuf<uint32_t> deg(n, s), big(n, s), big_cnt(1, s);
     RA_CUDA(cudaMemsetAsync(big_cnt.p, 0, 4, s));
     const size_t psmem = PWARPS * (PCAP * 12 + size_t(M) * 4);
     RA_CUDA(cudaFuncSetAttribute(k_prune, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
@@ -817,15 +868,16 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
     if (nbig) {
       // hub nodes with more candidates than shared memory holds: HBM buffers
       std::vector<uint64_t> h_off(size_t(n) + 1);
-      RA_CUDA(cudaMemcpy(h_off.data(), off.p, h_off.size() * 8, cudaMemcpyDeviceToHost));
+      RA_CUDA(cudaMemcpyAsync(h_off.data(), off.p, h_off.size() * 8, cudaMemcpyDeviceToHost, s));
+      RA_CUDA(cudaStreamSynchronize(s));
       uint64_t maxc = 0;
       for (uint32_t u = 0; u < n; ++u) maxc = std::max(maxc, h_off[u + 1] - h_off[u]);
       uint64_t p2 = 1;
       while (p2 < maxc) p2 <<= 1;
       const uint32_t gwarps = std::min<uint32_t>(nbig, 1024);
       const uint32_t ggrid = (gwarps + PWARPS - 1) / PWARPS;
-      DevBuf<double> gm(size_t(ggrid) * PWARPS * p2);
-      DevBuf<uint32_t> gv(size_t(ggrid) * PWARPS * p2);
+      DevBuf<double> gm(size_t(ggrid) * PWARPS * p2, s);
+      DevBuf<uint32_t> gv(size_t(ggrid) * PWARPS * p2, s);
       k_prune<<<ggrid, PWARPS * 32, psmem, s>>>(K, n, d, norms.p, edges.p, off.p, big.p, nbig, M,
                                                p->ef_construction, !p->prune_inner_product, gm.p,
                                                gv.p, p2, g->adj.p, deg.p, nullptr, nullptr);
@@ -835,16 +887,16 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
     st.ms_prune = tm.lap();
 
     // ---- entry point ----
-    DevBuf<uint32_t> covered(1);
+    DevBuf<uint32_t> covered(1, s);
     RA_CUDA(cudaMemsetAsync(covered.p, 0, 4, s));
     k_any_covered<<<(n + 255) / 256, 256, 0, s>>>(deg.p, n, covered.p);
-    DevBuf<double> mean(d);
+    DevBuf<double> mean(d, s);
     if (!p->entry_maxnorm) k_colmean<<<(d + 31) / 32, 256, 0, s>>>(K, n, d, mean.p);
     uint32_t any = 0;
     RA_CUDA(cudaMemcpyAsync(&any, covered.p, 4, cudaMemcpyDeviceToHost, s));
     RA_CUDA(cudaStreamSynchronize(s));
     const uint32_t eblocks = (n + 255) / 256;
-    DevBuf<unsigned long long> best(2 * eblocks);
+    DevBuf<unsigned long long> best(2 * eblocks, s);
     k_entry_key<<<eblocks, 256, 0, s>>>(K, n, d, mean.p, norms.p, deg.p, any, p->entry_maxnorm,
                                         best.p);
     RA_LAUNCH_CHECK();
@@ -867,15 +919,24 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
 
     // ---- phase 4 + CSR ----
     const uint32_t rounds0 = st.repair_rounds;
+    const auto tr0 = std::chrono::steady_clock::now();
     repair(ctx, kv, norms.p, g->entry, M, h_adj, h_deg, &st);
+    const auto tr1 = std::chrono::steady_clock::now();
     g->offsets.assign(size_t(n) + 1, 0);
     for (uint32_t u = 0; u < n; ++u) g->offsets[u + 1] = g->offsets[u] + h_deg[u];
     g->adjacency.resize(g->offsets[n]);
     for (uint32_t u = 0; u < n; ++u)
       std::copy(h_adj.begin() + size_t(u) * M, h_adj.begin() + size_t(u) * M + h_deg[u],
                 g->adjacency.begin() + g->offsets[u]);
+    const auto tr2 = std::chrono::steady_clock::now();
     if (st.repair_rounds != rounds0) graph_upload(ctx, g.get());  // else the device rows stand
+    const auto tr3 = std::chrono::steady_clock::now();
     st.ms_repair = tm.lap();
+    if (std::getenv("RA_REPAIR_TRACE")) {
+      auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      fprintf(stderr, "phase4: repair %.2f csr %.2f upload %.2f lap-wait %.2f ms\n", ms(tr0, tr1),
+              ms(tr1, tr2), ms(tr2, tr3), ms(tr3, std::chrono::steady_clock::now()));
+    }
 
     ra_kv_retain(kv);
     g->kv = kv;
@@ -905,17 +966,17 @@ extern "C" ra_status ra_flat_search_batch(ra_ctx* ctx, ra_kv* kv, uint32_t B, co
     DevBuf<uint32_t> bits;
     if (mask_n) {
       const uint64_t words = (n + 31) / 32;
-      bits.alloc(words);
+      bits.alloc(words, s);
       launch_mask_bitset(s, mask, mask_n, bits.p, words);
     }
     uint32_t cb = 1;
     while (cb < 2 * kt + KK) cb <<= 1;
     const uint64_t chunk = std::min<uint64_t>(
         B, std::max<uint64_t>(KQ, (1ull << 30) / (uint64_t(cb) * 12ull)) / KQ * KQ);
-    DevBuf<double> bs(size_t((chunk + KQ - 1) / KQ * KQ) * cb);
-    DevBuf<uint32_t> bi(size_t((chunk + KQ - 1) / KQ * KQ) * cb);
-    DevBuf<uint32_t> tk(size_t(chunk) * kt);
-    DevBuf<double> ts(size_t(chunk) * kt);
+    DevBuf<double> bs(size_t((chunk + KQ - 1) / KQ * KQ) * cb, s);
+    DevBuf<uint32_t> bi(size_t((chunk + KQ - 1) / KQ * KQ) * cb, s);
+    DevBuf<uint32_t> tk(size_t(chunk) * kt, s);
+    DevBuf<double> ts(size_t(chunk) * kt, s);
     for (uint64_t c0 = 0; c0 < B; c0 += chunk) {
       const uint32_t cn = uint32_t(std::min<uint64_t>(chunk, B - c0));
       k_knn<<<(cn + KQ - 1) / KQ, KTHREADS, 0, s>>>(q + c0 * d, cn, kv->keys.p, uint32_t(n), d, kt,

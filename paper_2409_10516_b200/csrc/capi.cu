@@ -21,7 +21,7 @@ void graph_upload(ra_ctx* ctx, ra_graph* g) {
   for (uint64_t u = 0; u < n; ++u)
     std::copy(g->adjacency.begin() + g->offsets[u], g->adjacency.begin() + g->offsets[u + 1],
               rows.begin() + u * M);
-  g->adj.alloc(rows.size());
+  if (g->adj.n != rows.size()) g->adj.alloc(rows.size());  // (a build re-uploads in place)
   RA_CUDA(cudaMemcpyAsync(g->adj.p, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice,
                           ctx->stream));
   RA_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -56,6 +56,13 @@ ra_status ra_ctx_create(int device, ra_ctx** out) {
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
     c->smem_optin = prop.sharedMemPerBlockOptin;
+    // stream-ordered scratch (DevBuf(count, stream)) stays cached in the
+    // default pool between calls instead of going back to the driver
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = 32ull << 30;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     *out = c.release();
   });
 }

@@ -59,14 +59,26 @@ template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  // stream-ordered temporaries (alloc with a stream): cudaMallocAsync /
+  // cudaFreeAsync from the device's default pool, which keeps freed blocks
+  // (release threshold set at context creation), so a build's gigabyte-
+  // sized scratch costs no cudaMalloc / cudaFree (device sync) per call.
+  // Only for buffers that die before their stream does.
+  cudaStream_t st = nullptr;
+  bool pooled = false;
   DevBuf() = default;
   explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(size_t count, cudaStream_t s) { alloc(count, s); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), st(o.st), pooled(o.pooled) {
+    o.p = nullptr, o.n = 0, o.pooled = false;
+  }
   DevBuf& operator=(DevBuf&& o) noexcept {
     std::swap(p, o.p);
     std::swap(n, o.n);
+    std::swap(st, o.st);
+    std::swap(pooled, o.pooled);
     return *this;
   }
   ~DevBuf() { reset(); }
@@ -75,14 +87,23 @@ struct DevBuf {
     if (count) RA_CUDA(cudaMalloc(&p, count * sizeof(T)));
     n = count;
   }
+  void alloc(size_t count, cudaStream_t s) {
+    reset();
+    if (count) RA_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
+    n = count, st = s, pooled = true;
+  }
   // grow-only reallocation (contents not preserved)
   void ensure(size_t count) {
     if (count > n) alloc(count);
   }
   void reset() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (pooled) cudaFreeAsync(p, st);
+      else cudaFree(p);
+    }
     p = nullptr;
     n = 0;
+    pooled = false;
   }
   size_t bytes() const { return n * sizeof(T); }
 };

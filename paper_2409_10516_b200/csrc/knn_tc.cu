@@ -517,15 +517,15 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
   constexpr uint32_t cb = 2048;     // survivor buffer per row
   constexpr uint32_t msamp = 2048;  // strided key sample for the threshold
   constexpr uint32_t target = 640;  // expected survivors per row (>= kt w.h.p.)
-  DevBuf<uint16_t> A(mt * TM * K3), B(nt * TN * K3);
+  DevBuf<uint16_t> A(mt * TM * K3, s), B(nt * TN * K3, s);
   {
     const uint64_t ta = mt * TM * d, tb = nt * TN * d;
     k_split<<<uint32_t((ta + 255) / 256), 256, 0, s>>>(Q, nq, d, TM, mt, 1, A.p);
     k_split<<<uint32_t((tb + 255) / 256), 256, 0, s>>>(K, n, d, TN, nt, 0, B.p);
     RA_LAUNCH_CHECK();
   }
-  DevBuf<float> bufS(nq * cb), thr(nq);
-  DevBuf<uint32_t> bufI(nq * cb), cnt(nq);
+  DevBuf<float> bufS(nq * cb, s), thr(nq, s);
+  DevBuf<uint32_t> bufI(nq * cb, s), cnt(nq, s);
   const size_t smem = size_t(TM) * K3 * 2 + NSTAGE * TN * KS * 2 + 256;
   RA_CUDA(cudaFuncSetAttribute(k_knn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaEvent_t e0, e1;
@@ -535,8 +535,8 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
   const bool sampled = n > cb;
   if (sampled) {
     // pass 1: S~ against a strided sample; threshold = r-th largest
-    DevBuf<float> ks(size_t(msamp) * d);
-    DevBuf<uint16_t> Bs(size_t(msamp) * K3);
+    DevBuf<float> ks(size_t(msamp) * d, s);
+    DevBuf<uint16_t> Bs(size_t(msamp) * K3, s);
     k_gather_sample<<<(msamp * d + 255) / 256, 256, 0, s>>>(K, n, d, msamp, ks.p);
     k_split<<<(msamp * d + 255) / 256, 256, 0, s>>>(ks.p, msamp, d, TN, msamp / TN, 0, Bs.p);
     TcArgs t1{A.p, Bs.p, nq, msamp, K3, cb, nullptr, bufS.p, bufI.p, cnt.p};
@@ -553,9 +553,9 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
       uint32_t m2 = msamp;
       while (m2 < n / 64 && m2 < 65536) m2 *= 2;
       m2 = (m2 / TN) * TN;
-      DevBuf<float> ks2(size_t(m2) * d);
-      DevBuf<uint16_t> Bs2(size_t(m2) * K3);
-      DevBuf<float> thr2(nq);
+      DevBuf<float> ks2(size_t(m2) * d, s);
+      DevBuf<uint16_t> Bs2(size_t(m2) * K3, s);
+      DevBuf<float> thr2(nq, s);
       k_gather_sample<<<uint32_t((uint64_t(m2) * d + 255) / 256), 256, 0, s>>>(K, n, d, m2, ks2.p);
       k_split<<<uint32_t((uint64_t(m2) * d + 255) / 256), 256, 0, s>>>(ks2.p, m2, d, TN, m2 / TN, 0,
                                                                       Bs2.p);
@@ -572,7 +572,7 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
   k_knn_tc<<<uint32_t(mt), KNN_THREADS, smem, s>>>(t2);
   RA_LAUNCH_CHECK();
   cudaEventRecord(e1, s);
-  DevBuf<unsigned long long> kmax(1);
+  DevBuf<unsigned long long> kmax(1, s);
   RA_CUDA(cudaMemsetAsync(kmax.p, 0, 8, s));
   k_max_norm<<<(n + 255) / 256, 256, 0, s>>>(K, n, d, kmax.p);
   unsigned long long km_bits = 0;
@@ -586,7 +586,7 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
   double kmax_norm;
   std::memcpy(&kmax_norm, &km_bits, 8);
   fail_rows.ensure(std::max<uint64_t>(nq, 1));
-  DevBuf<uint32_t> fcount(1);
+  DevBuf<uint32_t> fcount(1, s);
   RA_CUDA(cudaMemsetAsync(fcount.p, 0, 4, s));
   // |S - S~| <= (3 * 2^-16 + K3 * 2^-23) * |q| |k|; 2^-10 is generous
   const double delta_scale = 1.0 / 1024.0;

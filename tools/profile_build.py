@@ -9,6 +9,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--reps", type=int, default=1)
+    ap.add_argument("--heads", type=int, default=1, help="distinct prefill-query sets (of 4)")
     a = ap.parse_args()
     import torch
     import paper_2409_10516_b200 as ra
@@ -17,11 +19,13 @@ def main():
                                     seed=7, n_decode=1), 0, "cuda")
     kv = ra.KVGroup(w["keys"], w["values"])
     torch.cuda.synchronize()
-    t = time.time()
-    g = ra.ood_build(kv, w["prefill_q"][0], ra.OODGraphBuildParams(128, 24, 256, 8))
-    print(f"n={a.n} build {1e3 * (time.time() - t):.1f} ms phases {g.build_stats.ms} "
-          f"repair rounds {g.build_stats.repair_rounds} nodes {g.build_stats.repaired_nodes} "
-          f"fallback_rows {g.build_stats.knn_rows_widened}")
+    for r in range(a.reps):
+        t = time.time()
+        g = ra.ood_build(kv, w["prefill_q"][r % a.heads], ra.OODGraphBuildParams(128, 24, 256, 8))
+        ms = {k: round(v, 1) for k, v in g.build_stats.ms.items()}
+        print(f"n={a.n} build {1e3 * (time.time() - t):.1f} ms phases {ms} "
+              f"repair rounds {g.build_stats.repair_rounds} nodes {g.build_stats.repaired_nodes} "
+              f"fallback_rows {g.build_stats.knn_rows_widened}")
 
 
 if __name__ == "__main__":
