@@ -67,8 +67,11 @@ constexpr uint32_t kTW = RA_TP_WARPS;  // TP mode: queries (warps) per CTA
 #endif
 constexpr int kFR = 8;             // frontier entries per lane (sorted)
 constexpr int kUR = 8;             // pool-candidate entries per lane
-constexpr uint32_t kSlots = 64;    // packet table, 2-way set-associative by node id
-constexpr uint32_t kSlotBits = 6;
+#ifndef RA_PIPE_SLOT_BITS
+#define RA_PIPE_SLOT_BITS 7
+#endif
+constexpr uint32_t kSlotBits = RA_PIPE_SLOT_BITS;
+constexpr uint32_t kSlots = 1u << kSlotBits;  // packet table, 2-way set-associative by node id
 constexpr uint32_t kPick = 12;     // helpers consider the best kPick heads
 constexpr uint32_t kChain = 3;     // greedy chain depth after a pre-expansion
 #ifndef RA_PIPE_SLACK
@@ -213,7 +216,8 @@ __device__ __forceinline__ void warp_best(uint64_t& k, uint32_t& id) {
 struct PipeLayout {
   uint32_t D, MT, vis_words, vis_smem, capO;
   static constexpr size_t kBars = 0, kCtrl = 64, kPubK = 128, kPubId = 384, kSlotW = 512,
-                          kCnt = 1024, kMb = 1280, kNk = 1536, kPkId = 2048,
+                          kCnt = kSlotW + size_t(kSlots) * 8, kMb = kCnt + size_t(kSlots) * 4,
+                          kNk = kMb + size_t(kSlots) * 4, kPkId = kNk + size_t(kSlots) * 8,
                           kPkK = kPkId + size_t(kSlots) * 32 * 4,
                           kPubF = kPkK + size_t(kSlots) * 32 * 8,  // F: k u64[kFR][32], id u32[kFR][32]
                           kHint = kPubF + size_t(kFR) * 32 * 12,   // hints: k u64[32], id u32[32]
@@ -277,6 +281,13 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
   // right after their parent commits), written by helpers, read by helpers
   volatile uint64_t* hint_k = reinterpret_cast<volatile uint64_t*>(smem + PipeLayout::kHint);
   volatile uint32_t* hint_id = reinterpret_cast<volatile uint32_t*>(hint_k + 32);
+  // one entry into the 32-slot hint ring (any warp, one lane)
+  auto push_hint = [&](uint64_t k, uint32_t id) {
+    const uint32_t h = atomicAdd(const_cast<uint32_t*>(ctrl) + 12, 1u) & 31u;
+    hint_id[h] = kSentinel;
+    hint_k[h] = k;
+    hint_id[h] = id;
+  };
   unsigned long long* slotw = reinterpret_cast<unsigned long long*>(smem + PipeLayout::kSlotW);
   uint32_t* pk_cnt = reinterpret_cast<uint32_t*>(smem + PipeLayout::kCnt);
   uint32_t* pk_mb = reinterpret_cast<uint32_t*>(smem + PipeLayout::kMb);
@@ -684,6 +695,22 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         if (!(tk >= H && cH < ef) && count_gt(tk) >= ef) break;
       }
       PIPE_TICK(0)
+      // the top's packet: look it up and take a ready one (READY -> TAKEN)
+      // BEFORE the pop, which it does not depend on, so the pop's shuffles
+      // run in the shadow of the loads and the CAS; an in-flight packet is
+      // awaited after the pop
+      uint32_t sl = 0;
+      uint64_t w = 0;
+      bool took = false;
+      if constexpr (!TP) {
+        sl = slot_of(tid);
+        w = *reinterpret_cast<volatile unsigned long long*>(slotw + sl);
+        const uint64_t w1 = *reinterpret_cast<volatile unsigned long long*>(slotw + sl + 1);
+        if (uint32_t(w) != tid && uint32_t(w1) == tid) w = w1, ++sl;
+        if (lane == 0 && uint32_t(w) == tid && uint32_t(w >> 32) == sREADY)
+          took = atomicCAS(slotw + sl, slotword(tid, sREADY), slotword(tid, sTAKEN)) ==
+                 slotword(tid, sREADY);
+      }
       // pop (:391)
       if (from_fo) {
         ++c_fopop;
@@ -724,27 +751,19 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         pre = true;
         continue;
       }
-      // the top's packet: hit (ready or in flight) or expand inline
-      uint32_t sl = slot_of(tid);
-      uint64_t w = *reinterpret_cast<volatile unsigned long long*>(slotw + sl);
-      {
-        const uint64_t w1 = *reinterpret_cast<volatile unsigned long long*>(slotw + sl + 1);
-        if (uint32_t(w) != tid && uint32_t(w1) == tid) w = w1, ++sl;
-      }
-      bool hit = false;
-      if (uint32_t(w) == tid) {
-        if (uint32_t(w >> 32) == sBUSY) {
-          const uint64_t tw0 = clock64();
-          do {
-            __nanosleep(20);
-            w = *reinterpret_cast<volatile unsigned long long*>(slotw + sl);
-          } while (uint32_t(w >> 32) == sBUSY && uint32_t(w) == tid);
-          c_wait += clock64() - tw0;
-        }
+      // hit (taken above, or in flight: wait, then take) or expand inline
+      bool hit = __shfl_sync(kFull, took, 0);
+      if (!hit && uint32_t(w) == tid && uint32_t(w >> 32) == sBUSY) {
+        const uint64_t tw0 = clock64();
+        do {
+          __nanosleep(20);
+          w = *reinterpret_cast<volatile unsigned long long*>(slotw + sl);
+        } while (uint32_t(w >> 32) == sBUSY && uint32_t(w) == tid);
+        c_wait += clock64() - tw0;
         if (lane == 0 && uint32_t(w) == tid && uint32_t(w >> 32) == sREADY)
-          hit = atomicCAS(slotw + sl, slotword(tid, sREADY), slotword(tid, sTAKEN)) ==
-                slotword(tid, sREADY);
-        hit = __shfl_sync(kFull, hit, 0);
+          took = atomicCAS(slotw + sl, slotword(tid, sREADY), slotword(tid, sTAKEN)) ==
+                 slotword(tid, sREADY);
+        hit = __shfl_sync(kFull, took, 0);
       }
       // expanded bit after the take: helpers may evict packets of expanded nodes
       if (lane == 0) atomicOr(expd + (tid >> 5), 1u << (tid & 31));
@@ -768,13 +787,27 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
       } else {
         ++c_miss;
 #ifdef RA_PIPE_MISSCLASS
-        // 1: slot held another live packet, 2: empty slot, 3: own id (taken race)
-        if (uint32_t(w) != tid && uint32_t(w >> 32) != sFREE) cy[4] += 1;
-        else if (uint32_t(w) != tid) cy[4] += 1ull << 20;
+        // 1: a child of the node just visited from a packet, 2: a child of an
+        // inline expansion (miss chain), 3: older
+        if (__any_sync(kFull, cand && cv == tid)) cy[4] += pre ? (1ull << 20) : 1ull;
         else cy[4] += 1ull << 40;
 #endif
         expand(tid, cv, cx, cand, cm);
         pre = true;
+        if (!(a.flags & (8u | 32768u))) {
+          // the likely next tops are this node's best children, which no
+          // helper has seen: hint the best two so helpers start on them now
+          uint64_t k1 = cand ? cx : 0;
+          uint32_t i1 = cand ? cv : kSentinel;
+          warp_best(k1, i1);
+          uint64_t k2 = (cand && cv != i1) ? cx : 0;
+          uint32_t i2 = (cand && cv != i1) ? cv : kSentinel;
+          warp_best(k2, i2);
+          if (lane == 0) {
+            if (i1 != kSentinel) push_hint(k1, i1);
+            if (i2 != kSentinel) push_hint(k2, i2);
+          }
+        }
       }
     }
     // ---- result (:402-410): the pool's top min(k, |pool|), best-first ----
@@ -1035,15 +1068,15 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
           uint64_t k2 = (isnew && v != cid) ? x : 0;
           uint32_t i2 = (isnew && v != cid) ? v : kSentinel;
           warp_best(k2, i2);
-          if (lane == 0 && i2 != kSentinel && k2 > gk && !(a.flags & 8u)) {
-            const uint32_t h = atomicAdd(const_cast<uint32_t*>(ctrl) + 12, 1u) & 31u;
-            hint_id[h] = kSentinel;
-            hint_k[h] = k2;
-            hint_id[h] = i2;
-          }
+          if (lane == 0 && i2 != kSentinel && k2 > gk && !(a.flags & 8u)) push_hint(k2, i2);
         }
-        if (depth + 1 >= chain_max || cid == kSentinel || ctrl[0]) break;
-        if (!(a.flags & 16384u) && !(ck2 > gk)) break;
+        const bool chain = !(depth + 1 >= chain_max || cid == kSentinel || ctrl[0]) &&
+                           ((a.flags & 16384u) || ck2 > gk);
+        // an unchained best child is still a likely top soon after this
+        // packet is committed: a hint for another helper
+        if (!chain && lane == 0 && cid != kSentinel && !(a.flags & (8u | 65536u)))
+          push_hint(ck2, cid);
+        if (!chain) break;
         if (vbit(expd, cid)) break;
         {
           const uint32_t s0 = slot_of(cid);

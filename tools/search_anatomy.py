@@ -62,8 +62,8 @@ def main():
         if os.environ.get("RA_MISSCLASS"):
             raw = d[:, 9].astype(np.uint64)
             coll, empty, own = raw & 0xFFFFF, (raw >> 20) & 0xFFFFF, raw >> 40
-            print(f"miss classes (mean/head): collision {coll.mean():.1f} "
-                  f"empty {empty.mean():.1f} own {own.mean():.1f}")
+            print(f"miss classes (mean/head): child of a packet {coll.mean():.1f} "
+                  f"child of an inline expansion {empty.mean():.1f} older {own.mean():.1f}")
         print("mean  " + " ".join(f"{c}={d[:, j].mean() / (clk if j in (1, 2, 7, 8, 9, 10, 11) else 1):.1f}"
                                   for j, c in enumerate(cols)))
         return
