@@ -1064,11 +1064,17 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         uint64_t ck2 = isnew ? x : 0;
         uint32_t cid = isnew ? v : kSentinel;
         warp_best(ck2, cid);
-        {  // the runner-up beating the parent becomes a hint for idle helpers
+        {  // the runner-up (and optionally the third) child: hints for idle helpers
           uint64_t k2 = (isnew && v != cid) ? x : 0;
           uint32_t i2 = (isnew && v != cid) ? v : kSentinel;
           warp_best(k2, i2);
-          if (lane == 0 && i2 != kSentinel && k2 > gk && !(a.flags & 8u)) push_hint(k2, i2);
+          if (lane == 0 && i2 != kSentinel && !(a.flags & 8u)) push_hint(k2, i2);
+          if (a.flags & 131072u) {
+            uint64_t k3 = (isnew && v != cid && v != i2) ? x : 0;
+            uint32_t i3 = (isnew && v != cid && v != i2) ? v : kSentinel;
+            warp_best(k3, i3);
+            if (lane == 0 && i3 != kSentinel) push_hint(k3, i3);
+          }
         }
         const bool chain = !(depth + 1 >= chain_max || cid == kSentinel || ctrl[0]) &&
                            ((a.flags & 16384u) || ck2 > gk);
