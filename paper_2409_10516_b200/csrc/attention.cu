@@ -283,38 +283,62 @@ __global__ void __launch_bounds__(128)
                   const double* __restrict__ s64, const uint32_t* __restrict__ n_out,
                   uint32_t k, uint32_t hpg, uint32_t C, uint32_t nW, double inv_sqrt_d,
                   const double* __restrict__ part_out, const double* __restrict__ part_m,
-                  const double* __restrict__ part_s, double* __restrict__ out) {
+                  const double* __restrict__ part_s, double* __restrict__ out, uint32_t TR) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t h = blockIdx.x, g = h / hpg, hl = h % hpg, tid = threadIdx.x;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-  T* Vt = reinterpret_cast<T*>(smem + 16);                          // [kWC][D]
-  double* e = reinterpret_cast<double*>(Vt + kWC * D);              // [kWC]
+  T* Vt = reinterpret_cast<T*>(smem + 16);                          // [TR][D]
+  double* e = reinterpret_cast<double*>(Vt + size_t(TR) * D);       // [TR]
+  double* wx = e + TR;                                              // [C] chunk weights
   __shared__ double red[4];
   const uint32_t m = n_out[h];
   const T* V = kv_vals<T>(hkv[h]);
-  if (tid == 0) mbar_init(bar);
+  // the first Omega tile's V rows are requested before anything else, so
+  // the copies overlap the max / W-fold arithmetic below
+  uint32_t rows = min(TR, m);
+  if (tid == 0) {
+    mbar_init(bar);
+    fence_proxy_async();
+    mbar_arrive_expect_tx(bar, rows * D * uint32_t(sizeof(T)));
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < rows; i += blockDim.x)
+    bulk_g2s(Vt + size_t(i) * D, V + size_t(ids[size_t(h) * k + i]) * D, D * uint32_t(sizeof(T)),
+             bar);
   // Omega max (scores are exact f64 search scores; z = s / sqrt(d))
   double zo = -DBL_MAX;
   for (uint32_t i = tid; i < m; i += blockDim.x) zo = fmax(zo, s64[size_t(h) * k + i] * inv_sqrt_d);
   for (int o = 16; o; o >>= 1) zo = fmax(zo, __shfl_xor_sync(kFull, zo, o));
   if ((tid & 31) == 0) red[tid >> 5] = zo;
+  // W chunk maxima -> smem (one load per chunk)
+  for (uint32_t c = tid; c < C; c += blockDim.x) wx[c] = part_m[(size_t(g) * C + c) * hpg + hl];
   __syncthreads();
   zo = fmax(fmax(red[0], red[1]), fmax(red[2], red[3]));
+  double zw = -DBL_MAX;
+  for (uint32_t c = 0; c < C; ++c) zw = fmax(zw, wx[c]);
+  __syncthreads();  // every thread has read the maxima
+  for (uint32_t c = tid; c < C; c += blockDim.x) wx[c] = exp(wx[c] - zw);
+  for (uint32_t i = tid; i < rows; i += blockDim.x) e[i] = exp(s64[size_t(h) * k + i] * inv_sqrt_d - zo);
+  __syncthreads();
+  double sw = 0.0;
+  for (uint32_t c = 0; c < C; ++c) sw += wx[c] * part_s[(size_t(g) * C + c) * hpg + hl];
   double acc[(D + 127) / 128] = {};
   double so = 0.0;
   uint32_t phase = 0;
-  for (uint32_t t0 = 0; t0 < m; t0 += kWC) {
-    const uint32_t rows = min(kWC, m - t0);
-    __syncthreads();  // previous tile fully consumed
-    if (tid == 0) {
-      fence_proxy_async();
-      mbar_arrive_expect_tx(bar, rows * D * uint32_t(sizeof(T)));
-    }
-    __syncthreads();
-    if (tid < rows) {
-      bulk_g2s(Vt + tid * D, V + size_t(ids[size_t(h) * k + t0 + tid]) * D,
-               D * uint32_t(sizeof(T)), bar);
-      e[tid] = exp(s64[size_t(h) * k + t0 + tid] * inv_sqrt_d - zo);
+  for (uint32_t t0 = 0; t0 < m; t0 += TR) {
+    if (t0) {  // further tiles (k > TR only)
+      rows = min(TR, m - t0);
+      __syncthreads();  // previous tile fully consumed
+      if (tid == 0) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(bar, rows * D * uint32_t(sizeof(T)));
+      }
+      __syncthreads();
+      for (uint32_t i = tid; i < rows; i += blockDim.x) {
+        bulk_g2s(Vt + size_t(i) * D, V + size_t(ids[size_t(h) * k + t0 + i]) * D,
+                 D * uint32_t(sizeof(T)), bar);
+        e[i] = exp(s64[size_t(h) * k + t0 + i] * inv_sqrt_d - zo);
+      }
     }
     mbar_wait(bar, phase);
     phase ^= 1u;
@@ -330,11 +354,6 @@ __global__ void __launch_bounds__(128)
     }
   }
   // W partial: fold the chunks (log-sum-exp), then merge() with Omega
-  double zw = -DBL_MAX;
-  for (uint32_t c = 0; c < C; ++c) zw = fmax(zw, part_m[(size_t(g) * C + c) * hpg + hl]);
-  double sw = 0.0;
-  for (uint32_t c = 0; c < C; ++c)
-    sw += exp(part_m[(size_t(g) * C + c) * hpg + hl] - zw) * part_s[(size_t(g) * C + c) * hpg + hl];
   const bool we = nW == 0, oe = m == 0;
   double gw = 1.0, go = 0.0;
   if (we) {
@@ -352,8 +371,7 @@ __global__ void __launch_bounds__(128)
     double ow = 0.0;
     if (!we) {
       for (uint32_t c = 0; c < C; ++c)
-        ow += exp(part_m[(size_t(g) * C + c) * hpg + hl] - zw) *
-              part_out[((size_t(g) * C + c) * hpg + hl) * D + j];
+        ow += wx[c] * part_out[((size_t(g) * C + c) * hpg + hl) * D + j];
       ow /= sw;
     }
     const double oo = oe ? 0.0 : acc[r] / so;
@@ -376,12 +394,15 @@ void launch_engine_attention_d(cudaStream_t st, const EngineAttn& a, int part) {
     RA_LAUNCH_CHECK();
     return;
   }
-  const size_t smem_o = 16 + kWC * D * sizeof(T) + kWC * 8;
+  // one Omega tile for k up to ~180 rows (the whole top-k in one TMA round)
+  const uint32_t TR = std::min<uint32_t>(std::max<uint32_t>(a.k, 1),
+                                         uint32_t((150u << 10) / (D * sizeof(T) + 8)));
+  const size_t smem_o = 16 + size_t(TR) * D * sizeof(T) + size_t(TR) * 8 + size_t(C) * 8;
   RA_CUDA(cudaFuncSetAttribute(k_omega_merge<D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem_o));
   k_omega_merge<D, T><<<a.H, 128, smem_o, st>>>(a.hkv, a.ids, a.s64, a.n_out, a.k, a.hpg, C,
                                                 a.nW, a.inv_sqrt_d, a.part_out, a.part_m,
-                                                a.part_s, a.out);
+                                                a.part_s, a.out, TR);
   RA_LAUNCH_CHECK();
 }
 
