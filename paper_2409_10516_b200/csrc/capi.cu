@@ -660,7 +660,9 @@ void record_timing(cudaEvent_t ev, cudaStream_t s) {
 }
 // run_head for every head (engine.cpp:69-101): search with Mask{W} ->
 // partial over W -> partial over Omega (scores reused) -> merge.
-void engine_enqueue(ra_engine* e, const float* q_dev) {
+// out_dev / ids_dev: where the attention output [H, d] f64 and the Omega
+// ids [H, k] go (the caller's device buffers, or the engine's own)
+void engine_enqueue(ra_engine* e, const float* q_dev, double* out_dev, uint32_t* ids_dev) {
   ra_ctx* ctx = e->ctx;
   cudaStream_t s = ctx->stream;
   const uint32_t H = e->H, d = e->d;
@@ -668,9 +670,9 @@ void engine_enqueue(ra_engine* e, const float* q_dev) {
   if (e->fast_attn) {
     const uint32_t C = uint32_t((e->n_static + 63) / 64);
     ea = EngineAttn{e->gkv.p, e->kvrefs.p, q_dev, e->w_ids.p, uint32_t(e->n_static), e->G, H,
-                    e->hpg, d, e->k, 1.0 / std::sqrt(double(d)), e->ids.p, e->scores64.p,
+                    e->hpg, d, e->k, 1.0 / std::sqrt(double(d)), ids_dev, e->scores64.p,
                     e->n_out.p, e->part.p, e->part.p + size_t(e->G) * std::max(C, 1u) * e->hpg * d,
-                    e->part.p + size_t(e->G) * std::max(C, 1u) * e->hpg * (d + 1), e->out.p,
+                    e->part.p + size_t(e->G) * std::max(C, 1u) * e->hpg * (d + 1), out_dev,
                     uint32_t(e->groups[0]->bf16_attn)};
     // fork: the W partials depend only on q, so they run beside the search
     RA_CUDA(cudaEventRecord(e->fork, s));
@@ -689,7 +691,7 @@ void engine_enqueue(ra_engine* e, const float* q_dev) {
     sa.k = e->k;
     sa.max_M = e->max_M;
     sa.bf16 = e->groups[0]->bf16;
-    sa.ids = e->ids.p;
+    sa.ids = ids_dev;
     sa.scores = e->scores.p;
     sa.scores64 = e->scores64.p;
     sa.n_out = e->n_out.p;
@@ -712,11 +714,11 @@ void engine_enqueue(ra_engine* e, const float* q_dev) {
   }
   launch_partial_attention_ex(s, e->kvrefs.p, d, H, q_dev, e->w_ids.p, 0, e->w_m.p, nullptr, 0,
                               e->ow.p, e->zw.p, e->sw.p, nullptr, 0, e->w_empty.p, e->flag.p);
-  launch_partial_attention_ex(s, e->kvrefs.p, d, H, q_dev, e->ids.p, e->k, e->n_out.p,
+  launch_partial_attention_ex(s, e->kvrefs.p, d, H, q_dev, ids_dev, e->k, e->n_out.p,
                               e->scores64.p, e->k, e->oo.p, e->zo.p, e->so.p, nullptr, 0,
                               e->o_empty.p, e->flag.p);
   launch_merge(s, H, d, e->ow.p, e->zw.p, e->sw.p, e->w_empty.p, e->oo.p, e->zo.p, e->so.p,
-               e->o_empty.p, e->out.p, nullptr, nullptr, e->flag.p);
+               e->o_empty.p, out_dev, nullptr, nullptr, e->flag.p);
   record_timing(e->ev[2], s);
 }
 }  // namespace
@@ -727,11 +729,8 @@ namespace {
 void step_device_ops(ra_engine* e, const float* q, double* out, uint32_t* omega,
                      uint64_t* scanned) {
   cudaStream_t s = e->ctx->stream;
-  engine_enqueue(e, q);
-  if (out)
-    RA_CUDA(cudaMemcpyAsync(out, e->out.p, size_t(e->H) * e->d * 8, cudaMemcpyDeviceToDevice, s));
-  if (omega && e->k)
-    RA_CUDA(cudaMemcpyAsync(omega, e->ids.p, size_t(e->H) * e->k * 4, cudaMemcpyDeviceToDevice, s));
+  // out and omega are written in place by the kernels (no copies)
+  engine_enqueue(e, q, out ? out : e->out.p, omega && e->k ? omega : e->ids.p);
   if (scanned)
     RA_CUDA(cudaMemcpyAsync(scanned, e->scanned.p, size_t(e->H) * 8, cudaMemcpyDeviceToDevice, s));
 }
@@ -740,7 +739,7 @@ void step_host_ops(ra_engine* e, const float* q, double* out, uint32_t* omega,
                    uint64_t* scanned) {
   cudaStream_t s = e->ctx->stream;
   RA_CUDA(cudaMemcpyAsync(e->q.p, q, size_t(e->H) * e->d * 4, cudaMemcpyHostToDevice, s));
-  engine_enqueue(e, e->q.p);
+  engine_enqueue(e, e->q.p, e->out.p, e->ids.p);
   if (out) RA_CUDA(cudaMemcpyAsync(out, e->out.p, size_t(e->H) * e->d * 8, cudaMemcpyDeviceToHost, s));
   if (omega && e->k)
     RA_CUDA(cudaMemcpyAsync(omega, e->ids.p, size_t(e->H) * e->k * 4, cudaMemcpyDeviceToHost, s));
