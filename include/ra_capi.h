@@ -225,8 +225,12 @@ void ra_engine_destroy(ra_engine* e);
  * [H][top_k] u32 (UINT32_MAX padded) and scanned [H] u64 may be NULL. */
 ra_status ra_engine_step_device(ra_engine* e, const float* q, double* out, uint32_t* omega,
                                 uint64_t* scanned);
-/* decode_step on HOST buffers: H2D of q, the step, D2H of out/omega/scanned,
- * synchronized. This is the drop-in call a CPU-side engine makes. */
+/* decode_step on HOST buffers: q in, out/omega/scanned back, synchronized.
+ * This is the drop-in call a CPU-side engine makes. When every buffer is
+ * page-locked host memory (cudaHostAlloc / cudaHostRegister / torch
+ * pin_memory) the kernels read q and write the results across the bus
+ * themselves (zero-copy, no separate copy operations; RA_NO_ZERO_COPY=1
+ * disables); otherwise q is copied in and the results copied out. */
 ra_status ra_engine_step_host(ra_engine* e, const float* q, double* out, uint32_t* omega,
                               uint64_t* scanned);
 /* device-side counters of the last step (for roofline accounting) */

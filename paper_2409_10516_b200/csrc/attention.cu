@@ -283,7 +283,8 @@ __global__ void __launch_bounds__(128)
                   const double* __restrict__ s64, const uint32_t* __restrict__ n_out,
                   uint32_t k, uint32_t hpg, uint32_t C, uint32_t nW, double inv_sqrt_d,
                   const double* __restrict__ part_out, const double* __restrict__ part_m,
-                  const double* __restrict__ part_s, double* __restrict__ out, uint32_t TR) {
+                  const double* __restrict__ part_s, double* __restrict__ out, uint32_t TR,
+                  uint32_t* __restrict__ ids_out) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t h = blockIdx.x, g = h / hpg, hl = h % hpg, tid = threadIdx.x;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
@@ -305,6 +306,8 @@ __global__ void __launch_bounds__(128)
   for (uint32_t i = tid; i < rows; i += blockDim.x)
     bulk_g2s(Vt + size_t(i) * D, V + size_t(ids[size_t(h) * k + i]) * D, D * uint32_t(sizeof(T)),
              bar);
+  if (ids_out)
+    for (uint32_t i = tid; i < k; i += blockDim.x) ids_out[size_t(h) * k + i] = ids[size_t(h) * k + i];
   // Omega max (scores are exact f64 search scores; z = s / sqrt(d))
   double zo = -DBL_MAX;
   for (uint32_t i = tid; i < m; i += blockDim.x) zo = fmax(zo, s64[size_t(h) * k + i] * inv_sqrt_d);
@@ -402,7 +405,7 @@ void launch_engine_attention_d(cudaStream_t st, const EngineAttn& a, int part) {
                                (int)smem_o));
   k_omega_merge<D, T><<<a.H, 128, smem_o, st>>>(a.hkv, a.ids, a.s64, a.n_out, a.k, a.hpg, C,
                                                 a.nW, a.inv_sqrt_d, a.part_out, a.part_m,
-                                                a.part_s, a.out, TR);
+                                                a.part_s, a.out, TR, a.ids_out);
   RA_LAUNCH_CHECK();
 }
 

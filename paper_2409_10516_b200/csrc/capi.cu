@@ -491,6 +491,7 @@ struct ra_engine {
   } sg[2];
   bool graphs_off = false;
   cudaStream_t cap_stream = nullptr;  // capture happens here (the legacy stream can't capture)
+  uint64_t* last_scanned = nullptr;   // where the last step's scanned went (device or mapped host)
   ra_ctx* ctx = nullptr;
   uint32_t H = 0, G = 0, d = 0, k = 0;
   uint64_t t = 0, n_pool = 0, n_static = 0;
@@ -662,8 +663,10 @@ void record_timing(cudaEvent_t ev, cudaStream_t s) {
 // partial over W -> partial over Omega (scores reused) -> merge.
 // out_dev / ids_dev: where the attention output [H, d] f64 and the Omega
 // ids [H, k] go (the caller's device buffers, or the engine's own)
-void engine_enqueue(ra_engine* e, const float* q_dev, double* out_dev, uint32_t* ids_dev) {
+void engine_enqueue(ra_engine* e, const float* q_dev, double* out_dev, uint32_t* ids_dev,
+                    uint64_t* scanned_dev, uint32_t* ids_copy = nullptr) {
   ra_ctx* ctx = e->ctx;
+  e->last_scanned = scanned_dev;
   cudaStream_t s = ctx->stream;
   const uint32_t H = e->H, d = e->d;
   EngineAttn ea{};
@@ -673,7 +676,7 @@ void engine_enqueue(ra_engine* e, const float* q_dev, double* out_dev, uint32_t*
                     e->hpg, d, e->k, 1.0 / std::sqrt(double(d)), ids_dev, e->scores64.p,
                     e->n_out.p, e->part.p, e->part.p + size_t(e->G) * std::max(C, 1u) * e->hpg * d,
                     e->part.p + size_t(e->G) * std::max(C, 1u) * e->hpg * (d + 1), out_dev,
-                    uint32_t(e->groups[0]->bf16_attn)};
+                    uint32_t(e->groups[0]->bf16_attn), ids_copy};
     // fork: the W partials depend only on q, so they run beside the search
     RA_CUDA(cudaEventRecord(e->fork, s));
     RA_CUDA(cudaStreamWaitEvent(e->aux, e->fork, 0));
@@ -695,14 +698,14 @@ void engine_enqueue(ra_engine* e, const float* q_dev, double* out_dev, uint32_t*
     sa.scores = e->scores.p;
     sa.scores64 = e->scores64.p;
     sa.n_out = e->n_out.p;
-    sa.scanned = e->scanned.p;
+    sa.scanned = scanned_dev;
     sa.truncated = e->truncated.p;
     sa.expanded = e->expanded.p;
     sa.dbg = e->dbg.p;
     launch_graph_search(ctx, sa, e->max_n, e->search_scratch.p);
   } else {
     RA_CUDA(cudaMemsetAsync(e->n_out.p, 0, H * 4, s));
-    RA_CUDA(cudaMemsetAsync(e->scanned.p, 0, H * 8, s));
+    RA_CUDA(cudaMemsetAsync(scanned_dev, 0, H * 8, s));
     RA_CUDA(cudaMemsetAsync(e->expanded.p, 0, H * 4, s));
   }
   record_timing(e->ev[1], s);
@@ -730,7 +733,7 @@ void step_device_ops(ra_engine* e, const float* q, double* out, uint32_t* omega,
                      uint64_t* scanned) {
   cudaStream_t s = e->ctx->stream;
   // out and omega are written in place by the kernels (no copies)
-  engine_enqueue(e, q, out ? out : e->out.p, omega && e->k ? omega : e->ids.p);
+  engine_enqueue(e, q, out ? out : e->out.p, omega && e->k ? omega : e->ids.p, e->scanned.p);
   if (scanned)
     RA_CUDA(cudaMemcpyAsync(scanned, e->scanned.p, size_t(e->H) * 8, cudaMemcpyDeviceToDevice, s));
 }
@@ -738,8 +741,34 @@ void step_device_ops(ra_engine* e, const float* q, double* out, uint32_t* omega,
 void step_host_ops(ra_engine* e, const float* q, double* out, uint32_t* omega,
                    uint64_t* scanned) {
   cudaStream_t s = e->ctx->stream;
+  // pinned (page-locked, device-mapped) host buffers: the kernels read q
+  // and write out / Omega / scanned across the bus themselves, so the step
+  // has no separate copy operations; pageable buffers go through copies
+  static const bool zc_off = std::getenv("RA_NO_ZERO_COPY") != nullptr;
+  auto mapped = [](const void* p) -> void* {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+  };
+  if (!zc_off) {
+    void* qd = mapped(q);
+    void* od = out ? mapped(out) : e->out.p;
+    void* id = omega && e->k ? mapped(omega) : e->ids.p;
+    void* sd = scanned ? mapped(scanned) : e->scanned.p;
+    if (qd && od && id && sd && e->fast_attn) {
+      // Omega ids stay in HBM for the attention; its kernel also writes
+      // them to the caller's buffer
+      engine_enqueue(e, static_cast<const float*>(qd), static_cast<double*>(od), e->ids.p,
+                     static_cast<uint64_t*>(sd),
+                     id == e->ids.p ? nullptr : static_cast<uint32_t*>(id));
+      return;
+    }
+  }
   RA_CUDA(cudaMemcpyAsync(e->q.p, q, size_t(e->H) * e->d * 4, cudaMemcpyHostToDevice, s));
-  engine_enqueue(e, e->q.p, e->out.p, e->ids.p);
+  engine_enqueue(e, e->q.p, e->out.p, e->ids.p, e->scanned.p);
   if (out) RA_CUDA(cudaMemcpyAsync(out, e->out.p, size_t(e->H) * e->d * 8, cudaMemcpyDeviceToHost, s));
   if (omega && e->k)
     RA_CUDA(cudaMemcpyAsync(omega, e->ids.p, size_t(e->H) * e->k * 4, cudaMemcpyDeviceToHost, s));
@@ -865,7 +894,8 @@ ra_status ra_engine_last_stats(ra_engine* e, uint64_t* total_scanned, uint64_t* 
     DeviceGuard dg(e->ctx->device);
     std::vector<uint64_t> sc(e->H);
     std::vector<uint32_t> ex(e->H);
-    RA_CUDA(cudaMemcpyAsync(sc.data(), e->scanned.p, e->H * 8, cudaMemcpyDeviceToHost, e->ctx->stream));
+    RA_CUDA(cudaMemcpyAsync(sc.data(), e->last_scanned ? e->last_scanned : e->scanned.p, e->H * 8,
+                            cudaMemcpyDefault, e->ctx->stream));
     RA_CUDA(cudaMemcpyAsync(ex.data(), e->expanded.p, e->H * 4, cudaMemcpyDeviceToHost, e->ctx->stream));
     RA_CUDA(cudaStreamSynchronize(e->ctx->stream));
     if (total_scanned) *total_scanned = std::accumulate(sc.begin(), sc.end(), uint64_t(0));

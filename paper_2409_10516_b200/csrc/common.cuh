@@ -270,6 +270,7 @@ struct EngineAttn {
   double* part_s;
   double* out;           // [H][d]
   uint32_t bf16;         // K/V read from the groups' bf16 copies
+  uint32_t* ids_out = nullptr;  // optional second home of the Omega ids (caller's buffer)
 };
 bool engine_attention_supported(uint32_t d);
 size_t engine_attention_part_doubles(uint32_t G, uint32_t hpg, uint32_t nW, uint32_t d);
