@@ -15,6 +15,10 @@
 #include <set>
 #include <cstring>
 #include <memory>
+#include <numeric>
+#include <optional>
+#include <span>
+#include <algorithm>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -502,6 +506,93 @@ int ref_build_report(const char* manifest_path, const char* out_dir, int kind, u
     if (!out) throw std::runtime_error("write failed");
     *checks = n_checks;
     *failures = n_fail;
+  });
+}
+
+// recall_sweep + SweepReport::to_csv / to_jsonl (diagnostics.cpp:132-225)
+// restated over the reference library (diagnostics.cpp itself needs Eigen
+// LLT / HouseholderQR for its Mahalanobis parts, which the shim lacks).
+// kind: 0 flat, 1 ivf, 2 oodgraph. Writes the CSV then the JSONL, each
+// NUL-terminated, into buf (cap bytes).
+int ref_recall_sweep(const float* keys, uint64_t n, uint32_t d, const float* pq, uint64_t npq,
+                     const float* dq, uint64_t nq, int kind, const uint32_t* grid, uint32_t ngrid,
+                     uint64_t k, uint32_t nlist, uint64_t seed, uint32_t iters, uint32_t nprobe,
+                     uint32_t k_train, uint32_t max_degree, uint32_t efc, uint32_t window,
+                     int n_threads, char* buf, uint64_t cap) {
+  return guard([&] {
+    auto ks = make_set(Role::Key, keys, n, d);
+    VectorSet pre(Role::Query, npq, d), dec(Role::Query, nq, d);
+    if (npq) std::memcpy(pre.data.data(), pq, sizeof(float) * npq * d);
+    if (nq) std::memcpy(dec.data.data(), dq, sizeof(float) * nq * d);
+    if (nq == 0) throw std::invalid_argument("no decode queries");
+    if (k < 1 || k > n) throw std::invalid_argument("k out of range");
+    auto recall = [](std::span<const uint32_t> got, std::span<const uint32_t> truth) {
+      std::vector<uint32_t> sorted(truth.begin(), truth.end());
+      std::sort(sorted.begin(), sorted.end());
+      size_t hits = 0;
+      for (uint32_t id : got)
+        if (std::binary_search(sorted.begin(), sorted.end(), id)) ++hits;
+      return double(hits) / double(truth.size());
+    };
+    FlatIndex flat(ks);
+    std::vector<std::vector<uint32_t>> truth(nq);
+    for (uint64_t i = 0; i < nq; ++i) truth[i] = flat.search(dec.row(i), k).ids;
+    struct Row { std::string kind; uint32_t param; double rec, scan; uint64_t nq; };
+    std::vector<Row> rows;
+    auto add_rows = [&](const SearchIndex& idx, std::vector<uint32_t> g) {
+      for (uint32_t param : g) {
+        std::vector<double> rec(nq), scan(nq);
+        for (uint64_t i = 0; i < nq; ++i) {
+          auto r = idx.search(dec.row(i), k, {},
+                              param ? std::optional<uint32_t>(param) : std::nullopt);
+          rec[i] = recall(r.ids, truth[i]);
+          scan[i] = double(r.scanned) / double(n);
+        }
+        rows.push_back({std::string(idx.kind()), param,
+                        std::accumulate(rec.begin(), rec.end(), 0.0) / double(nq),
+                        std::accumulate(scan.begin(), scan.end(), 0.0) / double(nq), nq});
+      }
+    };
+    std::vector<uint32_t> gv(grid, grid + ngrid);
+    if (kind == 0) {
+      add_rows(flat, {0u});
+    } else {
+      if (gv.empty()) throw std::invalid_argument("empty parameter grid");
+      for (uint32_t g : gv)
+        if (g < 1) throw std::invalid_argument("grid values must be >= 1");
+      if (kind == 1) {
+        IVFBuildParams p;
+        p.nlist = nlist, p.seed = seed, p.iters = iters, p.default_nprobe = nprobe;
+        auto idx = ivf_build(ks, p);
+        add_rows(*idx, gv);
+      } else {
+        OODGraphBuildParams p;
+        p.k_train = k_train, p.max_degree = max_degree, p.ef_construction = efc;
+        p.edge_window = window;
+        auto idx = ood_build(ks, pre, p, n_threads);
+        add_rows(*idx, gv);
+      }
+    }
+    auto fmt = [](double v) {
+      char b[40];
+      std::snprintf(b, sizeof b, "%.10g", v);
+      return std::string(b);
+    };
+    std::string csv = "index_kind,param,recall_at_k,scan_fraction,n_queries\n", jl;
+    for (const auto& r : rows) {
+      csv += r.kind + ',' + std::to_string(r.param) + ',' + fmt(r.rec) + ',' + fmt(r.scan) + ',' +
+             std::to_string(r.nq) + '\n';
+      nlohmann::ordered_json j;
+      j["index_kind"] = r.kind;
+      j["param"] = r.param;
+      j["recall_at_k"] = r.rec;
+      j["scan_fraction"] = r.scan;
+      j["n_queries"] = r.nq;
+      jl += j.dump() + '\n';
+    }
+    if (csv.size() + jl.size() + 2 > cap) throw std::runtime_error("buffer too small");
+    std::memcpy(buf, csv.c_str(), csv.size() + 1);
+    std::memcpy(buf + csv.size() + 1, jl.c_str(), jl.size() + 1);
   });
 }
 
