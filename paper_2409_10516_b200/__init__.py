@@ -13,5 +13,6 @@ from .api import (  # noqa: F401
     SearchResult, default_context, empty_partial, merge, merge_gammas, ood_build,
     partial_attention, search_batch, static_partition, flat_build, engine_init)
 from .report import VerifyLog, build_run  # noqa: F401
+from .diagnostics import SweepParams, SweepReport, recall_at_k, recall_sweep  # noqa: F401
 
 __version__ = lib.ra_version().decode()
