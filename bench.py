@@ -325,7 +325,8 @@ def main():
         "e2e": {"value": round(ms_e2e, 4), "unit": "ms/token",
                 "h2d_bytes_per_step": Hl * 128 * 4,
                 "d2h_bytes_per_step": Hl * 128 * 8 + Hl * max(eng.k, 1) * 4 + Hl * 8},
-        "gpu_launches": 3 * a.steps,  # W partial, search, Omega partial + merge
+        # fused step: 1 kernel (search + W / Omega partials + merge), else 3
+        "gpu_launches": eng.kernels_per_step() * a.steps,
         "roofline": {"bound": "hbm", "kernel": "k_graph_search_pipe (latency mode)",
                      "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 5), "peak_source": peak_kind,

@@ -239,6 +239,10 @@ ra_status ra_engine_last_stats(ra_engine* e, uint64_t* total_scanned,
 /* CUDA-event durations of the last step's search kernel and of its
  * attention + merge kernels (recorded on the ctx stream). Synchronizes. */
 ra_status ra_engine_last_timing(ra_engine* e, float* search_ms, float* attention_ms);
+/* Kernel launches per decode step: 1 when the search kernel also computes the
+ * attention (fused step: f32 groups, latency-mode batch), else 3 (W partials,
+ * search, Omega partial + merge). RA_FUSED_ATTN=0 disables fusion. */
+uint32_t ra_engine_kernels_per_step(const ra_engine* e);
 /* Profiling aid: search-kernel counters of the last step summed over heads:
  * {rounds, cycles pre-expanding, cycles committing, commits, commit-phase
  * cycles in argmax / stop test / packet apply / add+compact / select, 0,0,0}. */

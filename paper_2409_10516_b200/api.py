@@ -699,6 +699,10 @@ class Engine:
                                        sc.ctypes.data))
         return out, om[:, : self.k], sc
 
+    def kernels_per_step(self) -> int:
+        """1 for the fused step (search + attention in one kernel), else 3."""
+        return int(lib.ra_engine_kernels_per_step(self.h))
+
     def last_timing(self):
         """(search_ms, attention_ms) of the last step, CUDA events on the ctx stream."""
         a, b = C.c_float(), C.c_float()

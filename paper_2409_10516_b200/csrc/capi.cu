@@ -517,6 +517,12 @@ struct ra_engine {
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   // fast attention path: W partials on a side stream overlapping the search
   bool fast_attn = false;
+  // fused decode step: the search kernel also computes the W partials (idle
+  // helpers) and the Omega partial + merge (its tail); one launch per step
+  bool fused = false;
+  uint32_t fa_nchunk = 0;
+  DevBuf<const float*> hvals;  // [H] each head's V rows
+  DevBuf<double> fa_chunk;     // [H][nchunk][d + 2]
   cudaStream_t aux = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
   DevBuf<KVRef> gkv;
@@ -619,6 +625,24 @@ ra_status ra_engine_create(ra_ctx* ctx, ra_kv* const* groups, uint32_t n_groups,
     e->flag.alloc(1);
     for (auto* b : {&e->ow, &e->oo, &e->out}) b->alloc(size_t(H) * d);
     for (auto* b : {&e->zw, &e->sw, &e->zo, &e->so}) b->alloc(H);
+    {
+      SearchArgs probe{};
+      probe.B = H, probe.d = d, probe.max_M = e->max_M, probe.bf16 = e->groups[0]->bf16;
+      static const bool fa_off = [] {
+        const char* v = std::getenv("RA_FUSED_ATTN");
+        return v && v[0] == '0';
+      }();
+      e->fused = !fa_off && e->fast_attn && !e->groups[0]->bf16 && !e->groups[0]->bf16_attn &&
+                 e->n_pool > 0 && search_fuses_attention(ctx, probe, e->max_n);
+      if (e->fused) {
+        const uint32_t rows = std::max<uint32_t>(e->max_M, 1);  // the kernel's tile rows
+        e->fa_nchunk = uint32_t((ns + rows - 1) / rows);
+        std::vector<const float*> hv(H);
+        for (uint32_t h = 0; h < H; ++h) hv[h] = head_graphs[h]->kv->values.p;
+        up(e->hvals, hv);
+        e->fa_chunk.alloc(std::max<size_t>(size_t(H) * e->fa_nchunk * (d + 2), 1));
+      }
+    }
     const size_t sb = search_scratch_bytes(ctx, H, e->max_n, d);
     e->search_scratch.alloc(sb);
     for (auto& ev : e->ev) RA_CUDA(cudaEventCreate(&ev));
@@ -670,6 +694,31 @@ void engine_enqueue(ra_engine* e, const float* q_dev, double* out_dev, uint32_t*
   cudaStream_t s = ctx->stream;
   const uint32_t H = e->H, d = e->d;
   EngineAttn ea{};
+  if (e->fused) {  // one launch: search + W partials + Omega partial + merge
+    record_timing(e->ev[0], s);
+    SearchArgs sa{};
+    sa.desc = e->desc.p;
+    sa.q = q_dev;
+    sa.mask_bits = e->n_static ? e->w_bits.p : nullptr;
+    sa.B = H;
+    sa.d = d;
+    sa.k = e->k;
+    sa.max_M = e->max_M;
+    sa.ids = ids_copy ? ids_copy : ids_dev;
+    sa.scores = e->scores.p;
+    sa.scores64 = e->scores64.p;
+    sa.n_out = e->n_out.p;
+    sa.scanned = scanned_dev;
+    sa.truncated = e->truncated.p;
+    sa.expanded = e->expanded.p;
+    sa.dbg = e->dbg.p;
+    sa.fa = {e->hvals.p, e->w_ids.p, uint32_t(e->n_static), e->fa_nchunk,
+             1.0 / std::sqrt(double(d)), out_dev, e->fa_chunk.p};
+    launch_graph_search(ctx, sa, e->max_n, e->search_scratch.p);
+    record_timing(e->ev[1], s);
+    record_timing(e->ev[2], s);
+    return;
+  }
   if (e->fast_attn) {
     const uint32_t C = uint32_t((e->n_static + 63) / 64);
     ea = EngineAttn{e->gkv.p, e->kvrefs.p, q_dev, e->w_ids.p, uint32_t(e->n_static), e->G, H,
@@ -901,6 +950,10 @@ ra_status ra_engine_last_stats(ra_engine* e, uint64_t* total_scanned, uint64_t* 
     if (total_scanned) *total_scanned = std::accumulate(sc.begin(), sc.end(), uint64_t(0));
     if (total_expanded) *total_expanded = std::accumulate(ex.begin(), ex.end(), uint64_t(0));
   });
+}
+
+uint32_t ra_engine_kernels_per_step(const ra_engine* e) {
+  return !e ? 0u : e->fused ? 1u : e->fast_attn ? 3u : 4u;
 }
 
 ra_status ra_engine_last_timing(ra_engine* e, float* search_ms, float* attention_ms) {

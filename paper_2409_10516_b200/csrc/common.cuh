@@ -219,6 +219,17 @@ struct SearchArgs {
   uint32_t* vis_global;
   uint32_t flags;  // profiling switches (RA_PIPE_FLAGS): 1 = helpers idle
   uint32_t bf16;   // every desc[b].keys16 is set: score from the bf16 rows
+  // fused decode attention (latency-mode pipe kernel, f32 groups): idle
+  // helpers compute the W partials in chunks during the search, the CTA
+  // computes the Omega partial and the merge after it. out == nullptr: off.
+  struct FusedAttn {
+    const float* const* values;  // [B] the head's V rows (n x d f32)
+    const uint32_t* W;           // static ids, ascending
+    uint32_t nW, nchunk;         // nchunk = ceil(nW / rows per chunk)
+    double inv_sqrt_d;
+    double* out;                 // [B][d] attention output
+    double* chunk;               // scratch [B][nchunk][d + 2]: (out, max, expsum)
+  } fa;
 };
 
 // Returns bytes of scratch needed for (B, max_n, d); then launches.
@@ -229,6 +240,10 @@ void launch_graph_search(ra_ctx* ctx, SearchArgs a, uint32_t max_n, uint8_t* scr
 size_t search_pipe_scratch_bytes(uint32_t B, uint32_t max_n);
 bool launch_graph_search_pipe(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n,
                               uint8_t* scratch, int mode);
+// whether launch_graph_search will run a.fa (the fused attention) for this
+// batch: latency-mode pipe kernel, f32 rows, supported shape
+bool search_fuses_attention(const ra_ctx* ctx, const SearchArgs& a, uint32_t max_n);
+bool pipe_latency_supported(const ra_ctx* ctx, uint32_t d, uint32_t max_M, uint32_t max_n);
 
 void launch_mask_bitset(cudaStream_t s, const uint32_t* mask, uint64_t mask_n, uint32_t* bits,
                         uint64_t words);

@@ -1091,6 +1091,13 @@ int search_variant() {
   return v;
 }
 
+bool search_fuses_attention(const ra_ctx* ctx, const SearchArgs& a, uint32_t max_n) {
+  const int v = search_variant();
+  if (!(v == 0 || v == 4) || a.bf16 || a.B == 0) return false;
+  if (v == 0 && a.B > 2u * uint32_t(ctx->num_sms)) return false;  // throughput mode
+  return pipe_latency_supported(ctx, a.d, a.max_M, max_n);
+}
+
 void launch_graph_search(ra_ctx* ctx, SearchArgs a, uint32_t max_n, uint8_t* scratch) {
   if (a.B == 0) return;
   const int variant = search_variant();

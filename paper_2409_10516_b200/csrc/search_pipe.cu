@@ -256,6 +256,110 @@ struct Arr {  // (key, id) array: k u64[cap] then id u32[cap]
 // with inline expansions (key rows straight into registers), kTW queries
 // per CTA, visited set in HBM/L2; for batches that fill the GPU many times.
 // BF: key rows are read from the group's bf16 copy (half the bytes)
+// Omega partial over the sorted pool's top `m` (exact search scores, rank
+// order) + the W chunks folded in chunk order + merge (attention.cpp:102-157,
+// the same arithmetic as k_omega_merge). All threads of the CTA; the V rows
+// are staged in the (free) tile area behind the sorted array.
+template <int D>
+__device__ void fused_attention_tail(const SearchArgs& a, const PipeLayout& lay, uint32_t b,
+                                     const Arr& A, uint32_t p2, bool fin_smem, uint32_t m,
+                                     uint8_t* smem) {
+  const uint32_t tid = threadIdx.x, nth = blockDim.x;
+  const auto& fa = a.fa;
+  constexpr uint32_t CB = 16;  // W chunk partials staged per round
+  // a fresh mbarrier in ctrl[14..15] (unused words; the warps' own are left alone)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + PipeLayout::kCtrl + 14 * 4);
+  const size_t a_bytes = fin_smem ? ((PipeLayout::arr_bytes(p2) + 15) & ~size_t(15)) : 0;
+  uint8_t* base = smem + lay.tiles_off() + a_bytes;
+  double* red = reinterpret_cast<double*>(base);         // [8] block max
+  double* wx = red + 8;                                  // [CB] chunk weights
+  double* chs = wx + CB;                                 // [CB][D + 2] staged partials
+  double* e = chs + size_t(CB) * (D + 2);                // [R]
+  const size_t head = size_t(8 + CB + size_t(CB) * (D + 2)) * 8;
+  const size_t avail = size_t(kPW) * lay.tile_bytes() - a_bytes - head;
+  // rows per pass (>= 8, see fin_smem); even, so Vt stays 16-B aligned
+  const uint32_t R = uint32_t(avail / (size_t(D) * 4 + 8)) & ~1u;
+  float* Vt = reinterpret_cast<float*>(e + R);  // [R][D]
+  const float* V = fa.values[b];
+  const double* ch = fa.chunk + size_t(b) * fa.nchunk * (D + 2);
+  const double zo = m ? okey_inv(A.k[0]) * fa.inv_sqrt_d : -DBL_MAX;  // sorted: the max
+  if (tid == 0) mbar_init(bar);
+  __syncthreads();
+  uint32_t rows = min(R, m), phase = 0;
+  // the first pass's V rows are requested first; the W fold runs under them
+  if (tid == 0) {
+    fence_proxy_async();
+    mbar_arrive_expect_tx(bar, rows * uint32_t(D) * 4u);
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < rows; i += nth) {
+    bulk_g2s(Vt + size_t(i) * D, V + size_t(A.id[i]) * D, D * 4u, bar);
+    e[i] = exp(okey_inv(A.k[i]) * fa.inv_sqrt_d - zo);
+  }
+  // W: max over the chunk maxima (one parallel load), then the chunks in order
+  double zw = -DBL_MAX;
+  for (uint32_t c = tid; c < fa.nchunk; c += nth) zw = fmax(zw, ch[size_t(c) * (D + 2) + D]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) zw = fmax(zw, __shfl_xor_sync(kFull, zw, o));
+  if ((tid & 31) == 0) red[tid >> 5] = zw;
+  __syncthreads();
+  zw = red[0];
+  for (uint32_t w = 1; w < nth / 32; ++w) zw = fmax(zw, red[w]);
+  double sw = 0.0, ow = 0.0;
+  const uint32_t j = tid;  // this thread's output dimension (j < D)
+  for (uint32_t c0 = 0; c0 < fa.nchunk; c0 += CB) {
+    const uint32_t cn = min(CB, fa.nchunk - c0);
+    for (uint32_t x = tid; x < cn * (D + 2); x += nth) chs[x] = ch[size_t(c0) * (D + 2) + x];
+    __syncthreads();
+    if (tid < cn) wx[tid] = exp(chs[size_t(tid) * (D + 2) + D] - zw);
+    __syncthreads();
+    for (uint32_t c = 0; c < cn; ++c) {  // chunk order
+      sw += wx[c] * chs[size_t(c) * (D + 2) + D + 1];
+      if (j < uint32_t(D)) ow += wx[c] * chs[size_t(c) * (D + 2) + j];
+    }
+    __syncthreads();  // chs reused
+  }
+  // Omega: sum e_i v_i in rank order, pass by pass
+  double acc = 0.0, so = 0.0;
+  for (uint32_t t0 = 0; t0 < m; t0 += R) {
+    if (t0) {
+      rows = min(R, m - t0);
+      __syncthreads();  // previous pass consumed
+      if (tid == 0) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(bar, rows * uint32_t(D) * 4u);
+      }
+      __syncthreads();
+      for (uint32_t i = tid; i < rows; i += nth) {
+        bulk_g2s(Vt + size_t(i) * D, V + size_t(A.id[t0 + i]) * D, D * 4u, bar);
+        e[i] = exp(okey_inv(A.k[t0 + i]) * fa.inv_sqrt_d - zo);
+      }
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    __syncthreads();  // e[] visible
+    for (uint32_t i = 0; i < rows; ++i) {
+      const double ei = e[i];
+      so += ei;
+      if (j < uint32_t(D)) acc = fma(ei, (double)Vt[size_t(i) * D + j], acc);
+    }
+  }
+  if (j >= uint32_t(D)) return;
+  const bool we = fa.nW == 0, oe = m == 0;
+  double gw = 1.0, go = 0.0;
+  if (we) {
+    gw = 0.0, go = 1.0;
+  } else if (!oe) {
+    const double zref = fmax(zw, zo);
+    const double ew = exp(zw - zref) * sw, eo = exp(zo - zref) * so;
+    gw = ew / (ew + eo);
+    go = eo / (ew + eo);
+  }
+  if (!we) ow /= sw;
+  const double oo = oe ? 0.0 : acc / so;
+  fa.out[size_t(b) * D + j] = we ? oo : (oe ? ow : gw * ow + go * oo);
+}
+
 template <int D, bool VS, bool TP, bool BF>
 __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     k_graph_search_pipe(SearchArgs a, PipeLayout lay, uint32_t spill_cap) {
@@ -819,7 +923,11 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     } else {
       ctrl[0] = 1;  // helpers stop
       __syncwarp();
-      fin_smem = size_t(p2) * 12 <= size_t(kPW) * lay.tile_bytes();
+      // (fused attention: leave room for >= 8 staged V rows behind the array)
+      fin_smem = PipeLayout::arr_bytes(p2) + 16 +
+                     (a.fa.out && !BF ? (24 + 16 * (size_t(D) + 2)) * 8 + 8 * (size_t(D) * 4 + 8)
+                                      : 0) <=
+                 size_t(kPW) * lay.tile_bytes();
       if (lane == 0) {
         ctrl[4] = p2;
         ctrl[5] = fin_smem;
@@ -967,6 +1075,57 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
       sl = __shfl_sync(kFull, sl, 0);
       return __shfl_sync(kFull, ok, 0);
     };
+    // fused attention: one chunk of W (the tile's MT rows) -> its partial
+    // (sum e*v, max, sum e) in the head's scratch row, in W order
+    const bool fused = !BF && a.fa.out != nullptr;
+    auto wchunk = [&](uint32_t c) {
+      const uint32_t r0 = c * lay.MT, rows = min(lay.MT, a.fa.nW - r0);
+      const float* V = a.fa.values[b];
+      const uint32_t wid = lane < rows ? a.fa.W[r0 + lane] : 0u;
+      fence_proxy_async();
+      if (lane == 0) mbar_arrive_expect_tx(bar, rows * uint32_t(D) * 4u);
+      __syncwarp();
+      if (lane < rows) bulk_g2s(tile + size_t(lane) * RS, keys + size_t(wid) * D, D * 4u, bar);
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+      const double z = lane < rows ? row_dot<D>(qd, tile + size_t(lane) * RS) * a.fa.inv_sqrt_d
+                                   : -DBL_MAX;
+      double m = z;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(kFull, m, o));
+      const double e = lane < rows ? exp(z - m) : 0.0;
+      __syncwarp();  // every lane is done with the key rows
+      fence_proxy_async();
+      if (lane == 0) mbar_arrive_expect_tx(bar, rows * uint32_t(D) * 4u);
+      __syncwarp();
+      if (lane < rows) bulk_g2s(tile + size_t(lane) * RS, V + size_t(wid) * D, D * 4u, bar);
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+      constexpr int kJ = (D + 31) / 32;
+      double acc[kJ];
+#pragma unroll
+      for (int t = 0; t < kJ; ++t) acc[t] = 0.0;
+      double se = 0.0;
+      for (uint32_t i = 0; i < rows; ++i) {  // W order (partial_attention, attention.cpp:102-128)
+        const double ei = __shfl_sync(kFull, e, i);
+        se += ei;
+#pragma unroll
+        for (int t = 0; t < kJ; ++t)
+          if (lane + 32 * t < uint32_t(D))
+            acc[t] = fma(ei, (double)tile[size_t(i) * RS + lane + 32 * t], acc[t]);
+      }
+      double* dst = a.fa.chunk + (size_t(b) * a.fa.nchunk + c) * (D + 2);
+#pragma unroll
+      for (int t = 0; t < kJ; ++t)
+        if (lane + 32 * t < uint32_t(D)) dst[lane + 32 * t] = acc[t];
+      if (lane == 0) dst[D] = m, dst[D + 1] = se;
+      __syncwarp();
+    };
+    auto next_chunk = [&]() -> uint32_t {
+      uint32_t c = 0;
+      if (lane == 0) c = atomicAdd(const_cast<uint32_t*>(ctrl) + 13, 1u);
+      return __shfl_sync(kFull, c, 0);
+    };
     for (;;) {
       if (ctrl[0]) break;
       // the frontier's best `pick` nodes, best first: a tournament over the
@@ -1033,6 +1192,14 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         }
       }
       if (got == kSentinel) {
+        // idle: a chunk of W attention (by the last helpers only, so the
+        // others stay responsive to hints)
+        if (fused && ctrl[13] < a.fa.nchunk &&
+            warp + ((a.flags >> 19) & 7u ? (a.flags >> 19) & 7u : kPW) >= kPW) {
+          const uint32_t c = next_chunk();
+          if (c < a.fa.nchunk) wchunk(c);
+          continue;
+        }
         __nanosleep(64);
         continue;
       }
@@ -1095,6 +1262,8 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         ++n_chain;
       }
     }
+    if (fused)  // W chunks nobody got to during the search
+      for (uint32_t c = next_chunk(); c < a.fa.nchunk; c = next_chunk()) wchunk(c);
     if (lane == 0) {
       atomicAdd(const_cast<uint32_t*>(ctrl) + 8, n_exp);
       atomicAdd(const_cast<uint32_t*>(ctrl) + 9, n_chain);
@@ -1139,6 +1308,9 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     a.n_out[b] = take;
     a.truncated[b] = take < k;
   }
+  if constexpr (!BF) {
+    if (a.fa.out) fused_attention_tail<D>(a, lay, b, A, p2, fin_smem, take, smem);
+  }
 }
 
 template <int D, bool BF>
@@ -1158,6 +1330,7 @@ bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* sc
   cur += (size_t(a.B) * 2 * PipeLayout::arr_bytes(spill_cap) + 255) & ~size_t(255);
   s.vis_global = reinterpret_cast<uint32_t*>(cur);
   if (tp) {
+    s.fa.out = nullptr;
     PipeLayout lay{uint32_t(D), std::max<uint32_t>(a.max_M, 1), (max_n + 31) / 32, 0, 256};
     const size_t bytes = kTW * lay.tp_warp_bytes();
     auto kern = k_graph_search_pipe<D, false, true, BF>;
@@ -1166,6 +1339,7 @@ bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* sc
     RA_LAUNCH_CHECK();
     return true;
   }
+  if (BF) s.fa.out = nullptr;  // fused attention reads f32 rows only
   PipeLayout lay{uint32_t(D), std::max<uint32_t>(a.max_M, 1), (max_n + 31) / 32, 1, 0};
   if (lay.bytes() + PipeLayout::arr_bytes(512) * 2 > budget) lay.vis_smem = 0;
   const size_t fixed = lay.bytes();
@@ -1182,6 +1356,15 @@ bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* sc
 }
 
 }  // namespace
+
+bool pipe_latency_supported(const ra_ctx* ctx, uint32_t d, uint32_t max_M, uint32_t max_n) {
+  if (max_M > 32 || max_M == 0) return false;
+  if (d != 8 && d != 16 && d != 32 && d != 64 && d != 128) return false;
+  const size_t budget = ctx->smem_optin ? ctx->smem_optin : 227 * 1024;
+  PipeLayout lay{d, max_M, (max_n + 31) / 32, 1, 0};
+  if (lay.bytes() + PipeLayout::arr_bytes(512) * 2 > budget) lay.vis_smem = 0;
+  return lay.bytes() + PipeLayout::arr_bytes(256) * 2 <= budget;
+}
 
 size_t search_pipe_scratch_bytes(uint32_t B, uint32_t max_n) {
   uint32_t p2 = 32;
