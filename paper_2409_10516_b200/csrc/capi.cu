@@ -782,9 +782,9 @@ void step_device_ops(ra_engine* e, const float* q, double* out, uint32_t* omega,
                      uint64_t* scanned) {
   cudaStream_t s = e->ctx->stream;
   // out and omega are written in place by the kernels (no copies)
-  engine_enqueue(e, q, out ? out : e->out.p, omega && e->k ? omega : e->ids.p, e->scanned.p);
-  if (scanned)
-    RA_CUDA(cudaMemcpyAsync(scanned, e->scanned.p, size_t(e->H) * 8, cudaMemcpyDeviceToDevice, s));
+  engine_enqueue(e, q, out ? out : e->out.p, omega && e->k ? omega : e->ids.p,
+                 scanned ? scanned : e->scanned.p);
+  (void)s;
 }
 
 void step_host_ops(ra_engine* e, const float* q, double* out, uint32_t* omega,

@@ -1348,8 +1348,15 @@ bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* sc
   if (lay.bytes() > budget) return false;
   auto kern = lay.vis_smem ? k_graph_search_pipe<D, true, false, BF>
                            : k_graph_search_pipe<D, false, false, BF>;
-  RA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(lay.bytes())));
+  {  // the attribute only ever grows; set it when a launch needs more
+    static int set_bytes[64][2] = {};  // per device (the attribute is per device)
+    int& have = set_bytes[ctx->device & 63][lay.vis_smem ? 1 : 0];
+    if (int(lay.bytes()) > have) {
+      RA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(lay.bytes())));
+      have = int(lay.bytes());
+    }
+  }
   kern<<<a.B, kPW * 32, lay.bytes(), ctx->stream>>>(s, lay, spill_cap);
   RA_LAUNCH_CHECK();
   return true;
