@@ -215,7 +215,8 @@ __device__ __forceinline__ void warp_best(uint64_t& k, uint32_t& id) {
 
 struct PipeLayout {
   uint32_t D, MT, vis_words, vis_smem, capO;
-  static constexpr size_t kBars = 0, kCtrl = 64, kPubK = 128, kPubId = 384, kSlotW = 512,
+  static constexpr size_t kBars = 0, kCtrl = (size_t(kPW) * 8 + 63) / 64 * 64,  // one mbarrier per warp
+                          kPubK = kCtrl + 64, kPubId = kPubK + 256, kSlotW = kPubId + 128,
                           kCnt = kSlotW + size_t(kSlots) * 8, kMb = kCnt + size_t(kSlots) * 4,
                           kNk = kMb + size_t(kSlots) * 4, kPkId = kNk + size_t(kSlots) * 8,
                           kPkK = kPkId + size_t(kSlots) * 32 * 4,
