@@ -332,10 +332,8 @@ __global__ void __launch_bounds__(128)
     if (t0) {  // further tiles (k > TR only)
       rows = min(TR, m - t0);
       __syncthreads();  // previous tile fully consumed
-      if (tid == 0) {
-        fence_proxy_async();
-        mbar_arrive_expect_tx(bar, rows * D * uint32_t(sizeof(T)));
-      }
+      fence_proxy_async();  // each issuing thread orders the reads before its copies
+      if (tid == 0) mbar_arrive_expect_tx(bar, rows * D * uint32_t(sizeof(T)));
       __syncthreads();
       for (uint32_t i = tid; i < rows; i += blockDim.x) {
         bulk_g2s(Vt + size_t(i) * D, V + size_t(ids[size_t(h) * k + t0 + i]) * D,

@@ -288,10 +288,9 @@ __device__ void fused_attention_tail(const SearchArgs& a, const PipeLayout& lay,
   __syncthreads();
   uint32_t rows = min(R, m), phase = 0;
   // the first pass's V rows are requested first; the W fold runs under them
-  if (tid == 0) {
-    fence_proxy_async();
-    mbar_arrive_expect_tx(bar, rows * uint32_t(D) * 4u);
-  }
+  // (every issuing thread orders the area's earlier generic accesses first)
+  fence_proxy_async();
+  if (tid == 0) mbar_arrive_expect_tx(bar, rows * uint32_t(D) * 4u);
   __syncthreads();
   for (uint32_t i = tid; i < rows; i += nth) {
     bulk_g2s(Vt + size_t(i) * D, V + size_t(A.id[i]) * D, D * 4u, bar);
@@ -326,10 +325,8 @@ __device__ void fused_attention_tail(const SearchArgs& a, const PipeLayout& lay,
     if (t0) {
       rows = min(R, m - t0);
       __syncthreads();  // previous pass consumed
-      if (tid == 0) {
-        fence_proxy_async();
-        mbar_arrive_expect_tx(bar, rows * uint32_t(D) * 4u);
-      }
+      fence_proxy_async();
+      if (tid == 0) mbar_arrive_expect_tx(bar, rows * uint32_t(D) * 4u);
       __syncthreads();
       for (uint32_t i = tid; i < rows; i += nth) {
         bulk_g2s(Vt + size_t(i) * D, V + size_t(A.id[t0 + i]) * D, D * 4u, bar);
