@@ -965,7 +965,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     }
     if constexpr (TP) {
       __syncwarp();
-      if (fin_smem && p2 <= 256) {
+      if (p2 <= 256) {  // (A in shared memory or in the HBM slot)
         // pool in registers (element lane * 8 + i), warp bitonic sort
         uint64_t sk8[8];
         uint32_t si8[8];
@@ -1342,7 +1342,10 @@ bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* sc
   s.vis_global = reinterpret_cast<uint32_t*>(cur);
   if (tp) {
     s.fa.out = nullptr;
-    PipeLayout lay{uint32_t(D), std::max<uint32_t>(a.max_M, 1), (max_n + 31) / 32, 0, 256};
+#ifndef RA_TP_CAPO
+#define RA_TP_CAPO 256
+#endif
+    PipeLayout lay{uint32_t(D), std::max<uint32_t>(a.max_M, 1), (max_n + 31) / 32, 0, RA_TP_CAPO};
     const size_t bytes = kTW * lay.tp_warp_bytes();
     auto kern = k_graph_search_pipe<D, false, true, BF>;
     RA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
