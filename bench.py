@@ -314,6 +314,10 @@ def main():
     step_ms, ms, ms_e2e = ms, ms / units, ms_e2e / units
     d, M = 128, a.max_degree
     bytes_search = statistics.mean([s * d * 4 + e * M * 4 + 0.0 for s, e in zip(scanned, expanded)])
+    fused = eng.kernels_per_step() == 1
+    if fused:  # the kernel also reads W's K and V rows (once per group) and the Omega V rows
+        nW = min(128, a.n_ctx) + min(512, max(a.n_ctx - 128, 0))
+        bytes_search += len(my_groups) * nW * d * 8 + Hl * a.top_k * d * 4
     peak, peak_kind = measured_peaks()
     achieved = bytes_search / (statistics.mean(search_ms) * 1e-3) / 1e9
     res = {
@@ -333,7 +337,10 @@ def main():
                 "d2h_bytes_per_step": Hl * 128 * 8 + Hl * max(eng.k, 1) * 4 + Hl * 8},
         # fused step: 1 kernel (search + W / Omega partials + merge), else 3
         "gpu_launches": eng.kernels_per_step() * a.steps,
-        "roofline": {"bound": "hbm", "kernel": "k_graph_search_pipe (latency mode)",
+        "roofline": {"bound": "hbm",
+                     "kernel": "k_graph_search_pipe (latency mode" +
+                               (", fused attention: search + W / Omega partials + merge)"
+                                if fused else ")"),
                      "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 5), "peak_source": peak_kind,
                      "traffic": ncu_traffic(),
