@@ -267,7 +267,7 @@ __device__ void fused_attention_tail(const SearchArgs& a, const PipeLayout& lay,
                                      uint8_t* smem) {
   const uint32_t tid = threadIdx.x, nth = blockDim.x;
   const auto& fa = a.fa;
-  constexpr uint32_t CB = 16;  // W chunk partials staged per round
+  constexpr uint32_t CB = 32;  // W chunk partials staged per round
   // a fresh mbarrier in ctrl[14..15] (unused words; the warps' own are left alone)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + PipeLayout::kCtrl + 14 * 4);
   const size_t a_bytes = fin_smem ? ((PipeLayout::arr_bytes(p2) + 15) & ~size_t(15)) : 0;
@@ -296,21 +296,31 @@ __device__ void fused_attention_tail(const SearchArgs& a, const PipeLayout& lay,
     bulk_g2s(Vt + size_t(i) * D, V + size_t(A.id[i]) * D, D * 4u, bar);
     e[i] = exp(okey_inv(A.k[i]) * fa.inv_sqrt_d - zo);
   }
-  // W: max over the chunk maxima (one parallel load), then the chunks in order
+  // W: the chunk partials (one staging round when they fit), their max, then
+  // the chunks in order
+  const bool one = fa.nchunk <= CB;
   double zw = -DBL_MAX;
-  for (uint32_t c = tid; c < fa.nchunk; c += nth) zw = fmax(zw, ch[size_t(c) * (D + 2) + D]);
+  if (one) {
+    for (uint32_t x = tid; x < fa.nchunk * (D + 2); x += nth) chs[x] = ch[x];
+    __syncthreads();
+    for (uint32_t c = 0; c < fa.nchunk; ++c) zw = fmax(zw, chs[size_t(c) * (D + 2) + D]);
+  } else {
+    for (uint32_t c = tid; c < fa.nchunk; c += nth) zw = fmax(zw, ch[size_t(c) * (D + 2) + D]);
 #pragma unroll
-  for (int o = 16; o; o >>= 1) zw = fmax(zw, __shfl_xor_sync(kFull, zw, o));
-  if ((tid & 31) == 0) red[tid >> 5] = zw;
-  __syncthreads();
-  zw = red[0];
-  for (uint32_t w = 1; w < nth / 32; ++w) zw = fmax(zw, red[w]);
+    for (int o = 16; o; o >>= 1) zw = fmax(zw, __shfl_xor_sync(kFull, zw, o));
+    if ((tid & 31) == 0) red[tid >> 5] = zw;
+    __syncthreads();
+    zw = red[0];
+    for (uint32_t w = 1; w < nth / 32; ++w) zw = fmax(zw, red[w]);
+  }
   double sw = 0.0, ow = 0.0;
   const uint32_t j = tid;  // this thread's output dimension (j < D)
   for (uint32_t c0 = 0; c0 < fa.nchunk; c0 += CB) {
     const uint32_t cn = min(CB, fa.nchunk - c0);
-    for (uint32_t x = tid; x < cn * (D + 2); x += nth) chs[x] = ch[size_t(c0) * (D + 2) + x];
-    __syncthreads();
+    if (!one) {
+      for (uint32_t x = tid; x < cn * (D + 2); x += nth) chs[x] = ch[size_t(c0) * (D + 2) + x];
+      __syncthreads();
+    }
     if (tid < cn) wx[tid] = exp(chs[size_t(tid) * (D + 2) + D] - zw);
     __syncthreads();
     for (uint32_t c = 0; c < cn; ++c) {  // chunk order
@@ -923,7 +933,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
       __syncwarp();
       // (fused attention: leave room for >= 8 staged V rows behind the array)
       fin_smem = PipeLayout::arr_bytes(p2) + 16 +
-                     (a.fa.out && !BF ? (24 + 16 * (size_t(D) + 2)) * 8 + 8 * (size_t(D) * 4 + 8)
+                     (a.fa.out && !BF ? (40 + 32 * (size_t(D) + 2)) * 8 + 8 * (size_t(D) * 4 + 8)
                                       : 0) <=
                  size_t(kPW) * lay.tile_bytes();
       if (lane == 0) {
