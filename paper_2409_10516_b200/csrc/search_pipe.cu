@@ -712,11 +712,14 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         fo_rescan();
       }
       nU = __reduce_add_sync(kFull, uint32_t(kUR) - __popc(ufree)) + nUO;
-      // pivot: the largest key with >= ef - 24 entries at or above it
-      // (bisection between thr and the U max), then its exact count
-      if (ef > 24) {
+      // pivot: the largest key with >= ef - 48 entries at or above it
+      // (bisection between thr and the U max), then its exact count; the
+      // slack is how many inserts above it the pivot survives (48 measured
+      // best of 24 / 32 / 48 / 64)
+      const uint32_t pslack = (a.flags >> 23) & 15u ? ((a.flags >> 23) & 15u) * 8u : 48u;
+      if (ef > pslack) {
         uint64_t plo = thr, phi = hmax;
-        const uint32_t target = ef - 24;
+        const uint32_t target = ef - pslack;
         if (count_gt(phi - 1) >= target) {
           plo = phi;
         } else {
