@@ -147,12 +147,32 @@ class ClockSampler:
 
 
 def measured_peaks():
+    """HBM GB/s from the driver-written MEASURED_PEAKS.json (any numeric entry
+    whose key path names HBM bandwidth; TB/s values are scaled), else the
+    profiling recipe's 6650 GB/s fallback."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+    found = []
+
+    def walk(node, path):
+        if isinstance(node, dict):
+            for k, v in node.items():
+                walk(v, path + [str(k).lower()])
+        elif isinstance(node, (int, float)) and not isinstance(node, bool):
+            key = "/".join(path)
+            if "hbm" in key and not any(t in key for t in ("tflop", "pflop", "clock", "mhz")):
+                found.append((key, float(node)))
+
+    walk(p, [])
+    for key, v in sorted(found, key=lambda kv: ("copy" not in kv[0] and "gb" not in kv[0],
+                                                 kv[0])):
+        gbs = v * 1000.0 if v < 100 else v  # a TB/s figure
+        if 1000.0 < gbs < 20000.0:
+            return gbs, "measured"
+    return 6650.0, "fallback"
 
 
 def ncu_traffic():
