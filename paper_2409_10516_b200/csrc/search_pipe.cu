@@ -100,6 +100,13 @@ __device__ __forceinline__ uint32_t slot_of(uint32_t id) {
   return ((id * 2654435761u) >> (33 - kSlotBits)) << 1;
 }
 __device__ __forceinline__ uint32_t lanemask_lt(uint32_t lane) { return (1u << lane) - 1u; }
+// release store to a shared word (the reads before it complete first)
+__device__ __forceinline__ void st_release_cta(unsigned long long* p, uint64_t v) {
+  asm volatile("st.release.cta.shared::cta.u64 [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(p))),
+               "l"(v)
+               : "memory");
+}
 
 // Best-first bitonic sort of 256 (key, id) entries held by one warp, entry
 // lane * 8 + i in register i: distances < 8 inside a lane, the rest by
@@ -886,18 +893,18 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
       if (hit) {
         ++c_hit;
         __threadfence_block();
-        const uint32_t cnt = pk_cnt[sl], mb = pk_mb[sl];
         const uint32_t j = (lane + rot) & 31u;
+        // all four loads at once (the entry loads do not wait for the count)
+        const uint32_t cnt = pk_cnt[sl], mb = pk_mb[sl];
+        const uint32_t pv = pk_id[sl * 32 + j];
+        const uint64_t px = pk_k[sl * 32 + j];
         cand = j < cnt;
-        cv = cand ? pk_id[sl * 32 + j] : kSentinel;
-        cx = cand ? pk_k[sl * 32 + j] : 0;
+        cv = cand ? pv : kSentinel;
+        cx = cand ? px : 0;
         cm = cand && ((mb >> j) & 1u);
         pre = false;  // other packets may have visited these since
         __syncwarp();
-        if (lane == 0) {
-          __threadfence_block();
-          *reinterpret_cast<volatile unsigned long long*>(slotw + sl) = slotword(kSentinel, sFREE);
-        }
+        if (lane == 0) st_release_cta(slotw + sl, slotword(kSentinel, sFREE));
         rot += cnt;
       } else {
         ++c_miss;
