@@ -844,9 +844,18 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         __syncwarp();
         fo_rescan();
       } else {
-        // owner lane: its last entry fills the hole; then the owner's new
-        // head is found by kFR lanes at once (one entry each, 3 REDUX)
+        // the owner's new head: kFR lanes read its other entries (one each,
+        // from the list as it was) and 3 REDUX pick the best; meanwhile the
+        // owner lane's last entry fills the hole (its stores follow the
+        // loads in program order)
         const uint32_t owner = __ffs(__ballot_sync(kFull, hi == tid)) - 1;
+        const uint32_t fc0 = __shfl_sync(kFull, fcnt, owner);
+        const uint32_t hp = __shfl_sync(kFull, hpos, owner);
+        uint64_t x = 0;
+        uint32_t v = kSentinel;
+        if (lane < uint32_t(kFR)) x = Fl_k[lane * 32 + owner], v = Fl_i[lane * 32 + owner];
+        const bool live = lane < fc0 && lane != hp;
+        if (!live) x = 0, v = kSentinel;
         if (lane == owner) {
           --fcnt;
           if (hpos != fcnt) {
@@ -855,15 +864,11 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
           }
           Fl_k[fcnt * 32 + lane] = 0, Fl_i[fcnt * 32 + lane] = kSentinel;
         }
-        __syncwarp();
-        const uint32_t fc = __shfl_sync(kFull, fcnt, owner);
-        uint64_t x = 0;
-        uint32_t v = kSentinel;
-        if (lane < fc) x = Fl_k[lane * 32 + owner], v = Fl_i[lane * 32 + owner];
         const uint32_t mine = v;
         warp_best(x, v);
-        const uint32_t pos = __ffs(__ballot_sync(kFull, lane < fc && mine == v)) - 1;
-        if (lane == owner) hk = x, hi = v, hpos = fc ? pos : 0;
+        const uint32_t pos = __ffs(__ballot_sync(kFull, live && mine == v)) - 1;
+        // (the old last entry now sits in the hole)
+        if (lane == owner) hk = x, hi = v, hpos = fcnt ? (pos == fcnt ? hp : pos) : 0;
       }
       ++expanded;
       PIPE_TICK(1)
