@@ -428,8 +428,13 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     __syncwarp();
   } else {
     if (lane == 0) mbar_init(bar);
+    // the query element is requested first (it may live in page-locked host
+    // memory: a bus round trip), the bitset zeroing runs under it
+    const float qe = threadIdx.x < uint32_t(D) ? a.q[size_t(b) * D + threadIdx.x] : 0.f;
     for (uint32_t w = threadIdx.x; w < 2 * vw; w += blockDim.x) vis[w] = 0;
-    for (uint32_t i = threadIdx.x; i < D; i += blockDim.x) qd[i] = (double)a.q[size_t(b) * D + i];
+    if (threadIdx.x < uint32_t(D)) qd[threadIdx.x] = (double)qe;
+    for (uint32_t i = threadIdx.x + blockDim.x; i < D; i += blockDim.x)
+      qd[i] = (double)a.q[size_t(b) * D + i];
     for (uint32_t i = threadIdx.x; i < kSlots; i += blockDim.x)
       slotw[i] = slotword(kSentinel, sFREE);
     if (threadIdx.x < 32) pub_k[threadIdx.x] = 0, pub_id[threadIdx.x] = kSentinel;
