@@ -1361,7 +1361,20 @@ bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* sc
   uint32_t spill_cap = 32;
   while (spill_cap < max_n) spill_cap <<= 1;
   SearchArgs s = a;
-  static const uint32_t env_flags = [] {  // profiling switches, read once
+  // RA_PIPE_FLAGS: profiling / tuning switches, read once (0 = the defaults):
+  //   bit 0      helpers idle (commit warp alone)
+  //   bit 1      no L2 prefetch of new nodes' adjacency rows
+  //   bit 3      no hint ring
+  //   bits 4-7   chain length (default 3)        bits 8-12  tournament pick (12)
+  //   bit 13     throughput mode: no L1 prefetch of key rows
+  //   bit 14     chain regardless of the parent's rank
+  //   bit 15     no hints from inline expansions   bit 16  no unchained-best hints
+  //   bit 17     also hint the third child
+  //   bits 19-21 helpers allowed to take W chunks during the search (default all)
+  //   bit 22     the commit warp's scheduler partner pre-expands too
+  //   bits 23-26 stop-test pivot slack / 8 (default 48)
+  //   bits 28-31 thr bisection steps / 4 (default 8)
+  static const uint32_t env_flags = [] {
     const char* f = std::getenv("RA_PIPE_FLAGS");
     return f ? uint32_t(std::atoi(f)) : 0u;
   }();
