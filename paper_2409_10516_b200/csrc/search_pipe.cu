@@ -66,6 +66,10 @@ constexpr uint32_t kTW = RA_TP_WARPS;  // TP mode: queries (warps) per CTA
 #define RA_TP_MINB 2  // <= 128 registers: 16 query warps per SM
 #endif
 constexpr int kFR = 8;             // frontier entries per lane (sorted)
+#ifndef RA_HINTS
+#define RA_HINTS 64
+#endif
+constexpr uint32_t kHintN = RA_HINTS;  // hint ring entries (a multiple of 32)
 constexpr int kUR = 8;             // pool-candidate entries per lane
 #ifndef RA_PIPE_SLOT_BITS
 #define RA_PIPE_SLOT_BITS 7
@@ -228,8 +232,8 @@ struct PipeLayout {
                           kNk = kMb + size_t(kSlots) * 4, kPkId = kNk + size_t(kSlots) * 8,
                           kPkK = kPkId + size_t(kSlots) * 32 * 4,
                           kPubF = kPkK + size_t(kSlots) * 32 * 8,  // F: k u64[kFR][32], id u32[kFR][32]
-                          kHint = kPubF + size_t(kFR) * 32 * 12,   // hints: k u64[32], id u32[32]
-                          kQd = kHint + 32 * 12;
+                          kHint = kPubF + size_t(kFR) * 32 * 12,   // hints: k u64[N], id u32[N]
+                          kQd = kHint + size_t(kHintN) * 12;
   __host__ __device__ size_t row_floats() const { return D + 4; }
   __host__ __device__ size_t tiles_off() const { return kQd + size_t(D) * 8; }
   __host__ __device__ size_t tile_bytes() const { return size_t(MT) * row_floats() * 4; }
@@ -399,10 +403,10 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
   // hint ring: the runner-up children of recent pre-expansions (likely tops
   // right after their parent commits), written by helpers, read by helpers
   volatile uint64_t* hint_k = reinterpret_cast<volatile uint64_t*>(smem + PipeLayout::kHint);
-  volatile uint32_t* hint_id = reinterpret_cast<volatile uint32_t*>(hint_k + 32);
+  volatile uint32_t* hint_id = reinterpret_cast<volatile uint32_t*>(hint_k + kHintN);
   // one entry into the 32-slot hint ring (any warp, one lane)
   auto push_hint = [&](uint64_t k, uint32_t id) {
-    const uint32_t h = atomicAdd(const_cast<uint32_t*>(ctrl) + 12, 1u) & 31u;
+    const uint32_t h = atomicAdd(const_cast<uint32_t*>(ctrl) + 12, 1u) & (kHintN - 1u);
     hint_id[h] = kSentinel;
     hint_k[h] = k;
     hint_id[h] = id;
@@ -439,7 +443,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
       slotw[i] = slotword(kSentinel, sFREE);
     if (threadIdx.x < 32) pub_k[threadIdx.x] = 0, pub_id[threadIdx.x] = kSentinel;
     for (uint32_t i = threadIdx.x; i < kFR * 32; i += blockDim.x) pubf_k[i] = 0, pubf_id[i] = kSentinel;
-    if (threadIdx.x < 32) hint_k[threadIdx.x] = 0, hint_id[threadIdx.x] = kSentinel;
+    for (uint32_t i = threadIdx.x; i < kHintN; i += blockDim.x) hint_k[i] = 0, hint_id[i] = kSentinel;
     if (threadIdx.x < 16) ctrl[threadIdx.x] = 0;
     __syncthreads();
   }
@@ -1199,12 +1203,16 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         const uint64_t w1 = *reinterpret_cast<volatile unsigned long long*>(slotw + s0 + 1);
         return uint32_t(w0) != id && uint32_t(w1) != id;  // not in flight / ready already
       };
-      // best claimable hint (one per lane)
-      uint64_t hx = hint_k[lane];
-      uint32_t hid = hint_id[lane];
-      if (!(a.flags & 8u) && hid != kSentinel && claimable(hid)) {
-      } else {
-        hx = 0, hid = kSentinel;
+      // best claimable hint (kHintN / 32 per lane)
+      uint64_t hx = 0;
+      uint32_t hid = kSentinel;
+      if (!(a.flags & 8u)) {
+#pragma unroll
+        for (uint32_t t = 0; t < kHintN / 32; ++t) {
+          const uint64_t k2 = hint_k[t * 32 + lane];
+          const uint32_t i2 = hint_id[t * 32 + lane];
+          if (i2 != kSentinel && better(k2, i2, hx, hid) && claimable(i2)) hx = k2, hid = i2;
+        }
       }
       warp_best(hx, hid);
       uint32_t got = kSentinel, sl = 0;
