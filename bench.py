@@ -1,17 +1,29 @@
 #!/usr/bin/env python3
 """Decode-attention benchmark: RetrievalAttention hot path at Llama-3-8B shape.
 
-Workload (BASELINE.json configs[1]): one layer, 32 query heads over 8 KV
-groups, d_head 128, 128K context, static set = first 128 + last 512 tokens,
-top-100 retrieval per head through the head's OODGraph (k_train 128, M 24,
-efc 256, window 8; README/acceptance parameters), ef 128. Inputs are the
-reference generator's synthetic OOD K/Q/V (seed 7), synthesized on the GPU
-(paper_2409_10516_b200.workload); graphs are built on the GPU (untimed).
+Headline workload (BASELINE.json configs[1]): one layer, 32 query heads over
+8 KV groups, d_head 128, 128K context, static set = first 128 + last 512
+tokens, top-100 retrieval per head through the head's OODGraph (k_train
+128, M 24, efc 256, window 8; README/acceptance parameters), ef 128. Inputs
+are the reference generator's synthetic OOD K/Q/V (seed 7), synthesized on
+the GPU (paper_2409_10516_b200.workload, equal to the reference generator's
+output: tests/test_workload_gpu.py); graphs are built on the GPU (untimed).
 
 One step = ra_engine decode step for all local heads: graph search ->
-partial attention over W -> partial over Omega -> LSE merge (+ NCCL
-all_gather of per-head outputs when N > 1, heads sharded by KV group).
+partial attention over W -> partial over Omega -> LSE merge.
 Metric: ms per decode step (token) for the layer, lower is better.
+
+Further lines in the same JSON object (`lines`), each with its own
+roofline: `layers32` (the north-star shape: 32 distinct layers x 8 KV
+groups x 4 heads at 128K, batch 1, one token = 1024 searches + attention),
+`batch8` (configs[2]'s per-GPU shard at 8 GPUs: 32 layers x 1 KV group x 8
+distinct batch contexts), `ctx_1m` (configs[4]: one full layer at a 1M-token
+context on one GPU).
+
+`--impl reference` runs the reference's own CPU path end to end from
+oracle/_ref (unmodified reference sources): generate_workload +
+engine_init (OODGraph builds) + decode_step, on the host cores, with no
+code of this repo on its path.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -33,16 +45,22 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "decode attention ms/token @128K (Llama-3-8B shape); search recall@100; HBM GB/s"
-TPUT_R = 128  # batched line: 128 decode queries per head x 32 heads = 4096 searches
 
 
 def workload_config(a, H, G):
-    """The workload both arms run (BASELINE.json configs[1])."""
+    """The workload both arms run (BASELINE.json configs[1]); identical dicts
+    in both arms (how each arm executes goes to the line's `execution`)."""
     return {"workload": "configs[1]: Llama-3-8B shape single layer, 32 Q heads / 8 KV "
                         "groups, d=128, 128K ctx, top-100 + 640 static, ef 128",
             "n_ctx": a.n_ctx, "heads": H, "kv_groups": G, "top_k": a.top_k, "ef": a.ef,
             "graph": {"k_train": a.k_train, "max_degree": a.max_degree,
                       "ef_construction": a.ef_construction, "edge_window": 8},
+            "seed": 7,
+            "parallelism": (f"{a.gpus} GPU(s), " + ("KV groups sharded over ranks + NCCL "
+                                                    "all_gather of outputs"
+                                                    if a.shard == "heads" else
+                                                    "rank r decodes synthetic layer r")
+                            if a.gpus > 1 else "single device"),
             "l2": f"flushed between timed steps ({a.flush_mb} MiB write)"}
 
 
@@ -64,11 +82,19 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-bf16", action="store_true", help="skip the bf16-KV measurement")
-    ap.add_argument("--no-throughput", action="store_true",
-                    help="skip the batched (throughput-mode) line (launch-list profiling)")
-    ap.add_argument("--no-multilayer", action="store_true",
-                    help="skip the 4-distinct-layer batched measurement")
     ap.add_argument("--flush-mb", type=int, default=512)
+    ap.add_argument("--no-layers32", action="store_true",
+                    help="skip the 32-distinct-layer line (north-star shape)")
+    ap.add_argument("--no-batch8", action="store_true",
+                    help="skip configs[2]'s per-GPU shard line (32 layers x batch 8)")
+    ap.add_argument("--no-1m", action="store_true", help="skip the 1M-context line")
+    ap.add_argument("--lines-only", default="",
+                    help="comma list of lines to run (layers32,batch8,ctx_1m); "
+                         "skips the headline measurement (profiling)")
+    ap.add_argument("--line-layers", type=int, default=32)
+    ap.add_argument("--ref-build-workers", type=int, default=4,
+                    help="reference arm: heads built concurrently (each ood_build with "
+                         "nproc / workers threads)")
     ap.add_argument("--shard", default="layers", choices=["layers", "heads"],
                     help="N>1: layers = weak scaling, rank r decodes its own synthetic layer "
                          "(seed 7 + r, all 32 heads, no data-path collective); heads = strong "
@@ -175,46 +201,90 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
-def ncu_traffic():
-    """dram bytes per launch of the search kernel from the committed ncu
-    --set full capture (profiles/ncu_search_summary.json), if present."""
+def ncu_summary(name="ncu_search_summary.json"):
+    """A committed ncu summary under profiles/ (dram bytes per launch of a
+    line's dominant kernel, from a --set full / dram metrics capture)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_search_summary.json")) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return json.load(f)
     except Exception:
-        return None
+        return {}
+
+
+def ncu_traffic():
+    return ncu_summary().get("dram_bytes_per_launch")
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def timed(fn, stream, flush=None):
+    """Device time of fn() on `stream` (CUDA events), L2 flushed before."""
+    import torch
+    if flush is not None:
+        flush.zero_()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    fn()
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1)
 
 
 def main():
     a = parse()
+    if a.impl == "reference":
+        run_reference(a)  # no torch.cuda, no code of this package on that path
+        return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if a.impl == "reference" and rank != 0:
-        return  # the reference CPU arm runs on rank 0 only
     import torch
     torch.cuda.set_device(local)
     dist = None
-    if world > 1 and a.impl == "ours":
+    if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2409_10516_b200 as ra
     from paper_2409_10516_b200.workload import WorkloadSpec, generate_group
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(a.flush_mb * (1 << 20) // 4, dtype=torch.float32, device=dev)
+    parity_jobs = []
+
+    if a.lines_only:
+        lines = run_lines(a, ra, flush, stream, dev, parity_jobs,
+                          set(a.lines_only.split(",")))
+        print(json.dumps({"lines": lines}))
+        return
 
     H, G = a.heads, a.groups
     hpg = H // G
-    n_world = world if a.impl == "ours" else 1
     from paper_2409_10516_b200.shard import OutputGather, groups_for_rank
-    by_heads = a.shard == "heads" and n_world > 1
-    my_groups = (groups_for_rank(G, n_world, rank) if by_heads else list(range(G)))
-    layer = rank if (a.impl == "ours" and not by_heads) else 0
-    # decode queries: the timed steps, the e2e steps, and one batched step of
-    # TPUT_R queries per head (the throughput line)
-    n_dec = max(a.warmup + 2 * a.steps + 2, TPUT_R)
+    by_heads = a.shard == "heads" and world > 1
+    my_groups = (groups_for_rank(G, world, rank) if by_heads else list(range(G)))
+    layer = rank if not by_heads else 0
+    # decode queries: the timed steps and the e2e steps
+    n_dec = a.warmup + 2 * a.steps + 2
     # synthetic layer l uses seed 7 + l (SURVEY §8 d; the reference has no layers)
     spec = WorkloadSpec(n_ctx=a.n_ctx, d_model=256, d_head=128, n_heads=H, n_kv_groups=G,
                         seed=7 + layer, n_decode=n_dec)
-    dev = torch.device("cuda", local)
     t0 = time.time()
     kvs, graphs, dq, keys_host, vals_host = [], [], [], [], []
     bp = ra.OODGraphBuildParams(a.k_train, a.max_degree, a.ef_construction, 8)
@@ -229,7 +299,7 @@ def main():
             graphs.append(ra.ood_build(kv, w["prefill_q"][m], bp))
             build_ms.append((time.time() - tb) * 1e3)
             dq.append(w["decode_q"][m])
-        if a.impl == "reference" or rank == 0:
+        if rank == 0:
             keys_host.append(w["keys"].cpu().numpy())
             vals_host.append(w["values"].cpu().numpy())
         del w
@@ -239,14 +309,9 @@ def main():
     del dq
     cfg = ra.EngineConfig(128, 512, a.top_k, a.ef)
 
-    if a.impl == "reference":
-        run_reference(a, keys_host, vals_host, graphs, Q, cfg, H, G, setup_s)
-        return
-
     eng = ra.Engine(kvs, graphs, cfg)
-    stream = torch.cuda.current_stream()
-    flush = torch.empty(a.flush_mb * (1 << 20) // 4, dtype=torch.float32, device=dev)
     gather = OutputGather(G, hpg, 128, world, rank, dev) if (dist is not None and by_heads) else None
+    gather_ms = []
 
     def step(i):
         out, om, sc = eng.decode_step_device(Q[i])
@@ -260,27 +325,23 @@ def main():
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
-    times, search_ms, attn_ms, scanned, expanded = [], [], [], [], []
+    times, search_ms, scanned, expanded = [], [], [], []
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         for i in range(a.warmup, a.warmup + a.steps):
-            flush.zero_()  # evict L2 between timed steps (outside the events)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            step(i)
-            e1.record(stream)
-            e1.synchronize()
-            times.append(e0.elapsed_time(e1))
-            s_ms, a_ms = eng.last_timing()
-            search_ms.append(s_ms)
-            attn_ms.append(a_ms)
+            times.append(timed(lambda: step(i), stream, flush))
+            search_ms.append(eng.last_timing()[0])
             s, e = eng.last_stats()
             scanned.append(s)
             expanded.append(e)
         torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
+        if gather is not None:  # NCCL all_gather latency alone (per step)
+            out0 = eng.decode_step_device(Q[a.warmup])[0]
+            torch.cuda.synchronize()
+            for _ in range(5):
+                gather_ms.append(timed(lambda: gather(out0, dist), stream))
 
     # ---- end-to-end through the host API (H2D q, D2H out/omega/scanned) ----
     qh = torch.empty((Hl, 128), dtype=torch.float32, pin_memory=True)
@@ -293,20 +354,13 @@ def main():
         qh.copy_(Qh[i])
         flush.zero_()
         torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        eng.ctx.bind_stream()
-        ra.api._check(ra.lib.ra_engine_step_host(eng.h, qh.data_ptr(), out_h.data_ptr(),
-                                                 om_h.data_ptr(), sc_h.data_ptr()))
-        e1.record(stream)
-        e1.synchronize()
-        e2e.append(e0.elapsed_time(e1))
 
-    tput = (batched_throughput(a, ra, kvs, graphs, Q, cfg, flush, stream)
-            if not a.no_throughput else None)
-    tput_ml = (multilayer_throughput(a, ra, spec, my_groups, hpg, kvs, graphs, Q, cfg, flush,
-                                     stream, layer) if not a.no_multilayer else None)
+        def host_step():
+            eng.ctx.bind_stream()
+            ra.api._check(ra.lib.ra_engine_step_host(eng.h, qh.data_ptr(), out_h.data_ptr(),
+                                                     om_h.data_ptr(), sc_h.data_ptr()))
+        e2e.append(timed(host_step, stream))
+
     out32 = eng.decode_step_device(Q[a.warmup])[0].cpu().numpy()
     bf16 = (bf16_mode(a, ra, spec, my_groups, hpg, Q, cfg, flush, stream, out32, graphs)
             if not a.no_bf16 else None)
@@ -314,6 +368,7 @@ def main():
     ms = statistics.mean(times)
     ms_search = statistics.mean(search_ms)
     ms_e2e = statistics.mean(e2e)
+    shard_balance = None
     if dist is not None:
         t = torch.tensor([ms, ms_e2e, ms_search], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -326,36 +381,33 @@ def main():
         per_rank = [float(x) for x in all_sc]
         shard_balance = {"mean_scanned_per_head_by_rank": [round(x, 1) for x in per_rank],
                          "max_over_mean": round(max(per_rank) / statistics.mean(per_rank), 4)}
-    else:
-        shard_balance = None
-    # whole-job aggregate: layer-sharded ranks each decode one layer per step,
-    # so N layer-tokens complete in the (max-over-ranks) step time
-    units = world if (dist is not None and not by_heads) else 1
-    step_ms, ms, ms_e2e = ms, ms / units, ms_e2e / units
+        if gather_ms:
+            shard_balance["nccl_all_gather_ms"] = round(statistics.mean(gather_ms), 4)
     d, M = 128, a.max_degree
     bytes_search = statistics.mean([s * d * 4 + e * M * 4 + 0.0 for s, e in zip(scanned, expanded)])
     fused = eng.kernels_per_step() == 1
-    if fused:  # the kernel also reads W's K and V rows (once per group) and the Omega V rows
+    if fused:  # the kernel also computes the attention: W's K and V rows (algorithmically
+        # once per KV group; the kernel reads them per head) and the Omega V rows
         nW = min(128, a.n_ctx) + min(512, max(a.n_ctx - 128, 0))
         bytes_search += len(my_groups) * nW * d * 8 + Hl * a.top_k * d * 4
     peak, peak_kind = measured_peaks()
-    achieved = bytes_search / (statistics.mean(search_ms) * 1e-3) / 1e9
+    achieved = bytes_search / (ms_search * 1e-3) / 1e9
+    layer_tokens = world if (dist is not None and not by_heads) else 1
     res = {
         "metric": METRIC, "value": round(ms, 4), "unit": "ms/token", "n_gpus": world,
-        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(step_ms, 4),
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": False, "scaling": "strong" if by_heads else "weak",
         "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (reference OOD generator algorithm, seed 7, GPU-synthesized)",
-        "config": dict(workload_config(a, H, G),
-                       parallelism=(f"heads sharded by KV group over {world} GPU(s) + NCCL "
-                                    "all_gather of outputs" if by_heads else
-                                    f"layer-sharded: {world} GPU(s), rank r decodes synthetic "
-                                    "layer r (all 32 heads), no data-path collective; value = "
-                                    "step time / layers")),
+        "data": "synthetic: the reference OOD generator (workload.cpp:102-203) restated on "
+                "the GPU, seed 7 + layer",
+        "config": workload_config(a, H, G),
+        "execution": ("one ra_engine step per token (fused search + attention kernel)"
+                      if fused else "one ra_engine step per token (3 kernels)") +
+                     (f"; {world} ranks each decode their own layer per step "
+                      f"({layer_tokens} layer-tokens per step)" if layer_tokens > 1 else ""),
         "e2e": {"value": round(ms_e2e, 4), "unit": "ms/token",
                 "h2d_bytes_per_step": Hl * 128 * 4,
                 "d2h_bytes_per_step": Hl * 128 * 8 + Hl * max(eng.k, 1) * 4 + Hl * 8},
-        # fused step: 1 kernel (search + W / Omega partials + merge), else 3
         "gpu_launches": eng.kernels_per_step() * a.steps,
         "roofline": {"bound": "hbm",
                      "kernel": "k_graph_search_pipe (latency mode" +
@@ -365,14 +417,11 @@ def main():
                      "frac": round(achieved / peak, 5), "peak_source": peak_kind,
                      "traffic": ncu_traffic(),
                      "algorithmic_bytes_per_launch": int(bytes_search),
-                     "search_ms": round(ms_search, 4),
-                     "attention_ms": round(statistics.mean(attn_ms), 4)},
+                     "kernel_ms": round(ms_search, 4)},
         "search": {"mean_scanned_per_head": statistics.mean(scanned) / Hl,
                    "mean_expanded_per_head": statistics.mean(expanded) / Hl,
                    "scan_fraction": statistics.mean(scanned) / Hl / (a.n_ctx - 640)},
         "clocks": clk.summary(),
-        "throughput": tput,
-        "throughput_multilayer": tput_ml,
         "shard_balance": shard_balance,
         "bf16_kv": bf16,
         "setup_s": round(setup_s, 1),
@@ -382,118 +431,180 @@ def main():
             for k in ("knn", "knn_tensor", "edges", "prune", "entry", "repair")},
         "build_knn_rows_exact_fallback": sum(g.build_stats.knn_rows_widened for g in graphs),
     }
+    if layer_tokens > 1:
+        res["layer_tokens_per_s"] = round(layer_tokens / (ms * 1e-3), 1)
     if rank == 0:
         res["recall"] = recall(eng, graphs, kvs, Q, a, ra)
+    del eng
+    # the further lines (their own KV and graphs; the headline's memory is kept small)
+    if world == 1:
+        want = set()
+        if not a.no_layers32:
+            want.add("layers32")
+        if not a.no_batch8:
+            want.add("batch8")
+        if not a.no_1m:
+            want.add("ctx_1m")
+        res["lines"] = run_lines(a, ra, flush, stream, dev, parity_jobs, want)
+    if rank == 0:
         if world == 1 and not a.no_cpu_baseline:
             res["cpu_baseline"], res["parity"] = cpu_baseline(a, keys_host, vals_host, graphs,
-                                                              Q, cfg, eng)
+                                                              Q, cfg, parity_jobs)
         print(json.dumps(res))
     if dist is not None:
         dist.destroy_process_group()
 
 
-def batched_throughput(a, ra, kvs, graphs, Q, cfg, flush, stream, row_bytes=512):
-    """Batched decode: R decode queries per head issued as ONE engine step
-    over R x H heads (graphs and KV groups repeated R times, so every query
-    walks its head's real graph and KV): search (throughput-mode kernel) +
-    static/retrieved partial attention + merge for R x H queries (R = 128:
-    4096 searches, the per-GPU search count of configs[2] - 32 layers x batch
-    8 - sharded over 2 GPUs) with the layer's KV shared by the R queries of a
-    head."""
-    import torch
-    R = min(TPUT_R, Q.shape[0])
-    Hl = len(graphs)
-    eng = ra.Engine(list(kvs) * R, list(graphs) * R, cfg)
-    qb = [Q[j:j + R].reshape(R * Hl, -1).contiguous()
-          for j in range(0, Q.shape[0] - R + 1, R)]
-    for i in range(3):
-        eng.decode_step_device(qb[i % len(qb)])
-    torch.cuda.synchronize()
-    times, s_ms, sc, ex = [], [], [], []
-    for i in range(max(3, min(a.steps, 10))):
-        flush.zero_()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        eng.decode_step_device(qb[i % len(qb)])
-        e1.record(stream)
-        e1.synchronize()
-        times.append(e0.elapsed_time(e1))
-        s_ms.append(eng.last_timing()[0])
-        s, e = eng.last_stats()
-        sc.append(s)
-        ex.append(e)
-    ms, ms_s = statistics.mean(times), statistics.mean(s_ms)
-    by = statistics.mean([s * row_bytes + e * a.max_degree * 4 for s, e in zip(sc, ex)])
-    peak, kind = measured_peaks()
-    gbs = by / (ms_s * 1e-3) / 1e9
-    del eng
-    return {"queries_per_step": R * Hl, "decode_queries_per_head": R,
-            "ms_per_step": round(ms, 4), "us_per_query": round(ms * 1e3 / (R * Hl), 3),
-            "queries_per_s": round(R * Hl / (ms * 1e-3), 1),
-            "search_ms": round(ms_s, 4), "search_kernel": "k_graph_search_pipe (TP mode)",
-            "search_algorithmic_bytes": int(by),
-            "search_GBps": round(gbs, 1), "search_frac": round(gbs / peak, 4),
-            "peak_source": kind,
-            "note": "one engine step over R x H heads; KV of each head shared by its R queries"}
+# ---------------------------------------------------------------------------
+# multi-context lines: many independent (context, KV group) sets in HBM
+# ---------------------------------------------------------------------------
+def run_lines(a, ra, flush, stream, dev, parity_jobs, want):
+    out = {}
+    L = a.line_layers
+    if "layers32" in want:
+        # north-star shape: layer l = synthetic seed 7 + l, all 8 KV groups
+        ctxs = [(l, 7 + l, g) for l in range(L) for g in range(a.groups)]
+        out["layers32"] = multi_context_line(
+            a, ra, "layers32", ctxs, a.groups, a.n_ctx, flush, stream, dev, parity_jobs,
+            f"north-star shape: {L} distinct synthetic layers (seed 7 + l) x {a.groups} KV "
+            f"groups x {a.heads // a.groups} Q heads, {a.n_ctx} ctx, batch 1; one token = "
+            f"{L * a.heads} searches + sparse attention")
+    if "batch8" in want:
+        # configs[2] at 8 GPUs, heads sharded: this GPU owns KV group 0 of every
+        # layer for all 8 batch items; item b of layer l = seed 7 + 100 b + l
+        ctxs = [(l, 7 + 100 * b + l, 0) for l in range(L) for b in range(8)]
+        out["batch8"] = multi_context_line(
+            a, ra, "batch8", ctxs, 8, a.n_ctx, flush, stream, dev, parity_jobs,
+            f"configs[2] per-GPU shard at 8 GPUs: {L} layers x KV group 0 x 8 distinct batch "
+            f"contexts (seed 7 + 100 b + l) x {a.heads // a.groups} Q heads, {a.n_ctx} ctx; "
+            f"one decode step = {L * 8 * (a.heads // a.groups)} searches + attention")
+    if "ctx_1m" in want:
+        ctxs = [(0, 7, g) for g in range(a.groups)]
+        out["ctx_1m"] = multi_context_line(
+            a, ra, "ctx_1m", ctxs, a.groups, 1 << 20, flush, stream, dev, parity_jobs,
+            f"configs[4] on one GPU: one full layer ({a.groups} KV groups x "
+            f"{a.heads // a.groups} Q heads) at a 1,048,576-token context, batch 1",
+            samples=(0, a.groups - 1))
+    return out
 
 
-def multilayer_throughput(a, ra, spec, my_groups, hpg, kvs0, graphs0, Q0, cfg, flush, stream,
-                          layer0, n_layers=4, R=32):
-    """Layer-batched decode with DISTINCT layers: this layer plus 3 more
-    synthetic layers (seeds 7 + l, their own K/V and graphs), 32 decode
-    queries per head per layer, all 4096 searches + attention in one engine
-    step (configs[2]'s per-GPU shape with 4 layers x batch 32)."""
-    import dataclasses
+def multi_context_line(a, ra, name, ctxs, per_layer, n_ctx, flush, stream, dev, parity_jobs,
+                       desc, samples=None):
+    """Build every (layer, seed, group) context's KV group and its 4 query-head
+    graphs on the GPU, then time (i) the layer-batched step - one engine step
+    over all heads - and (ii) the layer-serial step - one engine step per
+    layer, back to back (the decode dependency chain). Sampled contexts are
+    queued for the reference parity check (cpu_baseline leg)."""
     import torch
-    from paper_2409_10516_b200.workload import generate_group
+    from paper_2409_10516_b200.workload import WorkloadSpec, generate_group
+    hpg = a.heads // a.groups
+    n_dec = a.warmup + a.steps + 1
     bp = ra.OODGraphBuildParams(a.k_train, a.max_degree, a.ef_construction, 8)
-    layers = [(list(kvs0), list(graphs0), Q0[:R])]
-    for l in range(1, n_layers):
-        sp = dataclasses.replace(spec, seed=7 + layer0 * n_layers + l, n_decode=R)
-        kvs, graphs, dq = [], [], []
-        for g in my_groups:
-            w = generate_group(sp, g, Q0.device)
-            kv = ra.KVGroup(w["keys"], w["values"])
-            kvs.append(kv)
-            for m in range(hpg):
-                graphs.append(ra.ood_build(kv, w["prefill_q"][m], bp))
-                dq.append(w["decode_q"][m])
-            del w
-        layers.append((kvs, graphs, torch.stack(dq, dim=1)))
-    G_all = [kv for kvs, _, _ in layers for _ in range(R) for kv in kvs]
-    H_all = [g for _, gr, _ in layers for _ in range(R) for g in gr]
-    eng = ra.Engine(G_all, H_all, cfg)
-    q = torch.cat([dq[:R].reshape(R * dq.shape[1], -1) for _, _, dq in layers]).contiguous()
-    for _ in range(3):
-        eng.decode_step_device(q)
+    cfg = ra.EngineConfig(128, 512, a.top_k, a.ef)
+    if samples is None:  # 8 contexts spread over the line (32 heads)
+        samples = tuple(sorted({int(round(i * (len(ctxs) - 1) / 7)) for i in range(8)}))
+    t0 = time.time()
+    kvs, graphs, qs, host = [], [], [], {}
+    build_ms = []
+    for ci, (l, seed, g) in enumerate(ctxs):
+        spec = WorkloadSpec(n_ctx=n_ctx, d_model=256, d_head=128, n_heads=a.heads,
+                            n_kv_groups=a.groups, seed=seed, n_decode=n_dec)
+        w = generate_group(spec, g, dev)
+        kv = ra.KVGroup(w["keys"], w["values"])
+        kvs.append(kv)
+        for m in range(hpg):
+            tb = time.time()
+            graphs.append(ra.ood_build(kv, w["prefill_q"][m], bp))
+            build_ms.append((time.time() - tb) * 1e3)
+            qs.append(w["decode_q"][m])
+        if ci in samples:
+            host[ci] = (w["keys"].cpu().numpy(), w["values"].cpu().numpy())
+        del w
     torch.cuda.synchronize()
-    times, s_ms, sc, ex = [], [], [], []
-    for _ in range(max(3, min(a.steps, 10))):
-        flush.zero_()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        eng.decode_step_device(q)
-        e1.record(stream)
-        e1.synchronize()
-        times.append(e0.elapsed_time(e1))
-        s_ms.append(eng.last_timing()[0])
-        s, e = eng.last_stats()
-        sc.append(s)
-        ex.append(e)
-    ms, ms_s = statistics.mean(times), statistics.mean(s_ms)
-    nq = len(H_all)
-    by = statistics.mean([s * 512 + e * a.max_degree * 4 for s, e in zip(sc, ex)])
+    setup_s = time.time() - t0
+    Q = torch.stack(qs, dim=1).contiguous()  # [n_dec, heads, d]
+    del qs
+    n_l = len(ctxs) // per_layer
+    hl = per_layer * hpg  # heads per layer
+    eng = ra.Engine(kvs, graphs, cfg)
+    per = [ra.Engine(kvs[i * per_layer:(i + 1) * per_layer], graphs[i * hl:(i + 1) * hl], cfg)
+           for i in range(n_l)] if n_l > 1 else [eng]
+
+    def serial(i):
+        for j, e in enumerate(per):
+            e.decode_step_device(Q[i, j * hl:(j + 1) * hl])
+
+    for i in range(a.warmup):
+        eng.decode_step_device(Q[i])
+        serial(i)
+    eng.last_timing(), eng.last_stats()
+    torch.cuda.synchronize()
+    t_b, s_b, sc, ex, t_s = [], [], [], [], []
+    with ClockSampler(dev.index or 0) as clk:
+        for i in range(a.warmup, a.warmup + a.steps):
+            t_b.append(timed(lambda: eng.decode_step_device(Q[i]), stream, flush))
+            s_b.append(eng.last_timing()[0])
+            s_, e_ = eng.last_stats()
+            sc.append(s_)
+            ex.append(e_)
+            t_s.append(timed(lambda: serial(i), stream, flush))
+    i0 = a.warmup
+    out, om, scn = (x.cpu().numpy() for x in eng.decode_step_device(Q[i0]))
+    for ci in sorted(host):
+        hs = slice(ci * hpg, (ci + 1) * hpg)
+        parity_jobs.append({"line": name, "ctx": ci, "keys": host[ci][0], "values": host[ci][1],
+                            "blobs": [g.serialize() for g in graphs[hs]],
+                            "q": Q[i0, hs].cpu().numpy(), "out": out[hs],
+                            "omega": om[hs].view(np.uint32), "scanned": scn[hs],
+                            "cfg": cfg})
+    nH = len(graphs)
+    d, M = 128, a.max_degree
+    k = eng.k
+    by_search = statistics.mean([s_ * d * 4 + e_ * M * 4 for s_, e_ in zip(sc, ex)])
+    nW = min(128, n_ctx) + min(512, max(n_ctx - 128, 0))
+    by_attn = len(ctxs) * nW * d * 8 + nH * k * d * 4  # W K+V once per group, Omega V rows
+    fused = eng.kernels_per_step() == 1
+    by_kernel = by_search + (by_attn if fused else 0)  # the fused kernel also does attention
+    ms_b, ms_s, ms_ser = statistics.mean(t_b), statistics.mean(s_b), statistics.mean(t_s)
     peak, kind = measured_peaks()
-    gbs = by / (ms_s * 1e-3) / 1e9
-    del eng
-    return {"layers": n_layers, "decode_queries_per_head_per_layer": R, "queries_per_step": nq,
-            "ms_per_step": round(ms, 4), "us_per_query": round(ms * 1e3 / nq, 3),
-            "queries_per_s": round(nq / (ms * 1e-3), 1), "search_ms": round(ms_s, 4),
-            "search_GBps": round(gbs, 1), "search_frac": round(gbs / peak, 4),
-            "peak_source": kind,
-            "note": "distinct synthetic layers (own K/V and graphs); one engine step"}
+    gbs = by_kernel / (ms_s * 1e-3) / 1e9
+    summ = ncu_summary(f"ncu_{name}_summary.json")
+    traffic = summ.get("dram_bytes_per_launch")
+    res = {
+        "workload": desc, "contexts": len(ctxs), "heads": nH, "n_ctx": n_ctx,
+        "value": round(ms_b, 4), "unit": "ms/step (layer-batched: one engine step over all "
+                                           "heads)",
+        "layer_serial_ms": round(ms_ser, 4),
+        "layer_serial_note": f"{n_l} engine steps of {hl} heads back to back (the layer "
+                             "dependency chain of real decode)",
+        "tokens_per_step": 8 if name == "batch8" else 1,
+        "searches_per_s": round(nH / (ms_b * 1e-3), 1),
+        "kernels_per_step_batched": eng.kernels_per_step(),
+        "roofline": {"bound": "hbm", "kernel": "k_graph_search_pipe (" +
+                     ("latency mode, fused attention" if fused else "search only") + ")",
+                     "achieved": round(gbs, 2), "peak": peak, "unit": "GB/s",
+                     "frac": round(gbs / peak, 4), "peak_source": kind, "traffic": traffic,
+                     "traffic_over_algorithmic": (round(traffic / by_kernel, 3)
+                                                  if traffic else None),
+                     "algorithmic_bytes_per_launch": int(by_kernel),
+                     "kernel_ms": round(ms_s, 4)},
+        "step_GBps": round((by_search + by_attn) / (ms_b * 1e-3) / 1e9, 1),
+        "step_frac": round((by_search + by_attn) / (ms_b * 1e-3) / 1e9 / peak, 4),
+        "attention_bytes_per_step": int(by_attn),
+        "mean_scanned_per_head": round(statistics.mean(sc) / nH, 1),
+        "mean_expanded_per_head": round(statistics.mean(ex) / nH, 1),
+        "clocks": clk.summary(), "setup_s": round(setup_s, 1),
+        "build_ms_per_head": round(statistics.mean(build_ms), 2),
+        "hbm_resident_bytes": int(len(ctxs) * n_ctx * d * 8 +
+                                  sum(g.device_bytes() for g in graphs)),
+    }
+    if summ:
+        res["roofline"]["ncu"] = {k2: v for k2, v in summ.items() if k2 != "dram_bytes_per_launch"}
+    del per, eng, kvs, graphs, Q
+    import gc
+    gc.collect()
+    torch.cuda.synchronize()
+    return res
 
 
 def bf16_mode(a, ra, spec, my_groups, hpg, Q, cfg, flush, stream, out32, graphs32):
@@ -542,14 +653,11 @@ def bf16_mode(a, ra, spec, my_groups, hpg, Q, cfg, flush, stream, out32, graphs3
         rel = np.linalg.norm(o - out32, axis=1) / np.linalg.norm(out32, axis=1)
         rb = 256 if mode == "bf16" else 512
         by = statistics.mean([s_ * rb + e_ * a.max_degree * 4 for s_, e_ in zip(sc, ex)])
-        tput = batched_throughput(a, ra, kvs, graphs, Q, cfg, flush, stream, row_bytes=rb)
         del eng
         res[mode] = {"value": round(statistics.mean(times), 4), "unit": "ms/token",
                      "search_ms": round(statistics.mean(s_ms), 4),
                      "search_GBps": round(by / (statistics.mean(s_ms) * 1e-3) / 1e9, 1),
-                     "out_rel_vs_f32": {"max": float(rel.max()), "mean": float(rel.mean())},
-                     "throughput_us_per_query": tput["us_per_query"],
-                     "throughput_search_GBps": tput["search_GBps"]}
+                     "out_rel_vs_f32": {"max": float(rel.max()), "mean": float(rel.mean())}}
     res["note"] = ("bf16: K/V rounded in HBM, graphs rebuilt on the rounded keys (= the "
                    "reference on the rounded inputs); bf16_attn: exact f32 search (same ids), "
                    "bf16 K/V in the attention; north-star bf16 tolerance 1e-2")
@@ -583,25 +691,29 @@ def recall(eng, graphs, kvs, Q, a, ra):
             "ef": a.ef, "ground_truth": "ra_flat_search_batch (GPU FlatIndex)"}
 
 
-def _ref_engine(keys_host, vals_host, graphs, cfg, threads):
+def _ref_engine(keys_host, vals_host, blobs, cfg, threads):
     from oracle.ffi import Oracle, available
     if not available("ref"):
         return None, None
     o = Oracle("ref")
-    blobs = [g.serialize() for g in graphs]
     eng = o.engine(np.stack(keys_host), np.stack(vals_host), blobs, cfg.s_init, cfg.s_local,
-                   cfg.top_k, cfg.search_param, threads)
+                   cfg.top_k, -1 if cfg.search_param is None else cfg.search_param, threads)
     return o, eng
 
 
-def cpu_baseline(a, keys_host, vals_host, graphs, Q, cfg, eng):
-    """The reference's own decode_step (oracle/_ref, unmodified sources) on the
-    host cores over the same graphs (loaded through OODGraph(keys, blob)),
-    bounded to ~cpu_seconds; doubles as a full-size parity check."""
+def cpu_baseline(a, keys_host, vals_host, graphs, Q, cfg, parity_jobs):
+    """CPU baseline leg (rank 0, N=1): the reference's own decode_step
+    (oracle/_ref, unmodified sources) on the host cores over the same graphs
+    (loaded through OODGraph(keys, blob)), bounded to ~cpu_seconds; plus the
+    single-thread latency of one reference OODGraph::search. Doubles as the
+    full-size parity check: the headline engine's outputs and every sampled
+    head of the further lines against the reference decode_step."""
+    import paper_2409_10516_b200 as ra
     threads = os.cpu_count() or 1
-    o, reng = _ref_engine(keys_host, vals_host, graphs, cfg, threads)
+    o, reng = _ref_engine(keys_host, vals_host, [g.serialize() for g in graphs], cfg, threads)
     if reng is None:
         return {"value": None, "unavailable": "oracle/_ref not built"}, None
+    eng = ra.Engine([g.keys for g in graphs[::cfg_hpg(a)]], graphs, cfg)
     Qh = Q.cpu().numpy()
     times, same_om, same_sc, max_rel, n = [], 0, 0, 0.0, 0
     t_end = time.time() + a.cpu_seconds
@@ -619,46 +731,112 @@ def cpu_baseline(a, keys_host, vals_host, graphs, Q, cfg, eng):
             max_rel = max(max_rel, float(rel.max()))
             n += q.shape[0]
         i += 1
+    del eng
+    # single-thread latency of one search (index_oodgraph.cpp:357-411), head 0
+    W = ra.static_partition(a.n_ctx, 128, 512).static_set
+    og = o.graph(keys_host[0], graphs[0].serialize(), a.ef)
+    st = []
+    for j in range(min(Q.shape[0], 32)):
+        t0 = time.perf_counter()
+        og.search(Qh[j, 0], a.top_k, W, a.ef)
+        st.append((time.perf_counter() - t0) * 1e3)
+    og.close()
     base = {"value": round(statistics.mean(times), 3), "unit": "ms/token", "cores": threads,
-            "kind": "reference",
+            "kind": "reference", "cpu_model": cpu_model(),
+            "single_thread_search_ms": round(statistics.median(st), 4),
             "sample": f"{len(times)} decode steps x {Qh.shape[1]} heads at n_ctx {a.n_ctx} "
-                      f"(reference decode_step, n_threads={threads}, GPU-built graphs via OODG)"}
+                      f"(reference decode_step, n_threads={threads}, GPU-built graphs via OODG); "
+                      f"single-thread search: median of {len(st)} OODGraph::search calls "
+                      f"(k {a.top_k}, ef {a.ef}, Mask W)"}
     parity = None if a.no_parity else {
         "heads_checked": n, "omega_identical": same_om, "scanned_identical": same_sc,
         "max_out_rel_err": max_rel}
+    if parity is not None and parity_jobs:
+        parity["lines"] = line_parity(o, parity_jobs, threads)
     return base, parity
 
 
-def run_reference(a, keys_host, vals_host, graphs, Q, cfg, H, G, setup_s):
-    threads = os.cpu_count() or 1
-    o, reng = _ref_engine(keys_host, vals_host, graphs, cfg, threads)
-    if reng is None:
+def cfg_hpg(a):
+    return a.heads // a.groups
+
+
+def line_parity(o, jobs, threads):
+    """Sampled heads of the multi-context lines vs the reference decode_step
+    on the same K/V, graphs (OODG blobs) and queries."""
+    res = {}
+    for j in jobs:
+        cfg = j["cfg"]
+        reng = o.engine(j["keys"][None], j["values"][None], j["blobs"], cfg.s_init, cfg.s_local,
+                        cfg.top_k, -1 if cfg.search_param is None else cfg.search_param, threads)
+        rout, rom, rsc = reng.step(np.ascontiguousarray(j["q"]), 0)
+        del reng
+        r = res.setdefault(j["line"], {"heads_checked": 0, "omega_identical": 0,
+                                       "scanned_identical": 0, "max_out_rel_err": 0.0,
+                                       "contexts": []})
+        om = j["omega"]
+        r["heads_checked"] += len(om)
+        r["omega_identical"] += int((om == rom[:, : om.shape[1]]).all(axis=1).sum())
+        r["scanned_identical"] += int((j["scanned"].astype(np.uint64) == rsc).sum())
+        rel = np.linalg.norm(j["out"] - rout, axis=1) / np.linalg.norm(rout, axis=1)
+        r["max_out_rel_err"] = max(r["max_out_rel_err"], float(rel.max()))
+        r["contexts"].append(j["ctx"])
+    return res
+
+
+def run_reference(a):
+    """--impl reference: the reference's own CPU path end to end, rank 0 only.
+    oracle/_ref is the unmodified reference sources (Eigen/doctest shims):
+    generate_workload (seed 7) -> engine_init's per-head ood_build ->
+    decode_step with all host threads. No code of this repo's package, no
+    GPU, on this path."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # the reference CPU arm runs on rank 0 only
+    sys.path.insert(0, ROOT)
+    from oracle.ffi import BuildParams, Oracle, available
+    if not available("ref"):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    Qh = Q.cpu().numpy()
+    threads = os.cpu_count() or 1
+    o = Oracle("ref")
+    n_dec = a.warmup + a.steps
+    t0 = time.time()
+    reng, dq, _, _, ms_gen, ms_build = o.engine_from_workload(
+        a.n_ctx, a.heads, a.groups, 7, n_dec,
+        BuildParams(a.k_train, a.max_degree, a.ef_construction, 8), 128, 512, a.top_k, a.ef,
+        threads, a.ref_build_workers)
+    setup_s = time.time() - t0
     for i in range(a.warmup):
-        reng.step(np.ascontiguousarray(Qh[i]), i)
+        reng.step(np.ascontiguousarray(dq[:, i, :]), i)
     times = []
     t_start = time.perf_counter()
     for i in range(a.warmup, a.warmup + a.steps):
-        t0 = time.perf_counter()
-        reng.step(np.ascontiguousarray(Qh[i]), i)
-        times.append((time.perf_counter() - t0) * 1e3)
+        q = np.ascontiguousarray(dq[:, i, :])
+        t1 = time.perf_counter()
+        reng.step(q, i)
+        times.append((time.perf_counter() - t1) * 1e3)
     ms = statistics.mean(times)
+    H, G = a.heads, a.groups
     sample = (f"{a.steps} reference decode_steps x {H} heads at n_ctx {a.n_ctx} "
-              f"(n_threads={threads}; graphs built on GPU, loaded via OODG blobs)")
+              f"(n_threads={threads}; graphs built by the reference's ood_build)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(ms, 3), "unit": "ms/token",
-        "n_gpus": 1, "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 3),
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference OOD generator algorithm, seed 7)",
-        "config": dict(workload_config(a, H, G),
-                       parallelism="reference decode_step on the host cores (rank 0)"),
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": False, "scaling": "strong" if a.shard == "heads" and a.gpus > 1
+        else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: the reference's own generate_workload (workload.cpp:102-203), "
+                "seed 7",
+        "config": workload_config(a, H, G),
+        "execution": "reference generate_workload + ood_build per head "
+                     f"({a.ref_build_workers} heads at a time, {max(1, threads // max(1, a.ref_build_workers))} "
+                     "threads each) + decode_step (engine.cpp:105-115) on the host cores "
+                     "(oracle/_ref: unmodified reference sources, shimmed Eigen/doctest)",
         "cpu_baseline": {"value": round(ms, 3), "unit": "ms/token", "cores": threads,
-                         "kind": "reference", "sample": sample},
+                         "kind": "reference", "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": round(ms, 3), "unit": "ms/token", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "wall_s": round(time.perf_counter() - t_start, 2), "setup_s": round(setup_s, 1)}))
+        "wall_s": round(time.perf_counter() - t_start, 2), "setup_s": round(setup_s, 1),
+        "setup_ms": {"generate_workload": round(ms_gen, 1), "graph_builds": round(ms_build, 1)}}))
 
 
 if __name__ == "__main__":

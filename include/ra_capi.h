@@ -222,10 +222,14 @@ ra_status ra_engine_create(ra_ctx* ctx, ra_kv* const* groups, uint32_t n_groups,
                            const ra_engine_config* cfg, ra_engine** out);
 void ra_engine_destroy(ra_engine* e);
 /* decode_step on DEVICE buffers: q [H][d] f32 -> out [H][d] f64; omega
- * [H][top_k] u32 (UINT32_MAX padded) and scanned [H] u64 may be NULL. */
+ * [H][k] u32 with row stride k = ra_engine_k(e) = min(top_k, |dynamic pool|)
+ * (UINT32_MAX padded past a head's n_out) and scanned [H] u64 may be NULL. */
 ra_status ra_engine_step_device(ra_engine* e, const float* q, double* out, uint32_t* omega,
                                 uint64_t* scanned);
-/* decode_step on HOST buffers: q in, out/omega/scanned back, synchronized.
+/* Row stride of the omega output: min(top_k, |dynamic pool|) (engine.cpp:80). */
+uint32_t ra_engine_k(const ra_engine* e);
+/* decode_step on HOST buffers (same shapes as ra_engine_step_device): q in,
+ * out/omega/scanned back, synchronized.
  * This is the drop-in call a CPU-side engine makes. When every buffer is
  * page-locked host memory (cudaHostAlloc / cudaHostRegister / torch
  * pin_memory) the kernels read q and write the results across the bus

@@ -125,6 +125,12 @@ class Oracle:
                                            C.c_uint64, C.c_uint32, C.c_int64, C.c_int,
                                            C.POINTER(C.c_void_p)]
             L("engine_step").argtypes = [C.c_void_p, f32p, C.c_uint64, f64p, u32p, u64p]
+            L("engine_from_workload").argtypes = (
+                [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64] + [C.c_uint32] * 4
+                + [C.c_uint64, C.c_uint64, C.c_uint32, C.c_int64, C.c_int, C.c_int]
+                + [f32p, f32p, f32p, f64p, f64p, C.POINTER(C.c_void_p)])
+            L("engine_graph_serialize").argtypes = [C.c_void_p, C.c_uint32, C.c_char_p,
+                                                    C.c_uint64, u64p]
             L("engine_free").argtypes = [C.c_void_p]
         else:
             L("training_knn").argtypes = [f32p, C.c_uint64, C.c_uint32, f32p, C.c_uint64,
@@ -264,6 +270,32 @@ class Oracle:
         return RefEngine(self, keys, values, blobs, s_init, s_local, top_k, ef, n_threads)
 
 
+    def engine_from_workload(self, n_ctx, n_heads=32, n_kv_groups=8, seed=7, n_decode=64,
+                             params: "BuildParams" = None, s_init=128, s_local=512,
+                             top_k=100, ef=-1, n_threads=1, build_workers=1,
+                             keep_kv=False):
+        """The reference's own setup: generate_workload + engine_init
+        (OODGraph). Returns (engine, decode_q [H, n_decode, d], keys, values,
+        ms_gen, ms_build); keys/values are None unless keep_kv."""
+        assert self.kind == "ref"
+        p = params or BuildParams()
+        d = 128
+        dq = np.zeros((n_heads, n_decode, d), np.float32)
+        K = np.zeros((n_kv_groups, n_ctx, d), np.float32) if keep_kv else None
+        V = np.zeros((n_kv_groups, n_ctx, d), np.float32) if keep_kv else None
+        h = C.c_void_p()
+        mg, mb = C.c_double(), C.c_double()
+        self._check(self._f("engine_from_workload")(
+            n_ctx, n_heads, n_kv_groups, seed, n_decode, p.k_train, p.max_degree,
+            p.ef_construction, p.edge_window, s_init, s_local, top_k, ef, n_threads,
+            build_workers, _ptr(dq, f32p), _ptr(K, f32p) if keep_kv else None,
+            _ptr(V, f32p) if keep_kv else None, C.byref(mg), C.byref(mb), C.byref(h)))
+        eng = RefEngine.__new__(RefEngine)
+        eng.o, eng.h, eng.H, eng.d, eng.top_k = self, h, n_heads, d, top_k
+        eng.keys = eng.values = None
+        return eng, dq, K, V, mg.value, mb.value
+
+
 class _OraGraph(C.Structure):
     _fields_ = [("n", C.c_uint64), ("d", C.c_uint32), ("max_degree", C.c_uint32),
                 ("default_ef", C.c_uint32), ("entry", C.c_uint64),
@@ -369,6 +401,14 @@ class RefEngine:
         self.o._check(self.o._f("engine_step")(self.h, _ptr(q, f32p), step, _ptr(out, f64p),
                                                _ptr(om, u32p), _ptr(sc, u64p)))
         return out, om, sc
+
+    def graph_blob(self, h: int) -> bytes:
+        size = C.c_uint64()
+        self.o._check(self.o._f("engine_graph_serialize")(self.h, h, None, 0, C.byref(size)))
+        buf = C.create_string_buffer(size.value)
+        self.o._check(self.o._f("engine_graph_serialize")(self.h, h, buf, size.value,
+                                                          C.byref(size)))
+        return buf.raw[: size.value]
 
     def __del__(self):
         try:

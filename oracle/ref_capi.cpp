@@ -311,6 +311,95 @@ int ref_engine_create(const float* keys, const float* values, uint64_t t, uint32
   });
 }
 
+// The reference's whole decode setup, nothing from this repo:
+// generate_workload (workload.cpp:102-203) + engine_init (engine.cpp:23-65,
+// OODGraph kind: static_partition + ood_build per head over the group's
+// shared keys). build_workers <= 1 is engine_init itself (heads built one
+// after another, each ood_build with n_threads); build_workers > 1 builds
+// that many heads at once through the same public ood_build
+// (index_oodgraph.hpp:78-81), n_threads / build_workers threads each, to
+// overlap the builder's serial phase-2 sort. decode_q receives
+// [n_heads][n_decode][d_head]; keys / values (nullable) [n_groups][n_ctx][d].
+int ref_engine_from_workload(uint64_t n_ctx, uint32_t n_heads, uint32_t n_kv_groups,
+                             uint64_t seed, uint64_t n_decode, uint32_t k_train,
+                             uint32_t max_degree, uint32_t ef_construction,
+                             uint32_t edge_window, uint64_t s_init, uint64_t s_local,
+                             uint32_t top_k, int64_t ef, int n_threads, int build_workers,
+                             float* decode_q, float* keys, float* values, double* ms_gen,
+                             double* ms_build, void** out) {
+  return guard([&] {
+    using clk = std::chrono::steady_clock;
+    WorkloadSpec s;
+    s.n_ctx = n_ctx;
+    s.n_heads = n_heads;
+    s.n_kv_groups = n_kv_groups;
+    s.seed = seed;
+    s.n_decode = n_decode;
+    auto t0 = clk::now();
+    auto w = generate_workload(s, n_threads);
+    auto t1 = clk::now();
+    EngineConfig c;
+    c.s_init = s_init;
+    c.s_local = s_local;
+    c.top_k = top_k;
+    c.index_kind = IndexKind::OODGraph;
+    c.graph.k_train = k_train;
+    c.graph.max_degree = max_degree;
+    c.graph.ef_construction = ef_construction;
+    c.graph.edge_window = edge_window;
+    if (ef >= 0) c.search_param = uint32_t(ef);
+    c.n_threads = n_threads;
+    auto e = std::make_unique<RefEngine>();
+    if (build_workers <= 1) {
+      e->st = engine_init(w, c);
+    } else {
+      e->st.config = c;
+      e->st.t = n_ctx;
+      e->st.heads.resize(w.size());
+      for (size_t h = 0; h < w.size(); ++h) {
+        HeadState& hs = e->st.heads[h];
+        hs.head_id = w[h].head_id;
+        hs.kv_group_id = w[h].kv_group_id;
+        hs.partition = static_partition(n_ctx, s_init, s_local);
+        hs.keys = w[h].keys;
+        hs.values = w[h].values;
+        e->st.decode_queries.push_back(w[h].decode_queries);
+      }
+      const int per = std::max(1, n_threads / build_workers);
+      parallel_for(w.size(), build_workers, [&](size_t h) {
+        e->st.heads[h].index = ood_build(w[h].keys, w[h].prefill_queries, c.graph, per);
+      });
+    }
+    auto t2 = clk::now();
+    const uint32_t d = s.d_head;
+    const size_t per_dec = size_t(n_decode) * d, per_ctx = size_t(n_ctx) * d;
+    for (uint32_t h = 0; h < n_heads; ++h) {
+      std::memcpy(decode_q + h * per_dec, w[h].decode_queries.data.data(),
+                  per_dec * sizeof(float));
+      const uint32_t g = w[h].kv_group_id;
+      if (keys)
+        std::memcpy(keys + g * per_ctx, w[h].keys->data.data(), per_ctx * sizeof(float));
+      if (values)
+        std::memcpy(values + g * per_ctx, w[h].values->data.data(), per_ctx * sizeof(float));
+    }
+    if (ms_gen) *ms_gen = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    if (ms_build) *ms_build = std::chrono::duration<double, std::milli>(t2 - t1).count();
+    *out = e.release();
+  });
+}
+
+// OODG blob of head h of an engine (the parity artefact of its graph)
+int ref_engine_graph_serialize(void* e, uint32_t h, char* buf, uint64_t cap, uint64_t* size) {
+  return guard([&] {
+    const auto& st = static_cast<RefEngine*>(e)->st;
+    const auto* g = dynamic_cast<const OODGraph*>(st.heads.at(h).index.get());
+    if (!g) throw std::runtime_error("not an OODGraph head");
+    const std::string b = g->serialize();
+    *size = b.size();
+    if (buf && cap >= b.size()) std::memcpy(buf, b.data(), b.size());
+  });
+}
+
 void ref_engine_free(void* e) { delete static_cast<RefEngine*>(e); }
 
 // One decode_step over all heads: q [n_heads][d] -> out [n_heads][d] f64,

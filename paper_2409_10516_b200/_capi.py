@@ -107,6 +107,7 @@ _SIGS = {
     "ra_engine_last_stats": (C.c_int, [c_vp, c_u64p, c_u64p]),
     "ra_engine_last_timing": (C.c_int, [c_vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "ra_engine_kernels_per_step": (C.c_uint32, [c_vp]),
+    "ra_engine_k": (C.c_uint32, [c_vp]),
     "ra_engine_debug_counters": (C.c_int, [c_vp, c_u64p]),
     "ra_engine_debug_counters_per_head": (C.c_int, [c_vp, c_u64p]),
 }

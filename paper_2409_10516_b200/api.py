@@ -689,8 +689,10 @@ class Engine:
         """decode_step (engine.cpp:105-115) from host queries [H, d]:
         returns (out [H,d] f64, omega [H,k] u32, scanned [H] u64) on the host."""
         q = np.ascontiguousarray(queries, np.float32)
-        if q.shape[0] != self.H:
+        if q.ndim != 2 or q.shape[0] != self.H:
             raise InvalidArgument("one query per head required")
+        if q.shape[1] != self.d:  # the C call reads exactly H * d floats
+            raise InvalidArgument("query dimension mismatch")
         out = np.empty((self.H, self.d), np.float64)
         om = np.empty((self.H, max(self.k, 1)), np.uint32)
         sc = np.empty(self.H, np.uint64)

@@ -491,7 +491,6 @@ struct ra_engine {
   } sg[2];
   bool graphs_off = false;
   cudaStream_t cap_stream = nullptr;  // capture happens here (the legacy stream can't capture)
-  uint64_t* last_scanned = nullptr;   // where the last step's scanned went (device or mapped host)
   ra_ctx* ctx = nullptr;
   uint32_t H = 0, G = 0, d = 0, k = 0;
   uint64_t t = 0, n_pool = 0, n_static = 0;
@@ -690,7 +689,6 @@ void record_timing(cudaEvent_t ev, cudaStream_t s) {
 void engine_enqueue(ra_engine* e, const float* q_dev, double* out_dev, uint32_t* ids_dev,
                     uint64_t* scanned_dev, uint32_t* ids_copy = nullptr) {
   ra_ctx* ctx = e->ctx;
-  e->last_scanned = scanned_dev;
   cudaStream_t s = ctx->stream;
   const uint32_t H = e->H, d = e->d;
   EngineAttn ea{};
@@ -709,6 +707,7 @@ void engine_enqueue(ra_engine* e, const float* q_dev, double* out_dev, uint32_t*
     sa.scores64 = e->scores64.p;
     sa.n_out = e->n_out.p;
     sa.scanned = scanned_dev;
+    sa.scanned_own = scanned_dev == e->scanned.p ? nullptr : e->scanned.p;
     sa.truncated = e->truncated.p;
     sa.expanded = e->expanded.p;
     sa.dbg = e->dbg.p;
@@ -748,6 +747,7 @@ void engine_enqueue(ra_engine* e, const float* q_dev, double* out_dev, uint32_t*
     sa.scores64 = e->scores64.p;
     sa.n_out = e->n_out.p;
     sa.scanned = scanned_dev;
+    sa.scanned_own = scanned_dev == e->scanned.p ? nullptr : e->scanned.p;
     sa.truncated = e->truncated.p;
     sa.expanded = e->expanded.p;
     sa.dbg = e->dbg.p;
@@ -755,6 +755,7 @@ void engine_enqueue(ra_engine* e, const float* q_dev, double* out_dev, uint32_t*
   } else {
     RA_CUDA(cudaMemsetAsync(e->n_out.p, 0, H * 4, s));
     RA_CUDA(cudaMemsetAsync(scanned_dev, 0, H * 8, s));
+    if (scanned_dev != e->scanned.p) RA_CUDA(cudaMemsetAsync(e->scanned.p, 0, H * 8, s));
     RA_CUDA(cudaMemsetAsync(e->expanded.p, 0, H * 4, s));
   }
   record_timing(e->ev[1], s);
@@ -943,14 +944,18 @@ ra_status ra_engine_last_stats(ra_engine* e, uint64_t* total_scanned, uint64_t* 
     DeviceGuard dg(e->ctx->device);
     std::vector<uint64_t> sc(e->H);
     std::vector<uint32_t> ex(e->H);
-    RA_CUDA(cudaMemcpyAsync(sc.data(), e->last_scanned ? e->last_scanned : e->scanned.p, e->H * 8,
-                            cudaMemcpyDefault, e->ctx->stream));
+    // the kernels also write scanned into the engine's own buffer, so this
+    // never reads through the caller's (possibly freed) output buffer
+    RA_CUDA(cudaMemcpyAsync(sc.data(), e->scanned.p, e->H * 8, cudaMemcpyDeviceToHost,
+                            e->ctx->stream));
     RA_CUDA(cudaMemcpyAsync(ex.data(), e->expanded.p, e->H * 4, cudaMemcpyDeviceToHost, e->ctx->stream));
     RA_CUDA(cudaStreamSynchronize(e->ctx->stream));
     if (total_scanned) *total_scanned = std::accumulate(sc.begin(), sc.end(), uint64_t(0));
     if (total_expanded) *total_expanded = std::accumulate(ex.begin(), ex.end(), uint64_t(0));
   });
 }
+
+uint32_t ra_engine_k(const ra_engine* e) { return e ? e->k : 0u; }
 
 uint32_t ra_engine_kernels_per_step(const ra_engine* e) {
   return !e ? 0u : e->fused ? 1u : e->fast_attn ? 3u : 4u;

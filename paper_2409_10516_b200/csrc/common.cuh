@@ -209,6 +209,7 @@ struct SearchArgs {
   double* scores64;           // optional [B][k] exact f64 scores
   uint32_t* n_out;            // [B]
   uint64_t* scanned;          // [B]
+  uint64_t* scanned_own;      // [B] optional second copy (engine-owned, read by last_stats)
   uint8_t* truncated;         // [B]
   uint32_t* expanded;         // optional [B]
   uint64_t* dbg;              // optional [B][4]: rounds, cycles A, cycles B, commits

@@ -416,6 +416,7 @@ __global__ void __launch_bounds__(128, 1) k_graph_search(SearchArgs a, uint32_t 
   if (lane == 0) {
     a.n_out[b] = take;
     a.scanned[b] = scanned;
+    if (a.scanned_own) a.scanned_own[b] = scanned;
     a.truncated[b] = take < k;
     if (a.expanded) a.expanded[b] = expanded;
   }
@@ -958,6 +959,7 @@ __global__ void __launch_bounds__(kCW * 32, 1)
   if (lane == 0) {
     a.n_out[b] = take;
     a.scanned[b] = scanned;
+    if (a.scanned_own) a.scanned_own[b] = scanned;
     a.truncated[b] = take < k;
     if (a.expanded) a.expanded[b] = expanded;
   }

@@ -16,11 +16,13 @@
 // equality is double equality); (key desc, id asc) is the reference order.
 //
 // Commit-side state, every operation a few independent instructions:
-//   F (frontier): unexpanded visited nodes with key >= thr. kFR entries per
-//     lane in registers, SORTED per lane (insert = one compare per slot plus
-//     predicated moves, pop = shift); a lane that overflows pushes its worst
-//     entry to the shared overflow FO, whose best entry is tracked exactly.
-//     Frontier top = 3-REDUX argmax of the lane heads vs FO's best.
+//   F (frontier): unexpanded visited nodes with key >= thr, kept as per-lane
+//     UNSORTED lists in shared memory (kFR entries per lane, column layout;
+//     helpers read them directly), each lane's best entry (its head) cached
+//     in registers. Insert = one store plus one head compare; a full lane
+//     hands new entries to the shared overflow FO, whose best entry is
+//     tracked exactly. Frontier top = 3-REDUX argmax of the lane heads vs
+//     FO's best; after a pop the owner lane's new head is rescanned.
 //   U (pool candidates): unmasked visited nodes with key >= thr, kUR per
 //     lane (unsorted, free mask) + overflow UO. pool.full() <=> #unmasked
 //     visited >= ef, and top < pool.worst (:390) <=> #{u in U : u > top} >=
@@ -29,8 +31,9 @@
 //     (key bisection, raised when U outgrows ef + slack). Nodes below the
 //     pool worst can never be popped (the stop rule fires first) nor enter
 //     the pool (its worst only rises), so dropping them is exact.
-// Helpers: read the published lane heads (a hint of the next tops), claim a
-// slot of a direct-mapped packet table with one 64-bit CAS, gather the
+// Helpers: read the frontier lists and the hint ring (likely next tops),
+// claim a way of a 2-way set-associative packet table with one 64-bit CAS,
+// gather the
 // adjacency row, TMA the unvisited neighbours' key rows into their tile,
 // run the exact chains, publish the packet; then chain greedily into the
 // best new neighbour (the likely next top) while it ranks among the heads.
@@ -69,7 +72,9 @@ constexpr int kFR = 8;             // frontier entries per lane (sorted)
 #ifndef RA_HINTS
 #define RA_HINTS 64
 #endif
-constexpr uint32_t kHintN = RA_HINTS;  // hint ring entries (a multiple of 32)
+constexpr uint32_t kHintN = RA_HINTS;  // hint ring entries (a power of two >= 32)
+static_assert((kHintN & (kHintN - 1)) == 0 && kHintN >= 32,
+              "the hint ring index is masked with kHintN - 1");
 constexpr int kUR = 8;             // pool-candidate entries per lane
 #ifndef RA_PIPE_SLOT_BITS
 #define RA_PIPE_SLOT_BITS 7
@@ -995,6 +1000,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     const uint32_t pool = uint32_t(u_total < ef ? u_total : ef);
     if (lane == 0) {
       a.scanned[b] = scanned;
+      if (a.scanned_own) a.scanned_own[b] = scanned;
       if (a.expanded) a.expanded[b] = expanded;
     }
     if constexpr (TP) {
