@@ -82,6 +82,12 @@ void ra_ctx_destroy(ra_ctx* ctx);
  * enqueued on it; calls taking host buffers synchronize it before returning. */
 ra_status ra_ctx_set_stream(ra_ctx* ctx, void* stream);
 ra_status ra_ctx_synchronize(ra_ctx* ctx);
+/* Graph-search kernel variant for this ctx (overrides RA_SEARCH_KERNEL):
+ * "auto" (latency mode up to 2 x SMs queries, then throughput mode),
+ * "lat", "tp", "tps" (throughput, shared-memory visited bits + TMA row
+ * tiles), "tpr" (throughput, register rows), "cta", "warp"; NULL = default.
+ * Every variant returns identical results. Engines read it at creation. */
+ra_status ra_ctx_set_search_kernel(ra_ctx* ctx, const char* name);
 
 /* ---- KV groups (types.hpp:18-35, 54-61) ------------------------------------
  * keys/values: n x d f32 row-major; values may be NULL (search-only).

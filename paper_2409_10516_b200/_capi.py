@@ -49,6 +49,7 @@ _SIGS = {
     "ra_ctx_destroy": (None, [c_vp]),
     "ra_ctx_set_stream": (C.c_int, [c_vp, c_vp]),
     "ra_ctx_synchronize": (C.c_int, [c_vp]),
+    "ra_ctx_set_search_kernel": (C.c_int, [c_vp, C.c_char_p]),
     "ra_kv_create": (C.c_int, [c_vp, c_vp, c_vp, C.c_uint64, C.c_uint32, C.c_int,
                                C.POINTER(c_vp)]),
     "ra_kv_create_bf16": (C.c_int, [c_vp, c_vp, c_vp, C.c_uint64, C.c_uint32, C.c_int,

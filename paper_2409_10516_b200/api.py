@@ -75,6 +75,12 @@ class Context:
     def synchronize(self):
         _check(lib.ra_ctx_synchronize(self.h))
 
+    def set_search_kernel(self, name: Optional[str]):
+        """Graph-search kernel variant for this context ("auto", "lat",
+        "tp", "tps", "tpr", "cta", "warp"; None = default). Results are
+        identical across variants; engines read it at creation."""
+        _check(lib.ra_ctx_set_search_kernel(self.h, None if name is None else name.encode()))
+
     def close(self):
         if getattr(self, "h", None):
             lib.ra_ctx_destroy(self.h)

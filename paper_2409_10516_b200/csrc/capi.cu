@@ -81,6 +81,19 @@ ra_status ra_ctx_set_stream(ra_ctx* ctx, void* stream) {
   });
 }
 
+ra_status ra_ctx_set_search_kernel(ra_ctx* ctx, const char* name) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (!name) {
+      ctx->search_kernel = -1;
+      return;
+    }
+    const int v = ra::search_variant_of(name);
+    if (v < 0) invalid("unknown search kernel");
+    ctx->search_kernel = v;
+  });
+}
+
 ra_status ra_ctx_synchronize(ra_ctx* ctx) {
   return guard([&] {
     check_ctx(ctx);

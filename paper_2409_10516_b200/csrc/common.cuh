@@ -127,6 +127,7 @@ struct ra_ctx {
   cudaStream_t stream = nullptr;
   int num_sms = 148;
   size_t smem_optin = 0;
+  int search_kernel = -1;  // K6 variant override (ra_ctx_set_search_kernel); -1 = env / auto
   // grow-only scratch arenas reused across calls (one call at a time per ctx)
   ra::DevBuf<uint8_t> scratch_a;
   ra::DevBuf<uint8_t> scratch_b;
@@ -244,6 +245,8 @@ bool launch_graph_search_pipe(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n,
 // whether launch_graph_search will run a.fa (the fused attention) for this
 // batch: latency-mode pipe kernel, f32 rows, supported shape
 bool search_fuses_attention(const ra_ctx* ctx, const SearchArgs& a, uint32_t max_n);
+// K6 variant by name (RA_SEARCH_KERNEL / ra_ctx_set_search_kernel); -1 = unknown
+int search_variant_of(const char* name);
 bool pipe_latency_supported(const ra_ctx* ctx, uint32_t d, uint32_t max_M, uint32_t max_n);
 
 void launch_mask_bitset(cudaStream_t s, const uint32_t* mask, uint64_t mask_n, uint32_t* bits,

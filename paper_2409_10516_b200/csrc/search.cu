@@ -1082,19 +1082,25 @@ bool try_launch_cta(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* s
 }
 
 // RA_SEARCH_KERNEL = pipe (default: latency or throughput mode by batch) |
-// tp | lat | cta | warp selects the K6 variant
-int search_variant() {
+// tp | lat | tpr (throughput, register rows only) | tps (throughput, shared
+// visited bits + TMA tile) | cta | warp selects the K6 variant
+int search_variant_of(const char* e) {
+  if (!e) return 0;
+  const std::string s(e);
+  return s == "cta" ? 1 : s == "warp" ? 2 : s == "tp" ? 3 : s == "lat" ? 4 : s == "tpr" ? 5
+         : s == "tps" ? 6 : s == "pipe" || s == "auto" ? 0 : -1;
+}
+
+int search_variant(const ra_ctx* ctx) {
   static const int v = [] {
-    const char* e = std::getenv("RA_SEARCH_KERNEL");
-    if (!e) return 0;
-    const std::string s(e);
-    return s == "cta" ? 1 : s == "warp" ? 2 : s == "tp" ? 3 : s == "lat" ? 4 : 0;
+    const int x = search_variant_of(std::getenv("RA_SEARCH_KERNEL"));
+    return x < 0 ? 0 : x;
   }();
-  return v;
+  return ctx && ctx->search_kernel >= 0 ? ctx->search_kernel : v;
 }
 
 bool search_fuses_attention(const ra_ctx* ctx, const SearchArgs& a, uint32_t max_n) {
-  const int v = search_variant();
+  const int v = search_variant(ctx);
   if (!(v == 0 || v == 4) || a.bf16 || a.B == 0) return false;
   if (v == 0 && a.B > 2u * uint32_t(ctx->num_sms)) return false;  // throughput mode
   return pipe_latency_supported(ctx, a.d, a.max_M, max_n);
@@ -1102,10 +1108,11 @@ bool search_fuses_attention(const ra_ctx* ctx, const SearchArgs& a, uint32_t max
 
 void launch_graph_search(ra_ctx* ctx, SearchArgs a, uint32_t max_n, uint8_t* scratch) {
   if (a.B == 0) return;
-  const int variant = search_variant();
+  const int variant = search_variant(ctx);
   if ((variant == 0 || variant >= 3 || a.bf16) &&
       launch_graph_search_pipe(ctx, a, max_n, scratch,
-                               variant == 3 ? 1 : variant == 4 ? 2 : 0))
+                               variant == 3 ? 1 : variant == 4 ? 2 : variant == 5 ? 3
+                               : variant == 6 ? 4 : 0))
     return;
   // the older kernels read f32 rows; the f32 copy of a bf16 group holds the
   // same rounded values, so they stay exact for shapes the pipe kernel skips

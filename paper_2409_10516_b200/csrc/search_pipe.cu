@@ -252,10 +252,17 @@ struct PipeLayout {
   }
   __host__ __device__ size_t uo_off() const { return fo_off() + arr_bytes(capO); }
   __host__ __device__ size_t bytes() const { return uo_off() + arr_bytes(capO); }
-  // TP mode: per warp q (f64) | FO | UO
+  // TP mode: per warp q (f64) | FO | UO | F lists; with vis_smem (the
+  // "TPS" variant) also a TMA row tile and the visited bitset, behind a
+  // 128-B block of per-warp mbarriers
+  __host__ __device__ size_t tp_base() const { return vis_smem ? 128 : 0; }
   __host__ __device__ size_t tp_flist_off() const { return size_t(D) * 8 + 2 * arr_bytes(capO); }
+  __host__ __device__ size_t tp_tile_off() const { return tp_flist_off() + size_t(kFR) * 32 * 12; }
+  __host__ __device__ size_t tp_vis_off() const {
+    return tp_tile_off() + (vis_smem ? tile_bytes() : 0);
+  }
   __host__ __device__ size_t tp_warp_bytes() const {
-    return tp_flist_off() + size_t(kFR) * 32 * 12;
+    return tp_vis_off() + (vis_smem ? ((size_t(vis_words) * 4 + 15) & ~size_t(15)) : 0);
   }
 };
 
@@ -385,11 +392,11 @@ __device__ void fused_attention_tail(const SearchArgs& a, const PipeLayout& lay,
 }
 
 template <int D, bool VS, bool TP, bool BF>
-__global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
+__global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP_MINB) : 1)
     k_graph_search_pipe(SearchArgs a, PipeLayout lay, uint32_t spill_cap) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t b = TP ? blockIdx.x * kTW + warp : blockIdx.x;
+  const uint32_t b = TP ? blockIdx.x * (blockDim.x >> 5) + warp : blockIdx.x;
   if (TP && b >= a.B) return;  // warp-uniform; TP never uses CTA barriers
   const GraphDesc g = a.desc[b];
   const uint32_t M = g.M, ef = g.ef, k = a.k, n = g.n;
@@ -422,16 +429,20 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
   volatile uint64_t* pk_nk = reinterpret_cast<volatile uint64_t*>(smem + PipeLayout::kNk);
   uint32_t* pk_id = reinterpret_cast<uint32_t*>(smem + PipeLayout::kPkId);
   uint64_t* pk_k = reinterpret_cast<uint64_t*>(smem + PipeLayout::kPkK);
-  double* qd = TP ? reinterpret_cast<double*>(smem + warp * lay.tp_warp_bytes())
+  uint8_t* const wbase = smem + lay.tp_base() + warp * lay.tp_warp_bytes();  // TP: this query's
+  double* qd = TP ? reinterpret_cast<double*>(wbase)
                   : reinterpret_cast<double*>(smem + PipeLayout::kQd);
-  float* tile = reinterpret_cast<float*>(smem + lay.tiles_off() + warp * lay.tile_bytes());
+  float* tile = reinterpret_cast<float*>(TP ? wbase + lay.tp_tile_off()
+                                            : smem + lay.tiles_off() + warp * lay.tile_bytes());
   const uint32_t vw = lay.vis_words;
-  uint32_t* vis = (VS && !TP) ? reinterpret_cast<uint32_t*>(smem + lay.vis_off())
-                              : a.vis_global + size_t(b) * 2 * vw;
+  uint32_t* vis = VS ? reinterpret_cast<uint32_t*>(TP ? wbase + lay.tp_vis_off()
+                                                       : smem + lay.vis_off())
+                     : a.vis_global + size_t(b) * 2 * vw;
   uint32_t* expd = vis + vw;
   uint8_t* spill_slot = a.spill + size_t(b) * 2 * PipeLayout::arr_bytes(spill_cap);
 
   if constexpr (TP) {
+    if (VS && lane == 0) mbar_init(bar);
     for (uint32_t w = lane; w < vw; w += 32) vis[w] = 0;
     for (uint32_t i = lane; i < D; i += 32) qd[i] = (double)a.q[size_t(b) * D + i];
     __syncwarp();
@@ -473,7 +484,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     msk = isnew && masked_id(v);
     const uint32_t newmask = __ballot_sync(kFull, isnew);
     sk = 0;
-    if constexpr (TP) {
+    if constexpr (TP && !VS) {
       // every new row's lines in flight at once (the dot's loads then merge
       // with these misses instead of paying one L2 round trip per few lines)
       if (isnew && !(a.flags & 8192u)) {
@@ -500,19 +511,27 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         sk = okey(acc);
       }
     } else if (newmask) {
-      float* row = tile + size_t(__popc(newmask & lanemask_lt(lane))) * RS;
-      fence_proxy_async();
-      if (lane == 0) mbar_arrive_expect_tx(bar, __popc(newmask) * kRowBytes);
-      __syncwarp();
-      if (isnew) {
-        if constexpr (BF) bulk_g2s(row, keys16 + size_t(v) * D, kRowBytes, bar);
-        else bulk_g2s(row, keys + size_t(v) * D, kRowBytes, bar);
-      }
-      mbar_wait(bar, phase);
-      phase ^= 1u;
-      if (isnew) {
-        if constexpr (BF) sk = okey(row_dot_bf<D>(qd, reinterpret_cast<const uint4*>(row), false));
-        else sk = okey(row_dot<D>(qd, row));
+      // rows through this warp's tile, lay.MT at a time (one round unless
+      // the tile is shorter than the degree: TPS)
+      const uint32_t o = __popc(newmask & lanemask_lt(lane)), nn = __popc(newmask);
+      for (uint32_t c0 = 0; c0 < nn; c0 += lay.MT) {
+        const uint32_t cnt = nn - c0 < lay.MT ? nn - c0 : lay.MT;
+        const bool mine = isnew && o >= c0 && o < c0 + cnt;
+        float* row = tile + size_t(o - c0) * RS;
+        fence_proxy_async();
+        if (lane == 0) mbar_arrive_expect_tx(bar, cnt * kRowBytes);
+        __syncwarp();
+        if (mine) {
+          if constexpr (BF) bulk_g2s(row, keys16 + size_t(v) * D, kRowBytes, bar);
+          else bulk_g2s(row, keys + size_t(v) * D, kRowBytes, bar);
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        if (mine) {
+          if constexpr (BF) sk = okey(row_dot_bf<D>(qd, reinterpret_cast<const uint4*>(row), false));
+          else sk = okey(row_dot<D>(qd, row));
+        }
+        __syncwarp();
       }
     }
   };
@@ -522,8 +541,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     // F: per-lane unsorted lists in shared memory (column layout, entry i of
     // lane l at [i * 32 + l]; empty = (0, kSentinel)); the lane head (its
     // best entry and slot) in registers. Helpers read these lists directly.
-    volatile uint64_t* Fl_k = TP ? reinterpret_cast<volatile uint64_t*>(
-                                       smem + warp * lay.tp_warp_bytes() + lay.tp_flist_off())
+    volatile uint64_t* Fl_k = TP ? reinterpret_cast<volatile uint64_t*>(wbase + lay.tp_flist_off())
                                  : pubf_k;
     volatile uint32_t* Fl_i = reinterpret_cast<volatile uint32_t*>(Fl_k + kFR * 32);
     if constexpr (TP) {
@@ -536,7 +554,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     for (int i = 0; i < kUR; ++i) uk[i] = 0, uid[i] = kSentinel;
     uint32_t fcnt = 0, ufree = (1u << kUR) - 1u;
     uint32_t capFO = lay.capO, capUO = lay.capO, nFO = 0, nUO = 0;
-    uint8_t* fo_base = TP ? smem + warp * lay.tp_warp_bytes() + size_t(D) * 8 : smem + lay.fo_off();
+    uint8_t* fo_base = TP ? wbase + size_t(D) * 8 : smem + lay.fo_off();
     Arr FO = Arr::at(fo_base, lay.capO),
         UO = Arr::at(fo_base + PipeLayout::arr_bytes(lay.capO), lay.capO);
     bool fo_g = false, uo_g = false;
@@ -890,6 +908,10 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
         ++c_miss;
         expand(tid, cv, cx, cand, cm);
         pre = true;
+        if constexpr (VS) {  // the new frontier nodes' adjacency rows go to L2 now
+          if ((M * 4) % 16 == 0 && !(a.flags & 2u) && cand && cx >= thr)
+            bulk_prefetch_l2(adj + size_t(cv) * M, M * 4);
+        }
         continue;
       }
       // hit (taken above, or in flight: wait, then take) or expand inline
@@ -955,8 +977,14 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
     uint32_t p2 = 32;
     while (p2 < nU) p2 <<= 1;
     bool fin_smem;
+    uint8_t* fin_base = TP ? fo_base : smem + lay.tiles_off();
     if constexpr (TP) {
-      fin_smem = p2 <= lay.capO;  // this warp's (dead) FO region
+      if (VS) {  // this warp's (dead) row tile
+        fin_smem = PipeLayout::arr_bytes(p2) <= lay.tile_bytes();
+        fin_base = wbase + lay.tp_tile_off();
+      } else {
+        fin_smem = p2 <= lay.capO;  // this warp's (dead) FO region
+      }
     } else {
       ctrl[0] = 1;  // helpers stop
       __syncwarp();
@@ -972,7 +1000,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
       __syncthreads();  // helpers are done with their tiles (and TMA)
     }
     // A: shared memory when it fits, else FO's (dead) half of the HBM slot
-    Arr A = fin_smem ? Arr::at(TP ? fo_base : smem + lay.tiles_off(), p2) : Arr::at(spill_slot, p2);
+    Arr A = fin_smem ? Arr::at(fin_base, p2) : Arr::at(spill_slot, p2);
     uint32_t w = 0;
 #pragma unroll
     for (int i = 0; i < kUR; ++i) {
@@ -1370,7 +1398,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? RA_TP_MINB : 1)
 
 template <int D, bool BF>
 bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* scratch,
-                   bool tp) {
+                   bool tp, int tps) {
   const size_t budget = ctx->smem_optin ? ctx->smem_optin : 227 * 1024;
   uint32_t spill_cap = 32;
   while (spill_cap < max_n) spill_cap <<= 1;
@@ -1399,6 +1427,40 @@ bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* sc
   s.vis_global = reinterpret_cast<uint32_t*>(cur);
   if (tp) {
     s.fa.out = nullptr;
+    // TPS: visited bitset and a TMA row tile per query warp in shared
+    // memory (no HBM bitsets to zero, coalesced 512-B row copies), as many
+    // query warps per CTA as the batch needs to fill the SMs in ONE wave.
+    // Taken while the batch fits one wave (B <= num_sms x warps that fit);
+    // bigger batches keep the 16-warps-per-SM register-row kernel.
+    // tps: 0 auto, 1 forced (if it fits), -1 off
+#ifndef RA_TPS_ROWS
+#define RA_TPS_ROWS 12
+#endif
+#ifndef RA_TPS_CAPO
+#define RA_TPS_CAPO 128
+#endif
+    if (tps >= 0) {
+      PipeLayout ls{uint32_t(D), std::min<uint32_t>(std::max<uint32_t>(a.max_M, 1), RA_TPS_ROWS),
+                    (max_n + 31) / 32, 1, RA_TPS_CAPO};
+      const size_t wb = ls.tp_warp_bytes();
+      const uint32_t fit = uint32_t(std::min<size_t>((budget - ls.tp_base()) / wb, kTW));
+      const uint32_t sms = uint32_t(ctx->num_sms);
+      const uint32_t want = (a.B + sms - 1) / sms;
+      if (fit >= 1 && (tps == 1 || want <= fit)) {
+        const uint32_t wpc = std::max<uint32_t>(1, std::min(fit, want));
+        const size_t bytes = ls.tp_base() + wpc * wb;
+        auto kern = k_graph_search_pipe<D, true, true, BF>;
+        static int set_bytes[64] = {};
+        if (int(bytes) > set_bytes[ctx->device & 63]) {
+          RA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(bytes)));
+          set_bytes[ctx->device & 63] = int(bytes);
+        }
+        kern<<<(a.B + wpc - 1) / wpc, wpc * 32, bytes, ctx->stream>>>(s, ls, spill_cap);
+        RA_LAUNCH_CHECK();
+        return true;
+      }
+    }
 #ifndef RA_TP_CAPO
 #define RA_TP_CAPO 256
 #endif
@@ -1456,21 +1518,25 @@ size_t search_pipe_scratch_bytes(uint32_t B, uint32_t max_n) {
 bool launch_graph_search_pipe(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n,
                               uint8_t* scratch, int mode) {
   if (a.max_M > 32 || a.max_M == 0) return false;
-  const bool tp = mode == 1 || (mode == 0 && a.B > 2u * uint32_t(ctx->num_sms));
+  // mode 0 auto, 1 throughput (TPS when it fits one wave), 2 latency,
+  // 3 throughput with register rows only, 4 TPS forced
+  const bool tp = mode == 1 || mode == 3 || mode == 4 ||
+                  (mode == 0 && a.B > 2u * uint32_t(ctx->num_sms));
+  const int tps = mode == 3 ? -1 : mode == 4 ? 1 : 0;
   if (a.bf16) {  // bf16 rows: d in {32, 64, 128} (16-B multiples)
     switch (a.d) {
-      case 128: return launch_pipe_d<128, true>(ctx, a, max_n, scratch, tp);
-      case 64: return launch_pipe_d<64, true>(ctx, a, max_n, scratch, tp);
-      case 32: return launch_pipe_d<32, true>(ctx, a, max_n, scratch, tp);
+      case 128: return launch_pipe_d<128, true>(ctx, a, max_n, scratch, tp, tps);
+      case 64: return launch_pipe_d<64, true>(ctx, a, max_n, scratch, tp, tps);
+      case 32: return launch_pipe_d<32, true>(ctx, a, max_n, scratch, tp, tps);
       default: return false;
     }
   }
   switch (a.d) {
-    case 128: return launch_pipe_d<128, false>(ctx, a, max_n, scratch, tp);
-    case 64: return launch_pipe_d<64, false>(ctx, a, max_n, scratch, tp);
-    case 32: return launch_pipe_d<32, false>(ctx, a, max_n, scratch, tp);
-    case 16: return launch_pipe_d<16, false>(ctx, a, max_n, scratch, tp);
-    case 8: return launch_pipe_d<8, false>(ctx, a, max_n, scratch, tp);
+    case 128: return launch_pipe_d<128, false>(ctx, a, max_n, scratch, tp, tps);
+    case 64: return launch_pipe_d<64, false>(ctx, a, max_n, scratch, tp, tps);
+    case 32: return launch_pipe_d<32, false>(ctx, a, max_n, scratch, tp, tps);
+    case 16: return launch_pipe_d<16, false>(ctx, a, max_n, scratch, tp, tps);
+    case 8: return launch_pipe_d<8, false>(ctx, a, max_n, scratch, tp, tps);
     default: return false;
   }
 }

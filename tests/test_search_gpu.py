@@ -217,3 +217,30 @@ def test_search_throughput_mode_matches_oracle(port):
         res = ra.search_batch([g], Q, k, m, ef).host()
         for qi in range(0, B, 7):
             assert_same(res[qi], og.search(Q[qi], k, m, ef), f"tp ef={ef} q={qi}")
+
+
+@pytest.mark.parametrize("kernel", ["lat", "tp", "tps", "tpr"])
+def test_search_kernel_variants_identical(port, kernel):
+    """Every K6 variant (latency CTA pipeline, throughput with shared-memory
+    visited bits + TMA tiles, throughput with register rows) returns the
+    oracle's ids / scores / scanned / truncated on a d=128 multi-head batch."""
+    ra = _ra()
+    n, H, G = 16384, 4, 2
+    w = port.generate_workload(n, 256, 128, H, G, seed=9, n_decode=16)
+    kvs = [ra.KVGroup(w["keys"][g], w["values"][g]) for g in range(G)]
+    bp = ra.OODGraphBuildParams(32, 24, 128, 8)
+    graphs = [ra.ood_build(kvs[h // 2], w["prefill_q"][h], bp) for h in range(H)]
+    ograph = [port.graph(w["keys"][h // 2], graphs[h].serialize()) for h in range(H)]
+    W = ra.static_partition(n, 128, 512).static_set
+    ctx = ra.default_context()
+    ctx.set_search_kernel(kernel)
+    try:
+        steps = 16
+        Q = np.concatenate([np.stack([w["decode_q"][h][s] for h in range(H)])
+                            for s in range(steps)])
+        res = ra.search_batch(graphs * steps, Q, 100, W, 128).host()
+        for i in range(len(res)):
+            h = i % H
+            assert_same(res[i], ograph[h].search(Q[i], 100, W, 128), f"{kernel} q={i}")
+    finally:
+        ctx.set_search_kernel(None)
