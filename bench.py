@@ -547,6 +547,7 @@ def multi_context_line(a, ra, name, ctxs, per_layer, n_ctx, flush, stream, dev, 
             s_, e_ = eng.last_stats()
             sc.append(s_)
             ex.append(e_)
+        for i in range(a.warmup, a.warmup + a.steps):
             t_s.append(timed(lambda: serial(i), stream, flush))
     i0 = a.warmup
     out, om, scn = (x.cpu().numpy() for x in eng.decode_step_device(Q[i0]))
@@ -574,6 +575,7 @@ def multi_context_line(a, ra, name, ctxs, per_layer, n_ctx, flush, stream, dev, 
         "workload": desc, "contexts": len(ctxs), "heads": nH, "n_ctx": n_ctx,
         "value": round(ms_b, 4), "unit": "ms/step (layer-batched: one engine step over all "
                                            "heads)",
+        "step_ms_all": [round(x, 4) for x in t_b], "kernel_ms_all": [round(x, 4) for x in s_b],
         "layer_serial_ms": round(ms_ser, 4),
         "layer_serial_note": f"{n_l} engine steps of {hl} heads back to back (the layer "
                              "dependency chain of real decode)",

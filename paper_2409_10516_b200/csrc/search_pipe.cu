@@ -97,6 +97,16 @@ __device__ __forceinline__ uint64_t okey(double x) {
 __device__ __forceinline__ double okey_inv(uint64_t k) {
   return __longlong_as_double((k >> 63) ? (k & ~(1ull << 63)) : ~k);
 }
+// a split point strictly inside (lo, hi) for the key bisections: the midpoint
+// of the two SCORES (scores cluster: a key-space midpoint of keys whose
+// scores differ in sign or exponent barely moves in 8 steps), else the
+// key-space midpoint. Any split keeps the bisection exact.
+__device__ __forceinline__ uint64_t key_mid(uint64_t lo, uint64_t hi) {
+  const uint64_t km = lo + ((hi - lo) >> 1);
+  if (hi - lo < 4) return km;
+  const uint64_t vm = okey(0.5 * okey_inv(lo) + 0.5 * okey_inv(hi));
+  return (vm > lo && vm < hi) ? vm : km;
+}
 // (key desc, id asc); the empty entry (0, kSentinel) is worse than any node
 __device__ __forceinline__ bool better(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
   return ka > kb || (ka == kb && ia < ib);
@@ -553,7 +563,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
 #pragma unroll
     for (int i = 0; i < kUR; ++i) uk[i] = 0, uid[i] = kSentinel;
     uint32_t fcnt = 0, ufree = (1u << kUR) - 1u;
-    uint32_t capFO = lay.capO, capUO = lay.capO, nFO = 0, nUO = 0;
+    uint32_t capFO = lay.capO, capUO = lay.capO, nFO = 0, nUO = 0, pk_fo = 0, pk_uo = 0;
     uint8_t* fo_base = TP ? wbase + size_t(D) * 8 : smem + lay.fo_off();
     Arr FO = Arr::at(fo_base, lay.capO),
         UO = Arr::at(fo_base + PipeLayout::arr_bytes(lay.capO), lay.capO);
@@ -633,6 +643,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
           fo_ix = nFO + __popc(sm & lanemask_lt(__ffs(__ballot_sync(kFull, sp && si == bi)) - 1));
         }
         nFO += __popc(sm);
+        if (nFO > pk_fo) pk_fo = nFO;
         __syncwarp();
       }
     };
@@ -658,6 +669,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
         const uint32_t o = nUO + __popc(sm & lanemask_lt(lane));
         if (sp) UO.k[o] = x, UO.id[o] = v;
         nUO += __popc(sm);
+        if (nUO > pk_uo) pk_uo = nUO;
         __syncwarp();
       }
     };
@@ -695,7 +707,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
       } else {
 #pragma unroll 1
         for (int it = 0; it < bis_it && hi - lo > 1; ++it) {
-          const uint64_t mid = lo + ((hi - lo) >> 1);
+          const uint64_t mid = key_mid(lo, hi);
           if (count_gt(mid - 1) >= ef) lo = mid;
           else hi = mid;
         }
@@ -764,7 +776,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
         } else {
 #pragma unroll 1
           for (int it = 0; it < bis_it && phi - plo > 1; ++it) {
-            const uint64_t mid = plo + ((phi - plo) >> 1);
+            const uint64_t mid = key_mid(plo, phi);
             if (count_gt(mid - 1) >= target) plo = mid;
             else phi = mid;
           }
@@ -908,6 +920,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
         ++c_miss;
         expand(tid, cv, cx, cand, cm);
         pre = true;
+        PIPE_TICK(2)
         if constexpr (VS) {  // the new frontier nodes' adjacency rows go to L2 now
           if ((M * 4) % 16 == 0 && !(a.flags & 2u) && cand && cx >= thr)
             bulk_prefetch_l2(adj + size_t(cv) * M, M * 4);
@@ -1020,6 +1033,12 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
       d[0] = c_miss, d[1] = c_wait, d[2] = clock64() - t_begin, d[3] = expanded;
       d[4] = c_hit, d[5] = TP ? 0 : ctrl[8], d[6] = c_comp;
       d[7] = cy[0], d[8] = cy[1], d[9] = cy[2], d[10] = cy[3], d[11] = cyc_comp;
+#ifndef RA_PIPE_PROFILE
+      if (TP) {  // overflow anatomy: FO / UO spill rounds, FO pops, moved to HBM
+        d[7] = c_fsp, d[8] = c_fopop, d[9] = (fo_g ? 1u : 0u) | (uo_g ? 2u : 0u), d[10] = c_usp;
+        d[5] = pk_fo, d[11] = pk_uo;  // peak overflow sizes
+      }
+#endif
 #ifdef RA_PIPE_MISSCLASS
       d[9] = cy[4];
 #endif
@@ -1434,20 +1453,29 @@ bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* sc
     // bigger batches keep the 16-warps-per-SM register-row kernel.
     // tps: 0 auto, 1 forced (if it fits), -1 off
 #ifndef RA_TPS_ROWS
-#define RA_TPS_ROWS 12
+#define RA_TPS_ROWS 16
 #endif
 #ifndef RA_TPS_CAPO
 #define RA_TPS_CAPO 128
 #endif
     if (tps >= 0) {
+      // the overflow arrays FO / UO get what the warps leave of the budget
+      // (a search that outgrows them moves them to its HBM slot: exact, slow)
       PipeLayout ls{uint32_t(D), std::min<uint32_t>(std::max<uint32_t>(a.max_M, 1), RA_TPS_ROWS),
                     (max_n + 31) / 32, 1, RA_TPS_CAPO};
-      const size_t wb = ls.tp_warp_bytes();
-      const uint32_t fit = uint32_t(std::min<size_t>((budget - ls.tp_base()) / wb, kTW));
+      const uint32_t fit = uint32_t(std::min<size_t>((budget - ls.tp_base()) / ls.tp_warp_bytes(),
+                                                     kTW));
       const uint32_t sms = uint32_t(ctx->num_sms);
       const uint32_t want = (a.B + sms - 1) / sms;
       if (fit >= 1 && (tps == 1 || want <= fit)) {
         const uint32_t wpc = std::max<uint32_t>(1, std::min(fit, want));
+        {
+          PipeLayout l0 = ls;
+          l0.capO = 0;
+          const size_t per = (budget - ls.tp_base()) / wpc - l0.tp_warp_bytes();
+          ls.capO = uint32_t(std::min<size_t>(per / 24 - 2, 4096)) & ~31u;
+        }
+        const size_t wb = ls.tp_warp_bytes();
         const size_t bytes = ls.tp_base() + wpc * wb;
         auto kern = k_graph_search_pipe<D, true, true, BF>;
         static int set_bytes[64] = {};
