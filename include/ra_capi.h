@@ -16,7 +16,8 @@
  *   ra_flat_search_batch    <- FlatIndex::search                   include/attnindex/index_flat.hpp:14-15
  *   ra_ivf_build / _search_batch <- IVFIndex / IVFIndex::search     include/attnindex/index_ivf.hpp:17-37
  *   ra_partial_attention    <- partial_attention                   include/attnindex/attention.hpp:47-50
- *   ra_merge                <- merge_gammas + merge                include/attnindex/attention.hpp:52-60
+ *   ra_merge / _host        <- merge_gammas + merge                include/attnindex/attention.hpp:52-60
+ *   ra_partial_attention_host <- partial_attention (host buffers)  include/attnindex/attention.hpp:47-50
  *   ra_static_partition     <- static_partition                    include/attnindex/attention.hpp:44-45
  *   ra_engine_* / decode    <- engine_init / decode_step           include/attnindex/engine.hpp:103-111
  *
@@ -82,6 +83,10 @@ void ra_ctx_destroy(ra_ctx* ctx);
  * enqueued on it; calls taking host buffers synchronize it before returning. */
 ra_status ra_ctx_set_stream(ra_ctx* ctx, void* stream);
 ra_status ra_ctx_synchronize(ra_ctx* ctx);
+/* Page-locked, device-mapped host memory (for zero-copy ra_engine_step_host
+ * staging); free with ra_host_free. */
+ra_status ra_host_alloc(size_t bytes, void** out);
+void ra_host_free(void* p);
 /* Graph-search kernel variant for this ctx (overrides RA_SEARCH_KERNEL):
  * "auto" (latency mode up to 2 x SMs queries, then throughput mode),
  * "lat", "tp", "tps" (throughput, shared-memory visited bits + TMA row
@@ -105,6 +110,12 @@ ra_status ra_kv_create(ra_ctx* ctx, const float* keys, const float* values, uint
 ra_status ra_kv_create_bf16(ra_ctx* ctx, const float* keys, const float* values, uint64_t n,
                             uint32_t d, int on_device, int attention_only, ra_kv** out);
 int ra_kv_is_bf16(const ra_kv* kv);
+/* Uploads the values of a keys-only f32 group (n must equal its size): the
+ * group's graphs and engines then attend over them. Errors: already has
+ * values, n mismatch ("keys and values must have equal n"). */
+ra_status ra_kv_attach_values(ra_ctx* ctx, ra_kv* kv, const float* values, uint64_t n,
+                              int on_device);
+int ra_kv_has_values(const ra_kv* kv);
 void ra_kv_retain(ra_kv* kv);
 void ra_kv_release(ra_kv* kv);
 uint64_t ra_kv_size(const ra_kv* kv);
@@ -205,6 +216,22 @@ ra_status ra_static_partition(uint64_t t, uint64_t s_init, uint64_t s_local,
 ra_status ra_partial_attention(ra_ctx* ctx, ra_kv* kv, uint32_t B, const float* q,
                                const uint32_t* idx, uint32_t m_stride, const uint32_t* m,
                                double* out, double* zmax, double* expsum);
+/* partial_attention on HOST buffers, one query (attention.cpp:102-128):
+ * keys/values n x d f32; the rows named by idx[0..m) are staged in idx order
+ * and reduced on the device (in-order f64 dots, max-subtracted exps, the
+ * reference's accumulation order). Errors: "query dimension mismatch",
+ * "keys and values must have equal n", "empty index set",
+ * "index out of range". out [d] f64. */
+ra_status ra_partial_attention_host(ra_ctx* ctx, const float* q, uint32_t q_dim,
+                                    const float* keys, uint64_t n_keys, const float* values,
+                                    uint64_t n_values, uint32_t d, const uint32_t* idx,
+                                    uint64_t m, double* out, double* zmax, double* expsum);
+/* merge_gammas + merge of ONE partial pair on HOST buffers
+ * (attention.cpp:136-157): out [d]; gw / go may be NULL. An empty side
+ * returns the other side exactly; both empty: "empty attention support". */
+ra_status ra_merge_host(ra_ctx* ctx, uint32_t d, const double* ow, double zw, double sw,
+                        int w_empty, const double* oo, double zo, double so, int o_empty,
+                        double* out, double* gw, double* go);
 /* merge of B partial pairs (device arrays; *_empty [B] u8 flags). Error
  * "empty attention support" if both sides of any row are empty. */
 ra_status ra_merge(ra_ctx* ctx, uint32_t B, uint32_t d, const double* ow, const double* zw,

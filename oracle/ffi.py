@@ -4,7 +4,11 @@ Two backends with one numpy-facing API:
   * ``Oracle("port")`` -> oracle/_build/liboracle.so, our C restatement
     (oracle/ra_oracle.c), buildable anywhere with gcc;
   * ``Oracle("ref")``  -> oracle/_ref/libattnindex_ref.so, the unmodified
-    reference sources (/root/reference/proj/src) built by oracle/Makefile.
+    reference sources (/root/reference/proj/src) built by oracle/Makefile;
+  * ``Oracle("dropin")`` -> oracle/_ref/libattnindex_dropin.so, the same
+    reference library with src/index_oodgraph.cpp, attention.cpp and
+    engine.cpp replaced by the drop-in TUs (paper_2409_10516_b200/host/) over
+    libra_b200.so: the reference's own API, running on the GPU backend.
 
 Only tests/, ``__graft_entry__.smoke()`` and bench.py's CPU-baseline legs import
 this module. Errors raise ``OracleError`` carrying the reference's message.
@@ -21,6 +25,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 PORT_LIB = os.path.join(HERE, "_build", "liboracle.so")
 REF_LIB = os.path.join(HERE, "_ref", "libattnindex_ref.so")
+DROPIN_LIB = os.path.join(HERE, "_ref", "libattnindex_dropin.so")
 REF_SRC = "/root/reference/proj"
 
 u8p = C.POINTER(C.c_uint8)
@@ -42,7 +47,7 @@ def build(ref: bool = True) -> None:
 
 
 def available(kind: str) -> bool:
-    return os.path.exists(PORT_LIB if kind == "port" else REF_LIB)
+    return os.path.exists({"port": PORT_LIB, "ref": REF_LIB, "dropin": DROPIN_LIB}[kind])
 
 
 def _ptr(a: np.ndarray, t):
@@ -73,10 +78,12 @@ class BuildParams:
 
 class Oracle:
     def __init__(self, kind: str = "port"):
-        if kind not in ("port", "ref"):
+        if kind not in ("port", "ref", "dropin"):
             raise ValueError(kind)
+        self.backend = kind
+        kind = "ref" if kind == "dropin" else kind  # same C entry points
         self.kind = kind
-        path = PORT_LIB if kind == "port" else REF_LIB
+        path = {"port": PORT_LIB, "ref": REF_LIB, "dropin": DROPIN_LIB}[self.backend]
         if not os.path.exists(path):
             build(ref=(kind == "ref"))
         self.lib = C.CDLL(path)

@@ -81,6 +81,18 @@ ra_status ra_ctx_set_stream(ra_ctx* ctx, void* stream) {
   });
 }
 
+ra_status ra_host_alloc(size_t bytes, void** out) {
+  return guard([&] {
+    if (!out) invalid("null output");
+    *out = nullptr;
+    RA_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocMapped | cudaHostAllocPortable));
+  });
+}
+
+void ra_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 ra_status ra_ctx_set_search_kernel(ra_ctx* ctx, const char* name) {
   return guard([&] {
     check_ctx(ctx);
@@ -137,6 +149,26 @@ __global__ void k_to_bf16(float* x, uint16_t* y, uint64_t n, int round_f32) {
   }
 }
 }  // namespace
+
+ra_status ra_kv_attach_values(ra_ctx* ctx, ra_kv* kv, const float* values, uint64_t n,
+                              int on_device) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (!kv || !values) invalid("null kv or values");
+    if (n != kv->n) invalid("keys and values must have equal n");
+    if (kv->values.p) invalid("kv group already has values");
+    if (kv->bf16 || kv->bf16_attn) invalid("attach values to f32 groups only");
+    DeviceGuard dg(ctx->device);
+    kv->values.alloc(size_t(n) * kv->d);
+    if (n)
+      RA_CUDA(cudaMemcpyAsync(kv->values.p, values, size_t(n) * kv->d * 4,
+                              on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                              ctx->stream));
+    RA_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int ra_kv_has_values(const ra_kv* kv) { return kv && kv->values.p ? 1 : 0; }
 
 ra_status ra_kv_create_bf16(ra_ctx* ctx, const float* keys, const float* values, uint64_t n,
                             uint32_t d, int on_device, int attention_only, ra_kv** out) {
@@ -471,6 +503,100 @@ ra_status ra_partial_attention(ra_ctx* ctx, ra_kv* kv, uint32_t B, const float* 
     launch_partial_attention_ex(ctx->stream, refs, kv->d, B, q, idx, m_stride, m, nullptr, 0,
                                 out, zmax, expsum, z, m_stride, nullptr, flag);
     if (read_flag(ctx, flag) & 1u) invalid("index out of range");
+  });
+}
+
+// partial_attention on HOST buffers (attention.cpp:102-128): the rows named
+// by idx are staged (gathered in idx order) and the device kernel computes
+// the partial over them - the same arithmetic order as the reference.
+ra_status ra_partial_attention_host(ra_ctx* ctx, const float* q, uint32_t q_dim,
+                                    const float* keys, uint64_t n_keys, const float* values,
+                                    uint64_t n_values, uint32_t d, const uint32_t* idx,
+                                    uint64_t m, double* out, double* zmax, double* expsum) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (q_dim != d) invalid("query dimension mismatch");
+    if (n_keys != n_values || !values) invalid("keys and values must have equal n");
+    if (m == 0) invalid("empty index set");
+    if (m > 0xFFFFFFFFull) invalid("too many indices");
+    for (uint64_t i = 0; i < m; ++i)
+      if (idx[i] >= n_keys) invalid("index out of range");
+    DeviceGuard dg(ctx->device);
+    // device layout: q f32[d] | K f32[m][d] | V f32[m][d] | ids u32[m] | cnt u32 | pad
+    //                | out f64[d] | zmax | expsum | flag
+    const size_t rowb = size_t(d) * 4;
+    const size_t o_q = 0, o_k = (o_q + rowb + 15) & ~size_t(15);
+    const size_t o_v = (o_k + m * rowb + 15) & ~size_t(15);
+    const size_t o_i = (o_v + m * rowb + 15) & ~size_t(15);
+    const size_t o_c = (o_i + m * 4 + 15) & ~size_t(15);
+    const size_t o_o = (o_c + 16 + 15) & ~size_t(15);
+    const size_t o_end = o_o + (size_t(d) + 2) * 8 + 16;
+    std::vector<uint8_t> h(o_c + 16);
+    std::memcpy(h.data() + o_q, q, rowb);
+    for (uint64_t i = 0; i < m; ++i) {
+      std::memcpy(h.data() + o_k + i * rowb, keys + size_t(idx[i]) * d, rowb);
+      std::memcpy(h.data() + o_v + i * rowb, values + size_t(idx[i]) * d, rowb);
+      const uint32_t j = uint32_t(i);
+      std::memcpy(h.data() + o_i + i * 4, &j, 4);
+    }
+    const uint32_t cnt = uint32_t(m);
+    std::memcpy(h.data() + o_c, &cnt, 4);
+    uint8_t* dv = arena<uint8_t>(ctx->scratch_c, o_end + 256);
+    RA_CUDA(cudaMemcpyAsync(dv, h.data(), h.size(), cudaMemcpyHostToDevice, ctx->stream));
+    uint8_t* a = arena<uint8_t>(ctx->scratch_a, 256);
+    KVRef* ref = reinterpret_cast<KVRef*>(a);
+    uint32_t* flag = reinterpret_cast<uint32_t*>(a + 128);
+    const KVRef hr{reinterpret_cast<const float*>(dv + o_k), reinterpret_cast<const float*>(dv + o_v),
+                   m, nullptr, nullptr};
+    RA_CUDA(cudaMemcpyAsync(ref, &hr, sizeof(KVRef), cudaMemcpyHostToDevice, ctx->stream));
+    RA_CUDA(cudaMemsetAsync(flag, 0, 4, ctx->stream));
+    double* dout = reinterpret_cast<double*>(dv + o_o);
+    double* z = nullptr;
+    if (m > 8192) z = arena<double>(ctx->scratch_b, partial_scratch_doubles(1, uint32_t(m)));
+    launch_partial_attention_ex(ctx->stream, ref, d, 1, reinterpret_cast<const float*>(dv + o_q),
+                                reinterpret_cast<const uint32_t*>(dv + o_i), uint32_t(m),
+                                reinterpret_cast<const uint32_t*>(dv + o_c), nullptr, 0, dout,
+                                dout + d, dout + d + 1, z, uint32_t(m), nullptr, flag);
+    std::vector<double> r(size_t(d) + 2);
+    RA_CUDA(cudaMemcpyAsync(r.data(), dout, r.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (read_flag(ctx, flag) & 1u) invalid("index out of range");
+    std::memcpy(out, r.data(), size_t(d) * 8);
+    *zmax = r[d];
+    *expsum = r[size_t(d) + 1];
+  });
+}
+
+// merge_gammas + merge of one partial pair on HOST buffers
+// (attention.cpp:136-157); gw / go may be NULL.
+ra_status ra_merge_host(ra_ctx* ctx, uint32_t d, const double* ow, double zw, double sw,
+                        int w_empty, const double* oo, double zo, double so, int o_empty,
+                        double* out, double* gw, double* go) {
+  return guard([&] {
+    check_ctx(ctx);
+    DeviceGuard dg(ctx->device);
+    // device: ow[d] | oo[d] | zw sw zo so | out[d] | gw go | flags u8[2] | err u32
+    const size_t nd = size_t(d);
+    std::vector<double> h(3 * nd + 6 + 2, 0.0);
+    if (!w_empty) std::memcpy(h.data(), ow, nd * 8);
+    if (!o_empty) std::memcpy(h.data() + nd, oo, nd * 8);
+    h[2 * nd] = zw, h[2 * nd + 1] = sw, h[2 * nd + 2] = zo, h[2 * nd + 3] = so;
+    uint8_t* fl = reinterpret_cast<uint8_t*>(h.data() + 3 * nd + 6);
+    fl[0] = uint8_t(w_empty != 0), fl[1] = uint8_t(o_empty != 0);
+    double* dv = arena<double>(ctx->scratch_c, h.size() + 2);
+    uint32_t* flag = reinterpret_cast<uint32_t*>(dv + h.size());
+    RA_CUDA(cudaMemcpyAsync(dv, h.data(), h.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    RA_CUDA(cudaMemsetAsync(flag, 0, 4, ctx->stream));
+    const uint8_t* dfl = reinterpret_cast<const uint8_t*>(dv + 3 * nd + 6);
+    launch_merge(ctx->stream, 1, d, dv, dv + 2 * nd, dv + 2 * nd + 1, dfl, dv + nd,
+                 dv + 2 * nd + 2, dv + 2 * nd + 3, dfl + 1, dv + 2 * nd + 4, dv + 3 * nd + 4,
+                 dv + 3 * nd + 5, flag);
+    std::vector<double> r(nd + 2);
+    RA_CUDA(cudaMemcpyAsync(r.data(), dv + 2 * nd + 4, (nd + 2) * 8, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    if (read_flag(ctx, flag) & 2u) invalid("empty attention support");  // :138-139
+    if (out) std::memcpy(out, r.data(), nd * 8);
+    if (gw) *gw = r[nd];
+    if (go) *go = r[nd + 1];
   });
 }
 

@@ -481,14 +481,21 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
     return (reinterpret_cast<const volatile uint32_t*>(bits)[v >> 5] >> (v & 31)) & 1u;
   };
   uint32_t phase = 0;
+  uint64_t cy_adj = 0, cy_tma = 0;  // RA_PIPE_PROFILE: adjacency-load and TMA-wait cycles
   // Expansion of node c by this warp: lane l holds adjacency slot l; `isnew`
   // lanes hold an unvisited (at read time), first-occurrence neighbour v and
   // its exact score key. Key rows come through this warp's TMA tile.
   // The mask bit is fetched here too, so its load overlaps the row loads.
   auto expand = [&](uint32_t c, uint32_t& v, uint64_t& sk, bool& isnew, bool& msk) {
+#ifdef RA_PIPE_PROFILE
+    const uint64_t te0 = clock64();
+#endif
     v = lane < M ? __ldg(adj + size_t(c) * M + lane) : kSentinel;
     const bool valid = v != kSentinel;
     const uint32_t grp = __match_any_sync(kFull, v);
+#ifdef RA_PIPE_PROFILE
+    cy_adj += clock64() - te0;
+#endif
     const bool first = uint32_t(__ffs(grp) - 1) == lane;
     isnew = valid && first && !vbit(vis, v);
     msk = isnew && masked_id(v);
@@ -535,7 +542,13 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
           if constexpr (BF) bulk_g2s(row, keys16 + size_t(v) * D, kRowBytes, bar);
           else bulk_g2s(row, keys + size_t(v) * D, kRowBytes, bar);
         }
+#ifdef RA_PIPE_PROFILE
+        const uint64_t tw0 = clock64();
+#endif
         mbar_wait(bar, phase);
+#ifdef RA_PIPE_PROFILE
+        cy_tma += clock64() - tw0;
+#endif
         phase ^= 1u;
         if (mine) {
           if constexpr (BF) sk = okey(row_dot_bf<D>(qd, reinterpret_cast<const uint4*>(row), false));
@@ -1038,6 +1051,8 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
         d[7] = c_fsp, d[8] = c_fopop, d[9] = (fo_g ? 1u : 0u) | (uo_g ? 2u : 0u), d[10] = c_usp;
         d[5] = pk_fo, d[11] = pk_uo;  // peak overflow sizes
       }
+#else
+      if (TP) d[5] = cy_adj, d[11] = cy_tma;
 #endif
 #ifdef RA_PIPE_MISSCLASS
       d[9] = cy[4];

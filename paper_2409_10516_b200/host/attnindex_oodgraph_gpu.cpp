@@ -11,10 +11,12 @@
 // (ra_status INVALID_ARGUMENT -> std::invalid_argument, RUNTIME ->
 // std::runtime_error).
 //
-// Device state (keys upload + graph) is attached per OODGraph object through
-// a registry keyed by the object address (the header has no spare member)
-// and validated against the object's CSR identity before use. search() is
-// re-entrant: each calling thread gets its own ra_ctx (stream + scratch).
+// Device state: the key set is uploaded ONCE per VectorSet (gpu_registry:
+// the GQA heads of a group share it, as their shared_ptr does); each
+// OODGraph object's device graph lives in a registry keyed by the object
+// address, validated against the object's CSR identity before use, and freed
+// once the object's key set has expired. search() is re-entrant: each
+// calling thread gets its own ra_ctx (stream + scratch).
 #include <cstring>
 #include <fstream>
 #include <iterator>
@@ -25,54 +27,56 @@
 #include <vector>
 
 #include "attnindex/index_oodgraph.hpp"
+#include "gpu_registry.hpp"
 #include "ra_capi.h"
 
 namespace attnindex {
 namespace {
 
-[[noreturn]] void rethrow(ra_status st) {
-  const std::string msg = ra_last_error();
-  if (st == RA_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
-  throw std::runtime_error(msg);
-}
-void check(ra_status st) {
-  if (st != RA_OK) rethrow(st);
-}
-
-ra_ctx* thread_ctx() {
-  thread_local struct Holder {
-    ra_ctx* c = nullptr;
-    ~Holder() {
-      if (c) ra_ctx_destroy(c);
-    }
-  } h;
-  if (!h.c) check(ra_ctx_create(0, &h.c));
-  return h.c;
-}
+using gpu::check;
+using gpu::thread_ctx;
 
 struct DevGraph {
-  const VectorSet* keys = nullptr;  // identity of the object's CSR + keys
+  std::weak_ptr<const VectorSet> keys;  // the object's key set (expiry => object gone)
+  const VectorSet* keys_id = nullptr;   // identity of the object's CSR + keys
   const uint32_t* adj_data = nullptr;
   size_t adj_size = 0;
   uint64_t entry = 0;
-  ra_graph* g = nullptr;            // holds a reference on its ra_kv
+  ra_graph* g = nullptr;  // holds a reference on its ra_kv
 };
 
 std::mutex g_mu;
 std::unordered_map<const void*, DevGraph> g_graphs;  // per OODGraph object
 
-// upload the key set (the graph handle retains it; released with the graph)
-ra_kv* upload_keys(const std::shared_ptr<const VectorSet>& keys) {
-  ra_kv* kv = nullptr;
-  check(ra_kv_create(thread_ctx(), keys->data.data(), nullptr, keys->n, keys->d, 0, &kv));
-  return kv;
+void purge_locked() {
+  for (auto it = g_graphs.begin(); it != g_graphs.end();) {
+    if (it->second.keys.expired()) {
+      ra_graph_free(it->second.g);
+      it = g_graphs.erase(it);
+    } else {
+      ++it;
+    }
+  }
 }
 
-void attach(const void* self, const DevGraph& d) {
+void attach(const void* self, DevGraph d) {
   std::lock_guard<std::mutex> lk(g_mu);
+  purge_locked();
   auto it = g_graphs.find(self);
   if (it != g_graphs.end() && it->second.g) ra_graph_free(it->second.g);
-  g_graphs[self] = d;
+  g_graphs[self] = std::move(d);
+}
+
+// the attached graph if it still describes this object's CSR
+ra_graph* lookup(const void* self, const std::shared_ptr<const VectorSet>& keys,
+                 const std::vector<uint32_t>& adjacency, uint64_t entry) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_graphs.find(self);
+  if (it != g_graphs.end() && it->second.keys_id == keys.get() &&
+      it->second.keys.lock() == keys && it->second.adj_data == adjacency.data() &&
+      it->second.adj_size == adjacency.size() && it->second.entry == entry)
+    return it->second.g;
+  return nullptr;
 }
 
 }  // namespace
@@ -101,7 +105,7 @@ void OODGraph::build(const VectorSet& tq, const OODGraphBuildParams& p, int /*n_
                      p.prune_rule == PruneRule::InnerProduct ? 1 : 0,
                      p.default_ef};
   ra_graph* g = nullptr;
-  ra_kv* kv = upload_keys(keys_);
+  ra_kv* kv = gpu::keys_kv(keys_);
   const ra_status st = ra_graph_build(thread_ctx(), kv, tq.n ? tq.data.data() : nullptr, tq.n,
                                       tq.d, 0, &bp, nullptr, &g);
   ra_kv_release(kv);  // the graph holds its own reference
@@ -112,13 +116,13 @@ void OODGraph::build(const VectorSet& tq, const OODGraphBuildParams& p, int /*n_
   offsets_.assign(keys_->n + 1, 0);
   adjacency_.resize((ra_graph_memory_bytes(g) - offsets_.size() * 8) / 4);
   check(ra_graph_csr(g, offsets_.data(), adjacency_.data()));
-  attach(this, DevGraph{keys_.get(), adjacency_.data(), adjacency_.size(), entry_point_, g});
+  attach(this, DevGraph{keys_, keys_.get(), adjacency_.data(), adjacency_.size(), entry_point_, g});
 }
 
 // strict OODG v1 validation happens in ra_graph_deserialize (same texts)
 void OODGraph::from_blob(const std::string& blob) {
   ra_graph* g = nullptr;
-  ra_kv* kv = upload_keys(keys_);
+  ra_kv* kv = gpu::keys_kv(keys_);
   const ra_status st = ra_graph_deserialize(thread_ctx(), kv, blob.data(), blob.size(), &g);
   ra_kv_release(kv);
   check(st);
@@ -127,8 +131,35 @@ void OODGraph::from_blob(const std::string& blob) {
   offsets_.assign(keys_->n + 1, 0);
   adjacency_.resize((ra_graph_memory_bytes(g) - offsets_.size() * 8) / 4);
   check(ra_graph_csr(g, offsets_.data(), adjacency_.data()));
-  attach(this, DevGraph{keys_.get(), adjacency_.data(), adjacency_.size(), entry_point_, g});
+  attach(this, DevGraph{keys_, keys_.get(), adjacency_.data(), adjacency_.size(), entry_point_, g});
 }
+
+namespace gpu {
+// the object's CSR identity through its public accessors (adjacency_ starts
+// at neighbors(0); its size follows from memory_bytes(), :413-415)
+ra_graph* device_graph(const OODGraph& og) {
+  const auto& keys = og.keys();
+  const uint32_t* adj = og.neighbors(0).data();
+  const size_t adj_size = (og.memory_bytes() - (keys->n + 1) * sizeof(uint64_t)) / 4;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_graphs.find(&og);
+    if (it != g_graphs.end() && it->second.keys_id == keys.get() &&
+        it->second.keys.lock() == keys && it->second.adj_data == adj &&
+        it->second.adj_size == adj_size && it->second.entry == og.entry_point())
+      return it->second.g;
+  }
+  // e.g. a copied object: upload its CSR once
+  const std::string blob = og.serialize();
+  ra_graph* g = nullptr;
+  ra_kv* kv = keys_kv(keys);
+  const ra_status st = ra_graph_deserialize(thread_ctx(), kv, blob.data(), blob.size(), &g);
+  ra_kv_release(kv);
+  check(st);
+  attach(&og, DevGraph{keys, keys.get(), adj, adj_size, og.entry_point(), g});
+  return g;
+}
+}  // namespace gpu
 
 SearchResult OODGraph::search(std::span<const float> q, size_t k, Mask mask,
                               std::optional<uint32_t> ef) const {
@@ -136,23 +167,7 @@ SearchResult OODGraph::search(std::span<const float> q, size_t k, Mask mask,
   if (k < 1) throw std::invalid_argument("k must be >= 1");
   const size_t e = ef ? size_t(*ef) : size_t(default_ef_);
   if (e < k) throw std::invalid_argument("ef must be >= k");
-  ra_graph* g = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(g_mu);
-    auto it = g_graphs.find(this);
-    if (it != g_graphs.end() && it->second.keys == keys_.get() &&
-        it->second.adj_data == adjacency_.data() && it->second.adj_size == adjacency_.size() &&
-        it->second.entry == entry_point_)
-      g = it->second.g;
-  }
-  if (!g) {  // e.g. a copied object: upload its CSR once
-    const std::string blob = serialize();
-    ra_kv* kv = upload_keys(keys_);
-    const ra_status st = ra_graph_deserialize(thread_ctx(), kv, blob.data(), blob.size(), &g);
-    ra_kv_release(kv);
-    check(st);
-    attach(this, DevGraph{keys_.get(), adjacency_.data(), adjacency_.size(), entry_point_, g});
-  }
+  ra_graph* g = gpu::device_graph(*this);
   std::vector<uint32_t> ids(k);
   std::vector<float> scores(k);
   uint32_t n_out = 0;
@@ -194,15 +209,7 @@ uint64_t OODGraph::reachable_count() const {
 }
 
 std::string OODGraph::serialize() const {
-  ra_graph* g = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(g_mu);
-    auto it = g_graphs.find(this);
-    if (it != g_graphs.end() && it->second.keys == keys_.get() &&
-        it->second.adj_data == adjacency_.data() && it->second.adj_size == adjacency_.size() &&
-        it->second.entry == entry_point_)
-      g = it->second.g;
-  }
+  ra_graph* g = lookup(this, keys_, adjacency_, entry_point_);
   if (g) {  // byte format produced by the library (OODG v1)
     uint64_t size = 0;
     check(ra_graph_serialize(g, nullptr, 0, &size));

@@ -78,7 +78,8 @@ def main():
              "compactions_mean": float(c[:, 6].mean()),
              "misses_mean": float(c[:, 0].mean()),
              # RA_PIPE_PROFILE builds: per-phase cycles (top/stop, pop, expand, visit)
-             "profile_cycles_mean": [float(c[:, j].mean()) for j in (7, 8, 9, 10)]}
+             "profile_cycles_mean": [float(c[:, j].mean()) for j in (7, 8, 9, 10)],
+             "profile_adj_tma_cycles_mean": [float(c[:, 5].mean()), float(c[:, 11].mean())]}
         slow = np.argsort(-cyc)[:8]
         r["slowest"] = [{"head": int(h), "cycles": float(cyc[h]), "expanded": float(exp[h]),
                          "fo_pops": float(c[h, 8]), "fo_flags": int(c[h, 9])} for h in slow]
