@@ -450,6 +450,7 @@ def main():
         if world == 1 and not a.no_cpu_baseline:
             res["cpu_baseline"], res["parity"] = cpu_baseline(a, keys_host, vals_host, graphs,
                                                               Q, cfg, parity_jobs)
+            res["dropin"] = dropin_decode(a, res["e2e"]["value"])
         print(json.dumps(res))
     if dist is not None:
         dist.destroy_process_group()
@@ -756,6 +757,44 @@ def cpu_baseline(a, keys_host, vals_host, graphs, Q, cfg, parity_jobs):
     if parity is not None and parity_jobs:
         parity["lines"] = line_parity(o, parity_jobs, threads)
     return base, parity
+
+
+def dropin_decode(a, e2e_ms):
+    """The reference's own API end to end on the GPU backend: the reference
+    library with src/index_oodgraph.cpp, attention.cpp and engine.cpp
+    replaced by the drop-in TUs (paper_2409_10516_b200/host/*_gpu.cpp over
+    libra_b200.so; oracle/_ref/libattnindex_dropin.so): generate_workload
+    (seed 7) -> engine_init (ood_build per head, on the GPU) -> decode_step
+    per token, timed on the host clock (a synchronous C++ call: host q in,
+    TraceEntry out, copies included)."""
+    from oracle.ffi import BuildParams, Oracle, available
+    if not available("dropin"):
+        return {"unavailable": "oracle/_ref/libattnindex_dropin.so not built"}
+    o = Oracle("dropin")
+    n_dec = a.warmup + a.steps
+    t0 = time.time()
+    eng, dq, _, _, ms_gen, ms_build = o.engine_from_workload(
+        a.n_ctx, a.heads, a.groups, 7, n_dec,
+        BuildParams(a.k_train, a.max_degree, a.ef_construction, 8), 128, 512, a.top_k, a.ef,
+        os.cpu_count() or 1, 1)
+    for i in range(a.warmup):
+        eng.step(np.ascontiguousarray(dq[:, i, :]), i)
+    times = []
+    for i in range(a.warmup, n_dec):
+        q = np.ascontiguousarray(dq[:, i, :])
+        t1 = time.perf_counter()
+        eng.step(q, i)
+        times.append((time.perf_counter() - t1) * 1e3)
+    ms = statistics.mean(times)
+    del eng
+    return {"value": round(ms, 4), "unit": "ms/token",
+            "vs_ra_engine_step_host": round(ms / e2e_ms, 3) if e2e_ms else None,
+            "steps": len(times), "setup_s": round(time.time() - t0, 1),
+            "setup_ms": {"generate_workload": round(ms_gen, 1),
+                         "engine_init_gpu_builds": round(ms_build, 1)},
+            "path": "reference decode_step (engine.cpp:105-115) -> drop-in "
+                    "attnindex_engine_gpu.cpp -> ra_engine_step_host (one batched device "
+                    "step for all 32 heads), host clock per call"}
 
 
 def cfg_hpg(a):

@@ -109,6 +109,15 @@ _SIGS = {
     "ra_engine_last_timing": (C.c_int, [c_vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "ra_engine_kernels_per_step": (C.c_uint32, [c_vp]),
     "ra_engine_k": (C.c_uint32, [c_vp]),
+    "ra_kv_attach_values": (C.c_int, [c_vp, c_vp, c_vp, C.c_uint64, C.c_int]),
+    "ra_kv_has_values": (C.c_int, [c_vp]),
+    "ra_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(c_vp)]),
+    "ra_host_free": (None, [c_vp]),
+    "ra_partial_attention_host": (C.c_int, [c_vp, c_vp, C.c_uint32, c_vp, C.c_uint64, c_vp,
+                                            C.c_uint64, C.c_uint32, c_vp, C.c_uint64, c_vp,
+                                            c_vp, c_vp]),
+    "ra_merge_host": (C.c_int, [c_vp, C.c_uint32, c_vp, C.c_double, C.c_double, C.c_int, c_vp,
+                                C.c_double, C.c_double, C.c_int, c_vp, c_vp, c_vp]),
     "ra_engine_debug_counters": (C.c_int, [c_vp, c_u64p]),
     "ra_engine_debug_counters_per_head": (C.c_int, [c_vp, c_u64p]),
 }

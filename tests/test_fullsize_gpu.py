@@ -61,3 +61,46 @@ def test_fullsize_search_and_step_match_reference(layer):
         np.testing.assert_array_equal(sc, rsc)
         rel = np.linalg.norm(out - rout, axis=1) / np.linalg.norm(rout, axis=1)
         assert rel.max() <= 1e-12, rel
+
+
+def test_fullsize_build_blob_identical_to_reference_ood_build():
+    """configs[1]'s graph build at full size: the REFERENCE's own ood_build
+    (oracle/_ref, all host threads) and our GPU build on the same 128K head
+    (reference generator, seed 7, README parameters) write the same OODG
+    bytes (kNN lists, projection, prune, entry point and repair)."""
+    import os
+    import paper_2409_10516_b200 as ra
+    from oracle.ffi import BuildParams, Oracle
+    o = Oracle("ref")
+    n = 131072
+    w = o.generate_workload(n, 256, 128, 1, 1, seed=7, n_decode=1, n_threads=os.cpu_count())
+    keys, pq = w["keys"][0], w["prefill_q"][0]
+    ref_blob = o.graph_build(keys, pq, BuildParams(128, 24, 256, 8), n_threads=os.cpu_count())
+    kv = ra.KVGroup(keys, w["values"][0])
+    g = ra.ood_build(kv, pq, ra.OODGraphBuildParams(128, 24, 256, 8))
+    assert g.serialize() == ref_blob
+
+
+def test_256k_search_identical_to_reference():
+    """256K context (between configs[1] and configs[4]): GPU-built graph,
+    eight masked searches on the GPU vs the reference's search on the same
+    graph: identical ids, f32 scores, scanned and truncated."""
+    import paper_2409_10516_b200 as ra
+    from oracle.ffi import Oracle
+    from paper_2409_10516_b200.workload import WorkloadSpec, generate_group
+    n = 262144
+    spec = WorkloadSpec(n_ctx=n, d_model=256, d_head=128, n_heads=32, n_kv_groups=8,
+                        seed=11, n_decode=8)
+    w = generate_group(spec, 5, "cuda")
+    kv = ra.KVGroup(w["keys"], w["values"])
+    g = ra.ood_build(kv, w["prefill_q"][1], ra.OODGraphBuildParams(128, 24, 256, 8))
+    K = w["keys"].cpu().numpy()
+    Q = w["decode_q"][1].cpu().numpy()
+    W = ra.static_partition(n, 128, 512).static_set
+    og = Oracle("ref").graph(K, g.serialize())
+    res = ra.search_batch([g], Q, 100, W, 128).host()
+    for i in range(Q.shape[0]):
+        r = og.search(Q[i], 100, W, 128)
+        np.testing.assert_array_equal(res[i].ids, r.ids)
+        np.testing.assert_array_equal(res[i].scores, r.scores)
+        assert res[i].scanned == r.scanned and res[i].truncated == r.truncated
