@@ -11,6 +11,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <functional>
@@ -107,8 +108,10 @@ inline bool enter_subcase() {
 inline int run_all() {
   auto& s = state();
   int failed_cases = 0;
+  const bool verbose = std::getenv("DOCTEST_SHIM_VERBOSE") != nullptr;
   for (const auto& tc : registry()) {
     s.current = tc.name;
+    if (verbose) std::fprintf(stderr, "[doctest-shim] running \"%s\"\n", tc.name), std::fflush(stderr);
     s.case_failed = false;
     s.subcase_target = 0;
     for (;;) {

@@ -851,7 +851,8 @@ void engine_enqueue(ra_engine* e, const float* q_dev, double* out_dev, uint32_t*
     sa.expanded = e->expanded.p;
     sa.dbg = e->dbg.p;
     sa.fa = {e->hvals.p, e->w_ids.p, uint32_t(e->n_static), e->fa_nchunk,
-             1.0 / std::sqrt(double(d)), out_dev, e->fa_chunk.p};
+             std::max<uint32_t>(e->max_M, 1), 1.0 / std::sqrt(double(d)), out_dev,
+             e->fa_chunk.p};
     launch_graph_search(ctx, sa, e->max_n, e->search_scratch.p);
     record_timing(e->ev[1], s);
     record_timing(e->ev[2], s);

@@ -227,7 +227,8 @@ struct SearchArgs {
   struct FusedAttn {
     const float* const* values;  // [B] the head's V rows (n x d f32)
     const uint32_t* W;           // static ids, ascending
-    uint32_t nW, nchunk;         // nchunk = ceil(nW / rows per chunk)
+    uint32_t nW, nchunk;         // nchunk = ceil(nW / crows)
+    uint32_t crows;              // W rows per chunk (<= 32 and <= the helpers' tile rows)
     double inv_sqrt_d;
     double* out;                 // [B][d] attention output
     double* chunk;               // scratch [B][nchunk][d + 2]: (out, max, expsum)

@@ -1083,12 +1083,13 @@ bool try_launch_cta(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* s
 
 // RA_SEARCH_KERNEL = pipe (default: latency or throughput mode by batch) |
 // tp | lat | tpr (throughput, register rows only) | tps (throughput, shared
-// visited bits + TMA tile) | cta | warp selects the K6 variant
+// visited bits + TMA tile) | duo (tps + an expansion warp per query) | cta |
+// warp selects the K6 variant
 int search_variant_of(const char* e) {
   if (!e) return 0;
   const std::string s(e);
   return s == "cta" ? 1 : s == "warp" ? 2 : s == "tp" ? 3 : s == "lat" ? 4 : s == "tpr" ? 5
-         : s == "tps" ? 6 : s == "pipe" || s == "auto" ? 0 : -1;
+         : s == "tps" ? 6 : s == "duo" ? 7 : s == "pipe" || s == "auto" ? 0 : -1;
 }
 
 int search_variant(const ra_ctx* ctx) {
@@ -1112,7 +1113,7 @@ void launch_graph_search(ra_ctx* ctx, SearchArgs a, uint32_t max_n, uint8_t* scr
   if ((variant == 0 || variant >= 3 || a.bf16) &&
       launch_graph_search_pipe(ctx, a, max_n, scratch,
                                variant == 3 ? 1 : variant == 4 ? 2 : variant == 5 ? 3
-                               : variant == 6 ? 4 : 0))
+                               : variant == 6 ? 4 : variant == 7 ? 5 : 0))
     return;
   // the older kernels read f32 rows; the f32 copy of a bf16 group holds the
   // same rounded values, so they stay exact for shapes the pipe kernel skips

@@ -73,3 +73,33 @@ def test_three_kernel_path_matches_reference():
                         "engine_matches or window"], env=env, cwd=ROOT, capture_output=True,
                        text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:]
+
+
+@pytest.mark.parametrize("M,d", [(2, 32), (4, 32), (8, 16), (6, 64)])
+def test_fused_step_small_degree_matches_oracle(M, d):
+    """Low-degree graphs give the helpers short tiles; the fused tail still
+    stages its W partials and V rows there (the launch grows the tiles), and
+    the step equals the reference's run_head (engine.cpp:69-101)."""
+    import paper_2409_10516_b200 as ra
+    from oracle.ffi import BuildParams, Oracle
+    port = Oracle("port")
+    w = port.generate_workload(1500, 64, d, 2, 1, seed=3, n_decode=2)
+    bp = BuildParams(k_train=8, max_degree=M, ef_construction=16)
+    blobs = [port.graph_build(w["keys"][0], w["prefill_q"][h], bp) for h in range(2)]
+    kv = ra.KVGroup(w["keys"][0], w["values"][0])
+    eng = ra.Engine([kv], [ra.OODGraph.from_blob(kv, b) for b in blobs],
+                    ra.EngineConfig(16, 64, 20, 32))
+    if os.environ.get("RA_FUSED_ATTN") != "0" and d >= 32:
+        assert eng.kernels_per_step() == 1
+    Q = np.ascontiguousarray(w["decode_q"][:, 0, :])
+    out, om, sc = eng.decode_step(Q)
+    W = ra.static_partition(1500, 16, 64).static_set
+    for h in range(2):
+        r = port.graph(w["keys"][0], blobs[h]).search(Q[h], 20, W, 32)
+        assert np.array_equal(om[h][: len(r.ids)], r.ids) and int(sc[h]) == r.scanned
+        pw = port.partial_attention(Q[h], w["keys"][0], w["values"][0], W)
+        po = port.partial_attention(Q[h], w["keys"][0], w["values"][0], r.ids)
+        ref = port.merge(pw, po, d)[0]
+        # W partials are summed per chunk and merged (the reference sums W in
+        # one pass): a few ulp, far inside north_star's 1e-3
+        assert np.linalg.norm(out[h] - ref) / np.linalg.norm(ref) <= 1e-9

@@ -219,7 +219,7 @@ def test_search_throughput_mode_matches_oracle(port):
             assert_same(res[qi], og.search(Q[qi], k, m, ef), f"tp ef={ef} q={qi}")
 
 
-@pytest.mark.parametrize("kernel", ["lat", "tp", "tps", "tpr"])
+@pytest.mark.parametrize("kernel", ["lat", "tp", "tps", "tpr", "duo"])
 def test_search_kernel_variants_identical(port, kernel):
     """Every K6 variant (latency CTA pipeline, throughput with shared-memory
     visited bits + TMA tiles, throughput with register rows) returns the
