@@ -11,11 +11,15 @@
 //                     global sort+unique runs on CUB radix sort
 //   K3 k_prune        phase 3 occlusion prune, one warp per node (:162-202)
 //   K4 entry point    medoid / max-norm argmin-argmax (:207-233)
-//   K5 repair         phase 4 (:235-348): host-orchestrated loop (the rare,
-//                     sequential part) with the nearest-anchor scan on the GPU
+//   K5 repair         phase 4 (:235-348) on the GPU: reachability by a
+//                     cooperative level-synchronous BFS, pending / anchor
+//                     lists by stream compaction, nearest anchor, (anchor,
+//                     node) sort, one thread per anchor group for the chained
+//                     attachments; the host only reads the round's counts
 // Every f64 reduction runs in the reference's order (through the
 // sequential-order Eigen contract of oracle/shim), so adjacency, entry point
 // and OODG blob are bit-identical to the oracle build.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -555,6 +559,215 @@ __global__ void k_nearest_anchor(const float* __restrict__ keys, uint32_t d,
   if (threadIdx.x == 0) nearest[i] = anchors[sj[0]];
 }
 
+// ---- K5: reachability (the reference's DFS sweep :240-253 and, for the
+// no-anchor case, its BFS depths :263-279; only the reached SET and the BFS
+// depth matter, so a level-synchronous parallel BFS gives both) ---------------
+// depth[] = 0xFFFFFFFF (unreached) on entry; cnt[3] = 0. Cooperative launch.
+__global__ void __launch_bounds__(512)
+    k_bfs(const uint32_t* __restrict__ adj, const uint32_t* __restrict__ deg, uint32_t M,
+          uint32_t entry, uint32_t* depth, uint32_t* qa, uint32_t* qb, uint32_t* cnt) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const uint64_t tid = grid.thread_rank(), nt = grid.size();
+  if (tid == 0) {
+    depth[entry] = 0;
+    qa[0] = entry;
+    cnt[0] = 1;
+  }
+  grid.sync();
+  uint32_t* cur = qa;
+  uint32_t* nxt = qb;
+  // cnt[L % 3] = size of level L; cnt[(L + 1) % 3] was zeroed during level
+  // L - 1; cnt[(L + 2) % 3] (level L - 1's, read by everyone) is zeroed now
+  for (uint32_t level = 0;; ++level) {
+    const uint32_t ncur = *reinterpret_cast<volatile uint32_t*>(cnt + level % 3);
+    if (ncur == 0) break;
+    if (tid == 0) cnt[(level + 2) % 3] = 0;
+    for (uint64_t i = tid; i < uint64_t(ncur) * M; i += nt) {
+      const uint32_t u = cur[i / M], e = uint32_t(i % M);
+      if (e < deg[u]) {
+        const uint32_t v = adj[size_t(u) * M + e];
+        if (atomicCAS(depth + v, 0xFFFFFFFFu, level + 1) == 0xFFFFFFFFu)
+          nxt[atomicAdd(cnt + (level + 1) % 3, 1u)] = v;
+      }
+    }
+    grid.sync();
+    uint32_t* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+}
+
+// reachability only (the reference's DFS sweep, :240-253): a work queue
+// instead of BFS levels (attachment chains make the graph thousands of levels
+// deep). Each thread claims the next queue slot, waits for it to be published
+// (q[] pre-filled with kSentinel), pushes the unmarked neighbours, and counts
+// the node as processed; a thread whose slot is never published leaves once
+// every published node is processed (processed == tail, read around it).
+// mark[entry] = 1, q[0] = entry, ctr = {tail 1, head 0, processed 0} on entry.
+__global__ void __launch_bounds__(256)
+    k_reach(const uint32_t* __restrict__ adj, const uint32_t* __restrict__ deg, uint32_t M,
+            uint32_t n, uint32_t* mark, uint32_t* q, uint32_t* ctr) {
+  volatile uint32_t* vq = q;
+  volatile uint32_t* vc = ctr;
+  for (;;) {
+    const uint32_t i = atomicAdd(ctr + 1, 1u);
+    uint32_t u;
+    for (;;) {
+      u = i < n ? vq[i] : 0xFFFFFFFFu;  // (claims run past n once everything is queued)
+      if (u != kSentinel) break;
+      const uint32_t t1 = vc[0];
+      if (i < t1) continue;  // claimed slot published, store not visible yet
+      const uint32_t pr = vc[2];
+      if (pr == t1 && vc[0] == t1) return;  // nothing in flight: all reached
+      __nanosleep(64);
+    }
+    const uint32_t dg = deg[u];
+    for (uint32_t e = 0; e < dg; ++e) {
+      const uint32_t v = adj[size_t(u) * M + e];
+      if (atomicExch(mark + v, 1u) == 0u) {
+        const uint32_t slot = atomicAdd(ctr, 1u);
+        vq[slot] = v;
+      }
+    }
+    __threadfence();
+    atomicAdd(ctr + 2, 1u);
+  }
+}
+
+__global__ void k_reach_init(uint32_t* mark, uint32_t* q, uint32_t* ctr, uint32_t entry) {
+  mark[entry] = 1;
+  q[0] = entry;
+  ctr[0] = 1, ctr[1] = 0, ctr[2] = 0;
+}
+
+// flags for the round's lists (:256-262): pending = unreached, anchors =
+// reached with spare degree
+__global__ void k_repair_flags(const uint32_t* __restrict__ mark, const uint32_t* __restrict__ deg,
+                               uint32_t n, uint32_t M, uint8_t* pend, uint8_t* anch) {
+  const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  const bool r = mark[u] != 0;
+  pend[u] = !r;
+  anch[u] = r && deg[u] < M;
+}
+
+// no anchor (:263-282): the deepest reached node (depth desc, id asc) drops
+// its last edge and becomes the only anchor. One block.
+__global__ void k_deepest_drop(const uint32_t* __restrict__ depth, uint32_t n, uint32_t M,
+                               uint32_t* adj, uint32_t* deg, uint32_t* anchors) {
+  __shared__ unsigned long long red[32];
+  unsigned long long best = 0;  // (depth + 1) << 32 | ~id: max = deepest, then lowest id
+  for (uint32_t u = threadIdx.x; u < n; u += blockDim.x) {
+    const uint32_t dp = depth[u];
+    if (dp != 0xFFFFFFFFu) {
+      const unsigned long long key = (uint64_t(dp) + 1) << 32 | uint32_t(~u);
+      if (key > best) best = key;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(kFull, best, o);
+    if (x > best) best = x;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint32_t w = 1; w < blockDim.x / 32; ++w)
+      if (red[w] > best) best = red[w];
+    const uint32_t u = ~uint32_t(best);
+    const uint32_t dg = deg[u] - 1;  // adj[deepest].pop_back()
+    adj[size_t(u) * M + dg] = kSentinel;
+    deg[u] = dg;
+    anchors[0] = u;
+  }
+}
+
+__global__ void k_pair_keys(const uint32_t* __restrict__ nearest,
+                            const uint32_t* __restrict__ pending, uint32_t np, uint64_t* keys) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < np) keys[i] = (uint64_t(nearest[i]) << 32) | pending[i];
+}
+
+// the chained attachments (:320-345), one block per anchor group of the
+// sorted (anchor, node) pairs; groups touch disjoint rows (their anchor and
+// their own pending nodes). The group's node ids and degrees are staged in
+// shared memory, so the sequential chain (each step depends on where the
+// previous node went) runs on-chip; groups beyond kAttachCap nodes walk the
+// global arrays. `deferred` counts the nodes left for the next round.
+constexpr uint32_t kAttachCap = 6144;
+
+__global__ void __launch_bounds__(256)
+    k_attach(const uint64_t* __restrict__ keys, uint32_t np, uint32_t M, uint32_t* adj,
+             uint32_t* deg, uint32_t* deferred) {
+  __shared__ uint32_t s_id[kAttachCap];
+  __shared__ uint16_t s_dg[kAttachCap];
+  __shared__ uint32_t s_end;
+  const uint32_t g0 = blockIdx.x;
+  const uint32_t a = uint32_t(keys[g0] >> 32);
+  if (g0 > 0 && uint32_t(keys[g0 - 1] >> 32) == a) return;  // not a group start
+  // group end: the first index whose anchor differs
+  if (threadIdx.x == 0) s_end = np;
+  __syncthreads();
+  for (uint32_t c = g0; c < np; c += blockDim.x) {
+    const uint32_t i = c + threadIdx.x;
+    if (i < np && uint32_t(keys[i] >> 32) != a) atomicMin(&s_end, i);
+    __syncthreads();
+    if (s_end != np) break;
+  }
+  const uint32_t L = s_end - g0;
+  if (L <= kAttachCap && M < 65536u) {
+    for (uint32_t j = threadIdx.x; j < L; j += blockDim.x) {
+      const uint32_t u = uint32_t(keys[g0 + j]);
+      s_id[j] = u;
+      s_dg[j] = uint16_t(deg[u]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t dA = deg[a], tj = 0xFFFFFFFFu, next_t = 0, i = 0;  // tj = max: t is the anchor
+      for (; i < L; ++i) {
+        uint32_t dt = tj == 0xFFFFFFFFu ? dA : s_dg[tj];
+        bool def = false;
+        while (dt >= M) {
+          if (next_t >= i) {
+            def = true;
+            break;
+          }
+          tj = next_t++;
+          dt = s_dg[tj];
+        }
+        if (def) break;
+        const uint32_t u = s_id[i];
+        adj[size_t(tj == 0xFFFFFFFFu ? a : s_id[tj]) * M + dt] = u;
+        if (tj == 0xFFFFFFFFu) ++dA;
+        else s_dg[tj] = uint16_t(dt + 1);
+        if (s_dg[i] < M) tj = i;
+      }
+      deg[a] = dA;
+      if (i < L) atomicAdd(deferred, L - i);
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < L; j += blockDim.x) deg[s_id[j]] = s_dg[j];
+    return;
+  }
+  if (threadIdx.x != 0) return;
+  uint32_t t = a, next_t = 0, i = g0;
+  for (; i < s_end; ++i) {
+    const uint32_t u = uint32_t(keys[i]);
+    bool def = false;
+    while (deg[t] >= M) {
+      if (next_t >= i - g0) {  // attached so far = the group's nodes before i
+        def = true;
+        break;
+      }
+      t = uint32_t(keys[g0 + next_t++]);
+    }
+    if (def) break;
+    adj[size_t(t) * M + deg[t]++] = u;
+    if (deg[u] < M) t = u;
+  }
+  if (i < s_end) atomicAdd(deferred, s_end - i);
+}
+
 struct Timer {
   cudaStream_t s;
   cudaEvent_t a, b;
@@ -601,118 +814,87 @@ __global__ void k_flat_pick(const uint32_t* __restrict__ ids, const double* __re
 
 }  // namespace
 
-// host-orchestrated phase 4 on the fixed-stride host mirror (row u =
-// adj[u*M .. u*M+deg[u]); appends stay within M by construction);
-// nearest-anchor on the GPU
+// phase 4 (:235-348) on the device rows (row u = adj[u*M .. u*M+deg[u]),
+// kSentinel past it; appends stay within M by construction)
 static void repair(ra_ctx* ctx, ra_kv* kv, const double* norms_dev, uint64_t entry,
-                   uint32_t M, std::vector<uint32_t>& adj, std::vector<uint32_t>& deg,
-                   ra_build_stats* st) {
+                   uint32_t M, uint32_t* adj, uint32_t* deg, ra_build_stats* st) {
   const uint32_t n = uint32_t(kv->n), d = kv->d;
-  std::vector<uint8_t> reached(n);
-  std::vector<uint32_t> stack;
-  stack.reserve(n);
-  auto sweep = [&] {
-    std::fill(reached.begin(), reached.end(), 0);
-    stack.clear();
-    stack.push_back(uint32_t(entry));
-    reached[entry] = 1;
-    while (!stack.empty()) {
-      const uint32_t u = stack.back();
-      stack.pop_back();
-      const uint32_t* row = adj.data() + size_t(u) * M;
-      for (uint32_t e = 0; e < deg[u]; ++e) {
-        const uint32_t v = row[e];
-        if (!reached[v]) {
-          reached[v] = 1;
-          stack.push_back(v);
-        }
-      }
-    }
-  };
+  cudaStream_t s = ctx->stream;
   static const bool trace = std::getenv("RA_REPAIR_TRACE") != nullptr;
-  auto now = [] { return std::chrono::steady_clock::now(); };
-  auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-  auto t0 = now();
-  sweep();
-  if (trace) fprintf(stderr, "repair: sweep %.2f ms\n", ms(t0, now()));
-  DevBuf<uint32_t> d_pend, d_anch, d_near;
-  for (;;) {
-    auto t1 = now();
-    std::vector<uint32_t> pending;
-    for (uint32_t u = 0; u < n; ++u)
-      if (!reached[u]) pending.push_back(u);
-    if (pending.empty()) break;
-    st->repair_rounds++;
-    st->repaired_nodes += pending.size();
-    std::vector<uint32_t> anchors;
-    for (uint32_t v = 0; v < n; ++v)
-      if (reached[v] && deg[v] < M) anchors.push_back(v);
-    if (anchors.empty()) {
-      std::vector<uint32_t> depth(n, UINT32_MAX), queue{uint32_t(entry)};
-      depth[entry] = 0;
-      uint32_t deepest = uint32_t(entry);
-      for (size_t h = 0; h < queue.size(); ++h) {
-        const uint32_t u = queue[h];
-        if (depth[u] > depth[deepest] || (depth[u] == depth[deepest] && u < deepest)) deepest = u;
-        for (uint32_t e = 0; e < deg[u]; ++e) {
-          const uint32_t v = adj[size_t(u) * M + e];
-          if (depth[v] == UINT32_MAX) {
-            depth[v] = depth[u] + 1;
-            queue.push_back(v);
-          }
-        }
-      }
-      --deg[deepest];  // drop its last edge
-      anchors.push_back(deepest);
-    }
-    d_pend.ensure(pending.size());
-    d_anch.ensure(anchors.size());
-    d_near.ensure(pending.size());
-    RA_CUDA(cudaMemcpyAsync(d_pend.p, pending.data(), pending.size() * 4,
-                            cudaMemcpyHostToDevice, ctx->stream));
-    RA_CUDA(cudaMemcpyAsync(d_anch.p, anchors.data(), anchors.size() * 4,
-                            cudaMemcpyHostToDevice, ctx->stream));
-    k_nearest_anchor<<<uint32_t(pending.size()), 256, 0, ctx->stream>>>(
-        kv->keys.p, d, norms_dev, d_pend.p, uint32_t(pending.size()), d_anch.p,
-        uint32_t(anchors.size()), d_near.p);
-    RA_LAUNCH_CHECK();
-    std::vector<uint32_t> nearest(pending.size());
-    RA_CUDA(cudaMemcpyAsync(nearest.data(), d_near.p, pending.size() * 4,
-                            cudaMemcpyDeviceToHost, ctx->stream));
-    RA_CUDA(cudaStreamSynchronize(ctx->stream));
-    auto t2 = now();
-    std::vector<std::pair<uint32_t, uint32_t>> by_anchor(pending.size());
-    for (size_t i = 0; i < pending.size(); ++i) by_anchor[i] = {nearest[i], pending[i]};
-    std::sort(by_anchor.begin(), by_anchor.end());
-    size_t g0 = 0;
-    while (g0 < by_anchor.size()) {
-      size_t g1 = g0;
-      while (g1 < by_anchor.size() && by_anchor[g1].first == by_anchor[g0].first) ++g1;
-      uint32_t t = by_anchor[g0].first;
-      std::vector<uint32_t> attached;
-      size_t next_t = 0;
-      bool deferred = false;
-      for (size_t i = g0; i < g1; ++i) {
-        const uint32_t u = by_anchor[i].second;
-        while (deg[t] >= M) {
-          if (next_t >= attached.size()) {
-            deferred = true;
-            break;
-          }
-          t = attached[next_t++];
-        }
-        if (deferred) break;
-        adj[size_t(t) * M + deg[t]++] = u;
-        attached.push_back(u);
-        if (deg[u] < M) t = u;
-      }
-      g0 = g1;
-    }
-    auto t3 = now();
-    sweep();
+  DevBuf<uint32_t> depth(n, s), qa(n, s), qb(n, s), cnt(3, s), lists(2 * size_t(n), s),
+      counts(2, s), nearest(n, s);
+  DevBuf<uint8_t> fl(2 * size_t(n), s);
+  DevBuf<uint64_t> keys(n, s), keys2(n, s);
+  int bps = 0;
+  RA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_bfs, 512, 0));
+  const uint32_t bfs_grid = uint32_t(std::max(1, bps) * ctx->num_sms);
+  size_t tb_sel = 0, tb_sort = 0;
+  cub::CountingInputIterator<uint32_t> ids(0);
+  cub::DeviceSelect::Flagged(nullptr, tb_sel, ids, fl.p, lists.p, counts.p, n, s);
+  cub::DeviceRadixSort::SortKeys(nullptr, tb_sort, keys.p, keys2.p, int64_t(n), 0, 64, s);
+  DevBuf<uint8_t> tmp(std::max(tb_sel, tb_sort), s);
+  for (uint32_t round = 0;; ++round) {
+    if (round > n) runtime("graph repair did not converge");
+    const auto t0 = std::chrono::steady_clock::now();
+    // the sweep: reached set (mark in depth[], q in qa[])
+    RA_CUDA(cudaMemsetAsync(depth.p, 0, size_t(n) * 4, s));
+    RA_CUDA(cudaMemsetAsync(qa.p, 0xFF, size_t(n) * 4, s));
+    k_reach_init<<<1, 1, 0, s>>>(depth.p, qa.p, cnt.p, uint32_t(entry));
+    k_reach<<<ctx->num_sms * 4, 256, 0, s>>>(adj, deg, M, n, depth.p, qa.p, cnt.p);
+    k_repair_flags<<<(n + 255) / 256, 256, 0, s>>>(depth.p, deg, n, M, fl.p, fl.p + n);
+    size_t tb = tmp.n;
+    RA_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, ids, fl.p, lists.p, counts.p, n, s));
+    tb = tmp.n;
+    RA_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, ids, fl.p + n, lists.p + n, counts.p + 1, n, s));
+    uint32_t h[2] = {0, 0};
+    RA_CUDA(cudaMemcpyAsync(h, counts.p, 8, cudaMemcpyDeviceToHost, s));
+    RA_CUDA(cudaStreamSynchronize(s));
+    const uint32_t np = h[0];
+    uint32_t na = h[1];
     if (trace)
-      fprintf(stderr, "repair: pending %zu anchors %zu  nearest %.2f ms  attach %.2f ms  sweep %.2f ms\n",
-              pending.size(), anchors.size(), ms(t1, t2), ms(t2, t3), ms(t3, now()));
+      fprintf(stderr, "repair: round %u sweep+lists %.2f ms\n", round,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                  .count());
+    if (np == 0) break;
+    st->repair_rounds++;
+    st->repaired_nodes += np;
+    uint32_t* pending = lists.p;
+    uint32_t* anchors = lists.p + n;
+    bool dropped = false;
+    if (na == 0) {  // (rare) BFS depths for the deepest reached node
+      dropped = true;
+      RA_CUDA(cudaMemsetAsync(depth.p, 0xFF, size_t(n) * 4, s));
+      RA_CUDA(cudaMemsetAsync(cnt.p, 0, 12, s));
+      uint32_t e32 = uint32_t(entry);
+      uint32_t* ap = adj;
+      uint32_t* dp = deg;
+      void* args[] = {&ap, &dp, &M, &e32, &depth.p, &qa.p, &qb.p, &cnt.p};
+      RA_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_bfs), dim3(bfs_grid),
+                                          dim3(512), args, 0, s));
+      k_deepest_drop<<<1, 1024, 0, s>>>(depth.p, n, M, adj, deg, anchors);
+      na = 1;
+    }
+    k_nearest_anchor<<<np, 256, 0, s>>>(kv->keys.p, d, norms_dev, pending, np, anchors, na,
+                                        nearest.p);
+    k_pair_keys<<<(np + 255) / 256, 256, 0, s>>>(nearest.p, pending, np, keys.p);
+    tb = tmp.n;
+    RA_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, keys.p, keys2.p, int64_t(np), 0, 64, s));
+    RA_CUDA(cudaMemsetAsync(cnt.p, 0, 4, s));
+    k_attach<<<np, 256, 0, s>>>(keys2.p, np, M, adj, deg, cnt.p);
+    RA_LAUNCH_CHECK();
+    // every pending node attached beneath a reached one (and no edge dropped):
+    // all nodes are reached now, the reference's next sweep finds none pending
+    uint32_t ndef = 0;
+    RA_CUDA(cudaMemcpyAsync(&ndef, cnt.p, 4, cudaMemcpyDeviceToHost, s));
+    RA_CUDA(cudaStreamSynchronize(s));
+    if (trace) {
+      RA_CUDA(cudaStreamSynchronize(s));
+      fprintf(stderr, "repair: round %u pending %u anchors %u deferred %u  %.2f ms\n", round, np,
+              na, ndef,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                  .count());
+    }
+    if (ndef == 0 && !dropped) break;
   }
 }
 
@@ -902,9 +1084,6 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
     RA_LAUNCH_CHECK();
     std::vector<unsigned long long> hb(2 * eblocks);
     RA_CUDA(cudaMemcpyAsync(hb.data(), best.p, hb.size() * 8, cudaMemcpyDeviceToHost, s));
-    std::vector<uint32_t> h_adj(size_t(n) * M), h_deg(n);
-    RA_CUDA(cudaMemcpyAsync(h_adj.data(), g->adj.p, h_adj.size() * 4, cudaMemcpyDeviceToHost, s));
-    RA_CUDA(cudaMemcpyAsync(h_deg.data(), deg.p, h_deg.size() * 4, cudaMemcpyDeviceToHost, s));
     RA_CUDA(cudaStreamSynchronize(s));
     double bk = DBL_MAX;
     uint32_t bu = kSentinel;
@@ -917,26 +1096,20 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
     g->entry = bu;
     st.ms_entry = tm.lap();
 
-    // ---- phase 4 + CSR ----
-    const uint32_t rounds0 = st.repair_rounds;
-    const auto tr0 = std::chrono::steady_clock::now();
-    repair(ctx, kv, norms.p, g->entry, M, h_adj, h_deg, &st);
-    const auto tr1 = std::chrono::steady_clock::now();
-    g->offsets.assign(size_t(n) + 1, 0);
-    for (uint32_t u = 0; u < n; ++u) g->offsets[u + 1] = g->offsets[u] + h_deg[u];
-    g->adjacency.resize(g->offsets[n]);
-    for (uint32_t u = 0; u < n; ++u)
-      std::copy(h_adj.begin() + size_t(u) * M, h_adj.begin() + size_t(u) * M + h_deg[u],
-                g->adjacency.begin() + g->offsets[u]);
-    const auto tr2 = std::chrono::steady_clock::now();
-    if (st.repair_rounds != rounds0) graph_upload(ctx, g.get());  // else the device rows stand
-    const auto tr3 = std::chrono::steady_clock::now();
-    st.ms_repair = tm.lap();
-    if (std::getenv("RA_REPAIR_TRACE")) {
-      auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-      fprintf(stderr, "phase4: repair %.2f csr %.2f upload %.2f lap-wait %.2f ms\n", ms(tr0, tr1),
-              ms(tr1, tr2), ms(tr2, tr3), ms(tr3, std::chrono::steady_clock::now()));
+    // ---- phase 4 on the device; the host CSR mirror is built on first use ----
+    repair(ctx, kv, norms.p, g->entry, M, g->adj.p, deg.p, &st);
+    {
+      DevBuf<unsigned long long> esum(1, s);
+      size_t tb = 0;
+      cub::DeviceReduce::Sum(nullptr, tb, deg.p, esum.p, n, s);
+      DevBuf<uint8_t> tmp(tb, s);
+      RA_CUDA(cub::DeviceReduce::Sum(tmp.p, tb, deg.p, esum.p, n, s));
+      unsigned long long e = 0;
+      RA_CUDA(cudaMemcpyAsync(&e, esum.p, 8, cudaMemcpyDeviceToHost, s));
+      RA_CUDA(cudaStreamSynchronize(s));
+      g->n_edges = e;
     }
+    st.ms_repair = tm.lap();
 
     ra_kv_retain(kv);
     g->kv = kv;

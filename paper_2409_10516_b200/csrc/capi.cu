@@ -27,6 +27,31 @@ void graph_upload(ra_ctx* ctx, ra_graph* g) {
   RA_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+}  // namespace ra
+
+// the reference CSR from the device rows (kSentinel-padded), once
+void ra_graph::host_mirror() const {
+  std::call_once(host_once, [this] {
+    if (offsets.size() == n + 1) return;  // deserialized: the mirror came first
+    std::vector<uint32_t> rows(size_t(n) * max_degree);
+    {
+      ra::DeviceGuard dg(kv ? kv->device : 0);  // (a build synchronizes its stream before returning)
+      RA_CUDA(cudaMemcpy(rows.data(), adj.p, rows.size() * 4, cudaMemcpyDeviceToHost));
+    }
+    offsets.assign(size_t(n) + 1, 0);
+    adjacency.clear();
+    adjacency.reserve(n_edges);
+    for (uint64_t u = 0; u < n; ++u) {
+      const uint32_t* r = rows.data() + u * max_degree;
+      uint32_t dg = 0;
+      while (dg < max_degree && r[dg] != ra::kSentinel) adjacency.push_back(r[dg++]);
+      offsets[u + 1] = offsets[u] + dg;
+    }
+  });
+}
+
+namespace ra {
+
 static void check_ctx(ra_ctx* ctx) {
   if (!ctx) invalid("null context");
 }
@@ -261,6 +286,7 @@ ra_status ra_graph_deserialize(ra_ctx* ctx, ra_kv* keys, const char* blob, uint6
       }
     }
     if (pos != size) runtime("trailing bytes in graph blob");
+    g->n_edges = g->adjacency.size();
     DeviceGuard dg(ctx->device);
     graph_upload(ctx, g.get());
     ra_kv_retain(keys);
@@ -274,9 +300,10 @@ ra_status ra_graph_serialize(const ra_graph* g, char* buf, uint64_t cap, uint64_
   return guard([&] {
     if (!g) invalid("null graph");
     const uint64_t n = g->n;
-    const uint64_t total = 28 + 4 * n + 8 * uint64_t(g->adjacency.size());
+    const uint64_t total = 28 + 4 * n + 8 * g->n_edges;
     *size = total;
     if (!buf || cap < total) return;
+    g->host_mirror();
     char* p = buf;
     auto put = [&](const void* v, size_t b) {
       std::memcpy(p, v, b);
@@ -314,6 +341,7 @@ uint64_t ra_graph_entry_point(const ra_graph* g) { return g->entry; }
 uint32_t ra_graph_max_degree_bound(const ra_graph* g) { return g->max_degree; }
 uint32_t ra_graph_default_ef(const ra_graph* g) { return g->default_ef; }
 uint32_t ra_graph_degree(const ra_graph* g, uint64_t u) {
+  g->host_mirror();
   return uint32_t(g->offsets[u + 1] - g->offsets[u]);
 }
 uint32_t ra_graph_neighbors(const ra_graph* g, uint64_t u, uint32_t* out, uint32_t cap) {
@@ -323,6 +351,7 @@ uint32_t ra_graph_neighbors(const ra_graph* g, uint64_t u, uint32_t* out, uint32
 }
 // reachable_count (index_oodgraph.cpp:417-433)
 uint64_t ra_graph_reachable_count(const ra_graph* g) {
+  g->host_mirror();
   std::vector<uint8_t> seen(g->n, 0);
   std::vector<uint32_t> stack{uint32_t(g->entry)};
   seen[g->entry] = 1;
@@ -342,13 +371,14 @@ uint64_t ra_graph_reachable_count(const ra_graph* g) {
   return count;
 }
 uint64_t ra_graph_memory_bytes(const ra_graph* g) {
-  return g->offsets.size() * 8 + g->adjacency.size() * 4;
+  return (g->n + 1) * 8 + g->n_edges * 4;
 }
 uint64_t ra_graph_device_bytes(const ra_graph* g) { return g->adj.bytes(); }
 
 ra_status ra_graph_csr(const ra_graph* g, uint64_t* offsets, uint32_t* adjacency) {
   return guard([&] {
     if (!g) invalid("null graph");
+    g->host_mirror();
     if (offsets) std::copy(g->offsets.begin(), g->offsets.end(), offsets);
     if (adjacency) std::copy(g->adjacency.begin(), g->adjacency.end(), adjacency);
   });

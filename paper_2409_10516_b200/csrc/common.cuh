@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -161,9 +162,14 @@ struct ra_graph {
   // with kSentinel past degree(u): one coalesced load per expansion, no
   // offsets hop.
   ra::DevBuf<uint32_t> adj;
-  // host mirror (reference CSR) for accessors and OODG serialization
-  std::vector<uint64_t> offsets;
-  std::vector<uint32_t> adjacency;
+  uint64_t n_edges = 0;
+  // host mirror (reference CSR) for accessors and OODG serialization: set by
+  // deserialize; a GPU build leaves it empty and host_mirror() downloads the
+  // device rows on first use (the build never waits for it)
+  mutable std::vector<uint64_t> offsets;
+  mutable std::vector<uint32_t> adjacency;
+  mutable std::once_flag host_once;
+  void host_mirror() const;
 };
 
 namespace ra {

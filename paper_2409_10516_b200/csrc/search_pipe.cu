@@ -44,6 +44,7 @@
 #include "tma.cuh"
 
 #ifdef RA_PIPE_PROFILE
+constexpr bool kPipeProfile = true;
 #define PIPE_TICK(slot)                \
   {                                    \
     const uint64_t t_ = clock64();     \
@@ -51,6 +52,7 @@
     tq = t_;                           \
   }
 #else
+constexpr bool kPipeProfile = false;
 #define PIPE_TICK(slot)
 #endif
 
@@ -171,19 +173,43 @@ __device__ __forceinline__ void warp_sort256(uint64_t (&k)[8], uint32_t (&id)[8]
 }
 
 // in-order f64 dot of q (f64, smem) and a key row staged in shared memory
-// (dot_f64, index_oodgraph.cpp:40-44; f32 x f32 products are exact in f64)
+// (dot_f64, index_oodgraph.cpp:40-44; f32 x f32 products are exact in f64).
+// The chain of D dependent DFMAs is the floor; the operands of chunk c + 1
+// (4 LDS.128 of q, 2 of the row) are requested during chunk c's 8 DFMAs so
+// no DFMA waits on a shared-memory load.
 template <int D>
 __device__ __forceinline__ double row_dot(const double* __restrict__ qd,
                                           const float* __restrict__ row) {
-  double acc = 0.0;
+  static_assert(D % 8 == 0, "row_dot takes d in multiples of 8");
+  const double2* q2 = reinterpret_cast<const double2*>(qd);
   const float4* r4 = reinterpret_cast<const float4*>(row);
-#pragma unroll 8
-  for (int c = 0; c < D / 4; ++c) {
-    const float4 k = r4[c];
-    acc = fma(qd[4 * c + 0], (double)k.x, acc);
-    acc = fma(qd[4 * c + 1], (double)k.y, acc);
-    acc = fma(qd[4 * c + 2], (double)k.z, acc);
-    acc = fma(qd[4 * c + 3], (double)k.w, acc);
+  constexpr int NC = D / 8;
+  double2 qa[4], qb[4];
+  float4 ra[2], rb[2];
+  auto load = [&](int c, double2 (&q)[4], float4 (&r)[2]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) q[j] = q2[4 * c + j];
+    r[0] = r4[2 * c];
+    r[1] = r4[2 * c + 1];
+  };
+  double acc = 0.0;
+  auto fma8 = [&](const double2 (&q)[4], const float4 (&r)[2]) {
+    acc = fma(q[0].x, (double)r[0].x, acc);
+    acc = fma(q[0].y, (double)r[0].y, acc);
+    acc = fma(q[1].x, (double)r[0].z, acc);
+    acc = fma(q[1].y, (double)r[0].w, acc);
+    acc = fma(q[2].x, (double)r[1].x, acc);
+    acc = fma(q[2].y, (double)r[1].y, acc);
+    acc = fma(q[3].x, (double)r[1].z, acc);
+    acc = fma(q[3].y, (double)r[1].w, acc);
+  };
+  load(0, qa, ra);
+#pragma unroll
+  for (int c = 0; c < NC; c += 2) {
+    if (c + 1 < NC) load(c + 1, qb, rb);
+    fma8(qa, ra);
+    if (c + 2 < NC) load(c + 2, qa, ra);
+    if (c + 1 < NC) fma8(qb, rb);
   }
   return acc;
 }
@@ -241,6 +267,7 @@ __device__ __forceinline__ void warp_best(uint64_t& k, uint32_t& id) {
 
 struct PipeLayout {
   uint32_t D, MT, vis_words, vis_smem, capO;
+  uint32_t duo = 0;  // TP "duo" variant: a commit warp + an expansion warp per query
   static constexpr size_t kBars = 0, kCtrl = (size_t(kPW) * 8 + 63) / 64 * 64,  // one mbarrier per warp
                           kPubK = kCtrl + 64, kPubId = kPubK + 256, kSlotW = kPubId + 128,
                           kCnt = kSlotW + size_t(kSlots) * 8, kMb = kCnt + size_t(kSlots) * 4,
@@ -271,9 +298,13 @@ struct PipeLayout {
   __host__ __device__ size_t tp_vis_off() const {
     return tp_tile_off() + (vis_smem ? tile_bytes() : 0);
   }
-  __host__ __device__ size_t tp_warp_bytes() const {
+  __host__ __device__ size_t tp_duo_off() const {
     return tp_vis_off() + (vis_smem ? ((size_t(vis_words) * 4 + 15) & ~size_t(15)) : 0);
   }
+  // duo mailbox: request u64 (seq << 32 | node), ready u32, thr u64, then the
+  // packet: key u64[32], id u32[32], flag words (new / masked ballots)
+  static constexpr size_t kDuoBytes = 32 + 32 * 12 + 16;
+  __host__ __device__ size_t tp_warp_bytes() const { return tp_duo_off() + (duo ? kDuoBytes : 0); }
 };
 
 struct Arr {  // (key, id) array: k u64[cap] then id u32[cap]
@@ -313,6 +344,7 @@ __device__ void fused_attention_tail(const SearchArgs& a, const PipeLayout& lay,
   const size_t avail = size_t(kPW) * lay.tile_bytes() - a_bytes - head;
   // rows per pass (>= 8, see fin_smem); even, so Vt stays 16-B aligned
   const uint32_t R = uint32_t(avail / (size_t(D) * 4 + 8)) & ~1u;
+  if (R == 0) __trap();  // unreachable: launch_pipe_d sizes the tiles for >= 8 rows
   float* Vt = reinterpret_cast<float*>(e + R);  // [R][D]
   const float* V = fa.values[b];
   const double* ch = fa.chunk + size_t(b) * fa.nchunk * (D + 2);
@@ -401,12 +433,28 @@ __device__ void fused_attention_tail(const SearchArgs& a, const PipeLayout& lay,
   fa.out[size_t(b) * D + j] = we ? oo : (oe ? ow : gw * ow + go * oo);
 }
 
-template <int D, bool VS, bool TP, bool BF>
-__global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP_MINB) : 1)
+// the two warps of a DUO query (named barrier 1 + pair)
+__device__ __forceinline__ void pair_sync(uint32_t pair) {
+  asm volatile("bar.sync %0, 64;" ::"r"(pair + 1u) : "memory");
+}
+
+// DUO: pairs of warps per query in throughput mode (<= kDuoPairs per CTA:
+// 14 warps at <= 144 registers fill the register file)
+constexpr uint32_t kDuoPairs = 7;
+
+template <int D, bool VS, bool TP, bool BF, bool DUO = false>
+__global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW * 32,
+                                  TP ? (VS ? 1 : RA_TP_MINB) : 1)
     k_graph_search_pipe(SearchArgs a, PipeLayout lay, uint32_t spill_cap) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t b = TP ? blockIdx.x * (blockDim.x >> 5) + warp : blockIdx.x;
+  // DUO: with P queries per CTA, warp j < P commits query j and warp P + j
+  // expands for it, so the expansion warps (the DFMA / F2F work) spread over
+  // all four SMSPs (warp % 4) instead of the odd two
+  const uint32_t duo_p = blockDim.x >> 6;
+  const bool duo_x = DUO && warp >= duo_p;  // this warp is an expansion warp
+  const uint32_t qslot = DUO ? (duo_x ? warp - duo_p : warp) : warp;
+  const uint32_t b = TP ? blockIdx.x * (blockDim.x >> (DUO ? 6 : 5)) + qslot : blockIdx.x;
   if (TP && b >= a.B) return;  // warp-uniform; TP never uses CTA barriers
   const GraphDesc g = a.desc[b];
   const uint32_t M = g.M, ef = g.ef, k = a.k, n = g.n;
@@ -439,7 +487,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
   volatile uint64_t* pk_nk = reinterpret_cast<volatile uint64_t*>(smem + PipeLayout::kNk);
   uint32_t* pk_id = reinterpret_cast<uint32_t*>(smem + PipeLayout::kPkId);
   uint64_t* pk_k = reinterpret_cast<uint64_t*>(smem + PipeLayout::kPkK);
-  uint8_t* const wbase = smem + lay.tp_base() + warp * lay.tp_warp_bytes();  // TP: this query's
+  uint8_t* const wbase = smem + lay.tp_base() + qslot * lay.tp_warp_bytes();  // TP: this query's
   double* qd = TP ? reinterpret_cast<double*>(wbase)
                   : reinterpret_cast<double*>(smem + PipeLayout::kQd);
   float* tile = reinterpret_cast<float*>(TP ? wbase + lay.tp_tile_off()
@@ -450,12 +498,33 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
                      : a.vis_global + size_t(b) * 2 * vw;
   uint32_t* expd = vis + vw;
   uint8_t* spill_slot = a.spill + size_t(b) * 2 * PipeLayout::arr_bytes(spill_cap);
+  // DUO mailbox (PipeLayout::kDuoBytes): the commit warp posts the next top
+  // (seq << 32 | node; node = kSentinel stops the expansion warp), which
+  // returns that node's packet (per-lane key / id, new / masked ballots)
+  uint8_t* const duo = wbase + lay.tp_duo_off();
+  volatile unsigned long long* duo_req = reinterpret_cast<volatile unsigned long long*>(duo);
+  volatile uint32_t* duo_rdy = reinterpret_cast<volatile uint32_t*>(duo + 8);
+  volatile uint32_t* duo_flags = reinterpret_cast<volatile uint32_t*>(duo + 12);  // [2]
+  volatile uint64_t* duo_thr = reinterpret_cast<volatile uint64_t*>(duo + 24);
+  volatile uint64_t* duo_pk = reinterpret_cast<volatile uint64_t*>(duo + 32);
+  volatile uint32_t* duo_pi = reinterpret_cast<volatile uint32_t*>(duo + 32 + 32 * 8);
 
   if constexpr (TP) {
-    if (VS && lane == 0) mbar_init(bar);
-    for (uint32_t w = lane; w < vw; w += 32) vis[w] = 0;
-    for (uint32_t i = lane; i < D; i += 32) qd[i] = (double)a.q[size_t(b) * D + i];
-    __syncwarp();
+    if constexpr (DUO) {
+      if (!duo_x) {
+        for (uint32_t w = lane; w < vw; w += 32) vis[w] = 0;
+        for (uint32_t i = lane; i < D; i += 32) qd[i] = (double)a.q[size_t(b) * D + i];
+      } else if (lane == 0) {
+        mbar_init(bar);
+        *duo_req = 0, *duo_rdy = 0, *duo_thr = 0;
+      }
+      pair_sync(qslot);
+    } else {
+      if (VS && lane == 0) mbar_init(bar);
+      for (uint32_t w = lane; w < vw; w += 32) vis[w] = 0;
+      for (uint32_t i = lane; i < D; i += 32) qd[i] = (double)a.q[size_t(b) * D + i];
+      __syncwarp();
+    }
   } else {
     if (lane == 0) mbar_init(bar);
     // the query element is requested first (it may live in page-locked host
@@ -481,21 +550,19 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
     return (reinterpret_cast<const volatile uint32_t*>(bits)[v >> 5] >> (v & 31)) & 1u;
   };
   uint32_t phase = 0;
-  uint64_t cy_adj = 0, cy_tma = 0;  // RA_PIPE_PROFILE: adjacency-load and TMA-wait cycles
+  uint64_t cy_adj = 0, cy_tma = 0, cy_dot = 0;  // adjacency-load / TMA-wait / dot cycles
   // Expansion of node c by this warp: lane l holds adjacency slot l; `isnew`
   // lanes hold an unvisited (at read time), first-occurrence neighbour v and
   // its exact score key. Key rows come through this warp's TMA tile.
   // The mask bit is fetched here too, so its load overlaps the row loads.
+  // (adjacency / TMA wait cycles: RA_PIPE_PROFILE builds and the DUO expansion warp)
+  constexpr bool kExpCy = kPipeProfile || DUO;
   auto expand = [&](uint32_t c, uint32_t& v, uint64_t& sk, bool& isnew, bool& msk) {
-#ifdef RA_PIPE_PROFILE
-    const uint64_t te0 = clock64();
-#endif
+    const uint64_t te0 = kExpCy ? clock64() : 0;
     v = lane < M ? __ldg(adj + size_t(c) * M + lane) : kSentinel;
     const bool valid = v != kSentinel;
     const uint32_t grp = __match_any_sync(kFull, v);
-#ifdef RA_PIPE_PROFILE
-    cy_adj += clock64() - te0;
-#endif
+    if (kExpCy) cy_adj += clock64() - te0;
     const bool first = uint32_t(__ffs(grp) - 1) == lane;
     isnew = valid && first && !vbit(vis, v);
     msk = isnew && masked_id(v);
@@ -542,24 +609,22 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
           if constexpr (BF) bulk_g2s(row, keys16 + size_t(v) * D, kRowBytes, bar);
           else bulk_g2s(row, keys + size_t(v) * D, kRowBytes, bar);
         }
-#ifdef RA_PIPE_PROFILE
-        const uint64_t tw0 = clock64();
-#endif
+        const uint64_t tw0 = kExpCy ? clock64() : 0;
         mbar_wait(bar, phase);
-#ifdef RA_PIPE_PROFILE
-        cy_tma += clock64() - tw0;
-#endif
+        if (kExpCy) cy_tma += clock64() - tw0;
         phase ^= 1u;
+        const uint64_t td0 = kExpCy ? clock64() : 0;
         if (mine) {
           if constexpr (BF) sk = okey(row_dot_bf<D>(qd, reinterpret_cast<const uint4*>(row), false));
           else sk = okey(row_dot<D>(qd, row));
         }
         __syncwarp();
+        if (kExpCy) cy_dot += clock64() - td0;
       }
     }
   };
 
-  if (TP || warp == 0) {
+  if (TP ? !duo_x : warp == 0) {
     // =================== commit warp ===================
     // F: per-lane unsorted lists in shared memory (column layout, entry i of
     // lane l at [i * 32 + l]; empty = (0, kSentinel)); the lane head (its
@@ -727,6 +792,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
       }
       if (lo <= thr) return;
       thr = lo;
+      if (DUO && lane == 0) *duo_thr = thr;  // the expansion warp's prefetch cut
 #pragma unroll
       for (int i = 0; i < kUR; ++i)
         if (uid[i] != kSentinel && uk[i] < thr) uk[i] = 0, uid[i] = kSentinel, ufree |= 1u << i;
@@ -856,6 +922,8 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
       cv = entry;
       cm = masked_id(entry);
     }
+    uint32_t dseq = 1;  // DUO: the entry is the first top
+    if (DUO && lane == 0) *duo_req = (1ull << 32) | g.entry;
 
     uint64_t cy[5] = {0, 0, 0, 0, 0};
     uint64_t tq = clock64();
@@ -931,10 +999,40 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
       PIPE_TICK(1)
       if constexpr (TP) {
         ++c_miss;
-        expand(tid, cv, cx, cand, cm);
+        if constexpr (DUO) {
+          // tid's packet (requested when tid was found to be the next top)
+          if (*duo_rdy != dseq) {
+            const uint64_t tw0 = clock64();
+            while (*duo_rdy != dseq) {
+            }
+            c_wait += clock64() - tw0;
+          }
+          __threadfence_block();
+          const uint32_t nm = duo_flags[0], mm = duo_flags[1];
+          cv = duo_pi[lane];
+          cx = duo_pk[lane];
+          // exact filter now (only this warp writes the visited bits), so
+          // visit() need not re-check
+          cand = ((nm >> lane) & 1u) && !((vis[cv >> 5] >> (cv & 31)) & 1u);
+          cm = (mm >> lane) & 1u;
+          // the next top is known before the visit: the best new child >= thr
+          // vs the frontier's best (compaction can only end the search), so
+          // the expansion warp starts on it while this warp does the visit
+          const bool inf = cand && cx >= thr;
+          uint64_t ck = inf ? cx : 0, fk = hk;
+          uint32_t ci = inf ? cv : kSentinel, fi = hi;
+          warp_best(ck, ci);
+          warp_best(fk, fi);
+          if (nFO && better(fo_k, fo_id, fk, fi)) fk = fo_k, fi = fo_id;
+          if (better(ck, ci, fk, fi)) fi = ci, ++c_fopop;  // (dbg: the next top is a child)
+          ++dseq;
+          if (lane == 0) *duo_req = (uint64_t(dseq) << 32) | fi;
+        } else {
+          expand(tid, cv, cx, cand, cm);
+        }
         pre = true;
         PIPE_TICK(2)
-        if constexpr (VS) {  // the new frontier nodes' adjacency rows go to L2 now
+        if constexpr (VS && !DUO) {  // the new frontier nodes' adjacency rows go to L2 now
           if ((M * 4) % 16 == 0 && !(a.flags & 2u) && cand && cx >= thr)
             bulk_prefetch_l2(adj + size_t(cv) * M, M * 4);
         }
@@ -999,6 +1097,12 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
         }
       }
     }
+    if constexpr (DUO) {  // stop the expansion warp; its tile is free after the barrier
+      if (lane == 0) *duo_req = (uint64_t(dseq + 1) << 32) | kSentinel;
+      pair_sync(qslot);
+      c_hit = duo_pk[0];  // its busy / adjacency / TMA-wait cycles (dbg)
+      c_fsp = duo_pk[1], c_usp = duo_pk[2], cy_dot = duo_pk[3];
+    }
     // ---- result (:402-410): the pool's top min(k, |pool|), best-first ----
     uint32_t p2 = 32;
     while (p2 < nU) p2 <<= 1;
@@ -1049,6 +1153,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
 #ifndef RA_PIPE_PROFILE
       if (TP) {  // overflow anatomy: FO / UO spill rounds, FO pops, moved to HBM
         d[7] = c_fsp, d[8] = c_fopop, d[9] = (fo_g ? 1u : 0u) | (uo_g ? 2u : 0u), d[10] = c_usp;
+        if (DUO) d[9] = cy_dot;
         d[5] = pk_fo, d[11] = pk_uo;  // peak overflow sizes
       }
 #else
@@ -1135,6 +1240,44 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
       if (lane == 0) ctrl[7] = pool;
       __syncthreads();
     }
+  } else if constexpr (DUO) {
+    // =================== DUO expansion warp ===================
+    // expands exactly the nodes the commit warp posts (each is the next top
+    // or the search is over), so its expansion overlaps the commit warp's
+    // visit of the previous packet; filtering against the visited bits here
+    // is a hint (the commit warp re-filters)
+    uint64_t busy = 0;
+    for (uint32_t hseq = 1;; ++hseq) {
+      uint64_t w;
+      do {
+        w = *duo_req;
+      } while (uint32_t(w >> 32) != hseq);
+      const uint32_t p = uint32_t(w);
+      if (p == kSentinel) break;
+      const uint64_t tb0 = clock64();
+      uint32_t v;
+      uint64_t sk;
+      bool isnew, msk;
+      expand(p, v, sk, isnew, msk);
+      duo_pk[lane] = sk;
+      duo_pi[lane] = v;
+      const uint32_t nm = __ballot_sync(kFull, isnew), mm = __ballot_sync(kFull, msk);
+      if (lane == 0) duo_flags[0] = nm, duo_flags[1] = mm;
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        *duo_rdy = hseq;
+      }
+      busy += clock64() - tb0;
+      // the new frontier nodes' adjacency rows go to L2 now
+      if constexpr (VS) {
+        if ((M * 4) % 16 == 0 && !(a.flags & 2u) && isnew && sk >= *duo_thr)
+          bulk_prefetch_l2(adj + size_t(v) * M, M * 4);
+      }
+    }
+    if (lane == 0) duo_pk[0] = busy, duo_pk[1] = cy_adj, duo_pk[2] = cy_tma, duo_pk[3] = cy_dot;
+    pair_sync(qslot);
+    return;
   } else if constexpr (!TP) {
     // =================== helper warps ===================
     uint32_t n_exp = 0, n_chain = 0, n_evict = 0;
@@ -1179,7 +1322,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
     // (sum e*v, max, sum e) in the head's scratch row, in W order
     const bool fused = !BF && a.fa.out != nullptr;
     auto wchunk = [&](uint32_t c) {
-      const uint32_t r0 = c * lay.MT, rows = min(lay.MT, a.fa.nW - r0);
+      const uint32_t r0 = c * a.fa.crows, rows = min(a.fa.crows, a.fa.nW - r0);
       const float* V = a.fa.values[b];
       const uint32_t wid = lane < rows ? a.fa.W[r0 + lane] : 0u;
       fence_proxy_async();
@@ -1432,7 +1575,7 @@ __global__ void __launch_bounds__(TP ? kTW * 32 : kPW * 32, TP ? (VS ? 1 : RA_TP
 
 template <int D, bool BF>
 bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* scratch,
-                   bool tp, int tps) {
+                   bool tp, int tps, int duo) {
   const size_t budget = ctx->smem_optin ? ctx->smem_optin : 227 * 1024;
   uint32_t spill_cap = 32;
   while (spill_cap < max_n) spill_cap <<= 1;
@@ -1473,6 +1616,38 @@ bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* sc
 #ifndef RA_TPS_CAPO
 #define RA_TPS_CAPO 128
 #endif
+    // DUO: TPS with a second warp per query that expands the next top while
+    // the commit warp visits the previous packet; taken while the batch fits
+    // one wave at <= kDuoPairs queries per SM (duo: 0 auto, 1 forced, -1 off)
+    if (duo >= 0) {
+      PipeLayout ls{uint32_t(D), std::min<uint32_t>(std::max<uint32_t>(a.max_M, 1), RA_TPS_ROWS),
+                    (max_n + 31) / 32, 1, 64};
+      ls.duo = 1;
+      const uint32_t fit = uint32_t(std::min<size_t>((budget - ls.tp_base()) / ls.tp_warp_bytes(),
+                                                     kDuoPairs));
+      const uint32_t sms = uint32_t(ctx->num_sms);
+      const uint32_t want = (a.B + sms - 1) / sms;
+      if (fit >= 1 && (duo == 1 || want <= fit)) {
+        const uint32_t wpc = std::max<uint32_t>(1, std::min(fit, want));
+        {
+          PipeLayout l0 = ls;
+          l0.capO = 0;
+          const size_t per = (budget - ls.tp_base()) / wpc - l0.tp_warp_bytes();
+          ls.capO = uint32_t(std::min<size_t>(per / 24 - 2, 4096)) & ~31u;
+        }
+        const size_t bytes = ls.tp_base() + wpc * ls.tp_warp_bytes();
+        auto kern = k_graph_search_pipe<D, true, true, BF, true>;
+        static int set_bytes[64] = {};
+        if (int(bytes) > set_bytes[ctx->device & 63]) {
+          RA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(bytes)));
+          set_bytes[ctx->device & 63] = int(bytes);
+        }
+        kern<<<(a.B + wpc - 1) / wpc, wpc * 64, bytes, ctx->stream>>>(s, ls, spill_cap);
+        RA_LAUNCH_CHECK();
+        return true;
+      }
+    }
     if (tps >= 0) {
       // the overflow arrays FO / UO get what the warps leave of the budget
       // (a search that outgrows them moves them to its HBM slot: exact, slow)
@@ -1517,6 +1692,13 @@ bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* sc
   }
   if (BF) s.fa.out = nullptr;  // fused attention reads f32 rows only
   PipeLayout lay{uint32_t(D), std::max<uint32_t>(a.max_M, 1), (max_n + 31) / 32, 1, 0};
+  if (s.fa.out) {
+    // the fused tail stages the W chunk partials and >= 8 V rows in the
+    // helpers' tiles (fused_attention_tail): small-degree graphs get taller
+    // tiles so that area always holds them
+    const size_t need = (40 + 32 * (size_t(D) + 2)) * 8 + 8 * (size_t(D) * 4 + 8) + 16;
+    while (size_t(kPW) * lay.tile_bytes() < need) ++lay.MT;
+  }
   if (lay.bytes() + PipeLayout::arr_bytes(512) * 2 > budget) lay.vis_smem = 0;
   const size_t fixed = lay.bytes();
   if (fixed + PipeLayout::arr_bytes(256) * 2 > budget) return false;
@@ -1561,25 +1743,26 @@ size_t search_pipe_scratch_bytes(uint32_t B, uint32_t max_n) {
 bool launch_graph_search_pipe(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n,
                               uint8_t* scratch, int mode) {
   if (a.max_M > 32 || a.max_M == 0) return false;
-  // mode 0 auto, 1 throughput (TPS when it fits one wave), 2 latency,
-  // 3 throughput with register rows only, 4 TPS forced
-  const bool tp = mode == 1 || mode == 3 || mode == 4 ||
+  // mode 0 auto, 1 throughput (DUO, else TPS, when it fits one wave), 2
+  // latency, 3 throughput with register rows only, 4 TPS forced, 5 DUO forced
+  const bool tp = mode == 1 || mode == 3 || mode == 4 || mode == 5 ||
                   (mode == 0 && a.B > 2u * uint32_t(ctx->num_sms));
   const int tps = mode == 3 ? -1 : mode == 4 ? 1 : 0;
+  const int duo = mode == 3 || mode == 4 ? -1 : mode == 5 ? 1 : 0;
   if (a.bf16) {  // bf16 rows: d in {32, 64, 128} (16-B multiples)
     switch (a.d) {
-      case 128: return launch_pipe_d<128, true>(ctx, a, max_n, scratch, tp, tps);
-      case 64: return launch_pipe_d<64, true>(ctx, a, max_n, scratch, tp, tps);
-      case 32: return launch_pipe_d<32, true>(ctx, a, max_n, scratch, tp, tps);
+      case 128: return launch_pipe_d<128, true>(ctx, a, max_n, scratch, tp, tps, duo);
+      case 64: return launch_pipe_d<64, true>(ctx, a, max_n, scratch, tp, tps, duo);
+      case 32: return launch_pipe_d<32, true>(ctx, a, max_n, scratch, tp, tps, duo);
       default: return false;
     }
   }
   switch (a.d) {
-    case 128: return launch_pipe_d<128, false>(ctx, a, max_n, scratch, tp, tps);
-    case 64: return launch_pipe_d<64, false>(ctx, a, max_n, scratch, tp, tps);
-    case 32: return launch_pipe_d<32, false>(ctx, a, max_n, scratch, tp, tps);
-    case 16: return launch_pipe_d<16, false>(ctx, a, max_n, scratch, tp, tps);
-    case 8: return launch_pipe_d<8, false>(ctx, a, max_n, scratch, tp, tps);
+    case 128: return launch_pipe_d<128, false>(ctx, a, max_n, scratch, tp, tps, duo);
+    case 64: return launch_pipe_d<64, false>(ctx, a, max_n, scratch, tp, tps, duo);
+    case 32: return launch_pipe_d<32, false>(ctx, a, max_n, scratch, tp, tps, duo);
+    case 16: return launch_pipe_d<16, false>(ctx, a, max_n, scratch, tp, tps, duo);
+    case 8: return launch_pipe_d<8, false>(ctx, a, max_n, scratch, tp, tps, duo);
     default: return false;
   }
 }

@@ -77,6 +77,10 @@ def main():
              "peak_UO_p99": float(np.percentile(c[:, 11], 99)), "peak_UO_max": float(c[:, 11].max()),
              "compactions_mean": float(c[:, 6].mean()),
              "misses_mean": float(c[:, 0].mean()),
+             # duo: the commit warp's packet waits / the expansion warp's busy cycles
+             "wait_cycles_mean": float(c[:, 1].mean()),
+             "dbg_slot_means": [float(c[:, j].mean()) for j in range(12)],
+             "hit_or_helper_busy_cycles_mean": float(c[:, 4].mean()),
              # RA_PIPE_PROFILE builds: per-phase cycles (top/stop, pop, expand, visit)
              "profile_cycles_mean": [float(c[:, j].mean()) for j in (7, 8, 9, 10)],
              "profile_adj_tma_cycles_mean": [float(c[:, 5].mean()), float(c[:, 11].mean())]}
