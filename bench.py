@@ -430,6 +430,13 @@ def main():
             k: round(statistics.mean(g.build_stats.ms[k] for g in graphs), 2)
             for k in ("knn", "knn_tensor", "edges", "prune", "entry", "repair")},
         "build_knn_rows_exact_fallback": sum(g.build_stats.knn_rows_widened for g in graphs),
+        # configs[3] (index construction): the layer's graphs built back to back
+        # on this GPU (128K prefill queries -> 128K keys per query head)
+        "build_layer": {"heads": len(build_ms), "ms_total": round(sum(build_ms), 1),
+                        "ms_per_head_median": round(statistics.median(build_ms), 1),
+                        "knn_tflops_algorithmic": round(
+                            2.0 * a.n_ctx * a.n_ctx * 128 / (statistics.median(
+                                [g.build_stats.ms["knn_tensor"] for g in graphs]) * 1e-3) / 1e12, 1)},
     }
     if layer_tokens > 1:
         res["layer_tokens_per_s"] = round(layer_tokens / (ms * 1e-3), 1)

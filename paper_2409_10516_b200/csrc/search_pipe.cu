@@ -214,6 +214,24 @@ __device__ __forceinline__ double row_dot(const double* __restrict__ qd,
   return acc;
 }
 
+// the plain loop form of the same chain (the compiler interleaves the
+// operand loads with the DFMAs)
+template <int D>
+__device__ __forceinline__ double row_dot_seq(const double* __restrict__ qd,
+                                              const float* __restrict__ row) {
+  double acc = 0.0;
+  const float4* r4 = reinterpret_cast<const float4*>(row);
+#pragma unroll 8
+  for (int c = 0; c < D / 4; ++c) {
+    const float4 k = r4[c];
+    acc = fma(qd[4 * c + 0], (double)k.x, acc);
+    acc = fma(qd[4 * c + 1], (double)k.y, acc);
+    acc = fma(qd[4 * c + 2], (double)k.z, acc);
+    acc = fma(qd[4 * c + 3], (double)k.w, acc);
+  }
+  return acc;
+}
+
 __device__ __forceinline__ double bf_lo(uint32_t w) { return (double)__uint_as_float(w << 16); }
 __device__ __forceinline__ double bf_hi(uint32_t w) { return (double)__uint_as_float(w & 0xFFFF0000u); }
 
@@ -301,9 +319,10 @@ struct PipeLayout {
   __host__ __device__ size_t tp_duo_off() const {
     return tp_vis_off() + (vis_smem ? ((size_t(vis_words) * 4 + 15) & ~size_t(15)) : 0);
   }
-  // duo mailbox: request u64 (seq << 32 | node), ready u32, thr u64, then the
-  // packet: key u64[32], id u32[32], flag words (new / masked ballots)
-  static constexpr size_t kDuoBytes = 32 + 32 * 12 + 16;
+  // duo mailbox: request u64 (seq << 32 | node), ready u32, packet flags
+  // u32[2], thr u64, packet key u64[32] / id u32[32], request ids u32[32] +
+  // request flags u32[2] (see k_graph_search_pipe)
+  static constexpr size_t kDuoBytes = 32 + 32 * 12 + 32 * 4 + 16;
   __host__ __device__ size_t tp_warp_bytes() const { return tp_duo_off() + (duo ? kDuoBytes : 0); }
 };
 
@@ -508,6 +527,8 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
   volatile uint64_t* duo_thr = reinterpret_cast<volatile uint64_t*>(duo + 24);
   volatile uint64_t* duo_pk = reinterpret_cast<volatile uint64_t*>(duo + 32);
   volatile uint32_t* duo_pi = reinterpret_cast<volatile uint32_t*>(duo + 32 + 32 * 8);
+  volatile uint32_t* duo_rv = reinterpret_cast<volatile uint32_t*>(duo + 32 + 32 * 12);  // [32]
+  volatile uint32_t* duo_rf = reinterpret_cast<volatile uint32_t*>(duo + 32 + 32 * 16);  // [2]
 
   if constexpr (TP) {
     if constexpr (DUO) {
@@ -598,6 +619,31 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
       // rows through this warp's tile, lay.MT at a time (one round unless
       // the tile is shorter than the degree: TPS)
       const uint32_t o = __popc(newmask & lanemask_lt(lane)), nn = __popc(newmask);
+      if (TP && !BF && nn > lay.MT) {
+        // more new rows than tile slots: the tile's rows by TMA and the rest
+        // L1-prefetched, all in flight at once, then ONE dot chain for every
+        // lane through a generic pointer (tile or global row)
+        const bool intile = o < lay.MT;
+        float* row = tile + size_t(intile ? o : 0) * RS;
+        fence_proxy_async();
+        if (lane == 0) mbar_arrive_expect_tx(bar, lay.MT * kRowBytes);
+        __syncwarp();
+        const float* grow = keys + size_t(v) * D;
+        if (isnew && intile) bulk_g2s(row, grow, kRowBytes, bar);
+        if (isnew && !intile) {
+#pragma unroll
+          for (int l = 0; l < D * 4 / 128; ++l) prefetch_l1(reinterpret_cast<const char*>(grow) + 128 * l);
+        }
+        const uint64_t tw0 = kExpCy ? clock64() : 0;
+        mbar_wait(bar, phase);
+        if (kExpCy) cy_tma += clock64() - tw0;
+        phase ^= 1u;
+        const uint64_t td0 = kExpCy ? clock64() : 0;
+        if (isnew) sk = okey(row_dot<D>(qd, intile ? static_cast<const float*>(row) : grow));
+        __syncwarp();
+        if (kExpCy) cy_dot += clock64() - td0;
+        return;
+      }
       for (uint32_t c0 = 0; c0 < nn; c0 += lay.MT) {
         const uint32_t cnt = nn - c0 < lay.MT ? nn - c0 : lay.MT;
         const bool mine = isnew && o >= c0 && o < c0 + cnt;
@@ -616,7 +662,7 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
         const uint64_t td0 = kExpCy ? clock64() : 0;
         if (mine) {
           if constexpr (BF) sk = okey(row_dot_bf<D>(qd, reinterpret_cast<const uint4*>(row), false));
-          else sk = okey(row_dot<D>(qd, row));
+          else sk = okey((!TP && (a.flags & 4u)) ? row_dot_seq<D>(qd, row) : row_dot<D>(qd, row));
         }
         __syncwarp();
         if (kExpCy) cy_dot += clock64() - td0;
@@ -792,7 +838,6 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
       }
       if (lo <= thr) return;
       thr = lo;
-      if (DUO && lane == 0) *duo_thr = thr;  // the expansion warp's prefetch cut
 #pragma unroll
       for (int i = 0; i < kUR; ++i)
         if (uid[i] != kSentinel && uk[i] < thr) uk[i] = 0, uid[i] = kSentinel, ufree |= 1u << i;
@@ -922,8 +967,89 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
       cv = entry;
       cm = masked_id(entry);
     }
-    uint32_t dseq = 1;  // DUO: the entry is the first top
-    if (DUO && lane == 0) *duo_req = (1ull << 32) | g.entry;
+    // DUO: this warp starts each expansion - the node's adjacency row and
+    // the new-neighbour filter (against its visited bits as they are: the
+    // neighbours it is about to visit are dropped again at commit time),
+    // then per-lane L2 prefetches of the new key rows and of their own
+    // adjacency rows (vector prefetches: the bulk forms issue lane by lane)
+    // - and posts it; the expansion warp runs the dot chains on those rows
+    // and returns the packet while this warp visits the previous one.
+    uint32_t dseq = 0;
+    auto duo_issue = [&](uint32_t p) {
+      ++dseq;
+      if (p != kSentinel) {
+        const uint64_t ti0 = clock64();
+        const uint32_t v = lane < M ? __ldg(adj + size_t(p) * M + lane) : kSentinel;
+        const uint32_t grp = __match_any_sync(kFull, v);
+        c_usp += clock64() - ti0;  // (dbg: the adjacency-row wait)
+        const bool isnew = v != kSentinel && uint32_t(__ffs(grp) - 1) == lane &&
+                           !((vis[v >> 5] >> (v & 31)) & 1u);
+        if (isnew) {
+          const char* r = reinterpret_cast<const char*>(keys + size_t(v) * D);
+#pragma unroll
+          for (int l = 0; l < D * 4 / 128; ++l) prefetch_l2(r + 128 * l);
+        }
+        const uint32_t nm = __ballot_sync(kFull, isnew);
+        duo_rv[lane] = v;
+        if (lane == 0) duo_rf[0] = nm;
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();
+          *duo_req = (uint64_t(dseq) << 32) | p;
+        }
+        // (the best new neighbour is likely a top soon: its adjacency row,
+        // the first load of its issue, to L2 now)
+        if (isnew && !(a.flags & 2u)) {
+          const char* ar = reinterpret_cast<const char*>(adj + size_t(v) * M);
+          prefetch_l2(ar);
+          prefetch_l2(ar + M * 4 - 1);
+        }
+        c_fsp += clock64() - ti0;  // (dbg: the whole issue)
+      } else if (lane == 0) {
+        __threadfence_block();
+        *duo_req = (uint64_t(dseq) << 32) | p;
+      }
+    };
+    if constexpr (DUO) duo_issue(g.entry);  // the entry is the first top
+
+    // The next top is known before the visit: the best of this expansion's
+    // new children >= thr and the frontier after the pop (the visit only
+    // inserts those children; a compaction can only end the search). Found
+    // early (one argmax over per-lane bests and FO's best), it steers the
+    // work that would otherwise wait for the loop top: DUO posts it to the
+    // expansion warp, latency mode takes its packet now or hints it.
+    bool have_next = false, early_took = false;
+    uint64_t nk = 0, w_n = 0;
+    uint32_t nid = kSentinel, sl_n = 0;
+    auto next_top = [&](bool inf, uint64_t x, uint32_t v) {
+      uint64_t k0 = hk;
+      uint32_t i0 = hi;
+      if (inf && better(x, v, k0, i0)) k0 = x, i0 = v;
+      warp_best(k0, i0);
+      if (nFO && better(fo_k, fo_id, k0, i0)) k0 = fo_k, i0 = fo_id;
+      nk = k0, nid = i0, have_next = true;
+    };
+    // latency mode: take the next top's packet now if ready, else hint it
+    // when no helper holds it (its expansion overlaps the visit)
+    auto early_lookup = [&]() {
+      early_took = false;
+      if constexpr (!TP) {
+        if (nid == kSentinel) return;
+        sl_n = slot_of(nid);
+        w_n = *reinterpret_cast<volatile unsigned long long*>(slotw + sl_n);
+        const uint64_t w1 = *reinterpret_cast<volatile unsigned long long*>(slotw + sl_n + 1);
+        if (uint32_t(w_n) != nid && uint32_t(w1) == nid) w_n = w1, ++sl_n;
+        bool t = false;
+        if (lane == 0) {
+          if (uint32_t(w_n) == nid && uint32_t(w_n >> 32) == sREADY)
+            t = atomicCAS(slotw + sl_n, slotword(nid, sREADY), slotword(nid, sTAKEN)) ==
+                slotword(nid, sREADY);
+          else if (uint32_t(w_n) != nid && !(a.flags & 8u))
+            push_hint(nk, nid);
+        }
+        early_took = __shfl_sync(kFull, t, 0);
+      }
+    };
 
     uint64_t cy[5] = {0, 0, 0, 0, 0};
     uint64_t tq = clock64();
@@ -931,11 +1057,18 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
       visit(cand, cx, cv, cm, pre);
       PIPE_TICK(3)
       // frontier top (:387): lane heads vs the best overflow entry
-      uint64_t tk = hk;
-      uint32_t tid = hi;
-      warp_best(tk, tid);
-      const bool from_fo = nFO && better(fo_k, fo_id, tk, tid);
-      if (from_fo) tk = fo_k, tid = fo_id;
+      uint64_t tk;
+      uint32_t tid;
+      bool from_fo;
+      if (have_next) {  // (p sits in FO iff FO's best is p: ids are unique)
+        tk = nk, tid = nid, have_next = false;
+        from_fo = nFO && fo_id == tid;
+      } else {
+        tk = hk, tid = hi;
+        warp_best(tk, tid);
+        from_fo = nFO && better(fo_k, fo_id, tk, tid);
+        if (from_fo) tk = fo_k, tid = fo_id;
+      }
       if (tid == kSentinel) break;  // frontier exhausted
       if (u_total >= ef) {          // :390
         if (tk < thr) break;
@@ -949,7 +1082,9 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
       uint32_t sl = 0;
       uint64_t w = 0;
       bool took = false;
-      if constexpr (!TP) {
+      if (!TP && early_took) {
+        sl = sl_n, w = w_n, took = lane == 0, early_took = false;
+      } else if constexpr (!TP) {
         sl = slot_of(tid);
         w = *reinterpret_cast<volatile unsigned long long*>(slotw + sl);
         const uint64_t w1 = *reinterpret_cast<volatile unsigned long long*>(slotw + sl + 1);
@@ -1018,15 +1153,8 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
           // the next top is known before the visit: the best new child >= thr
           // vs the frontier's best (compaction can only end the search), so
           // the expansion warp starts on it while this warp does the visit
-          const bool inf = cand && cx >= thr;
-          uint64_t ck = inf ? cx : 0, fk = hk;
-          uint32_t ci = inf ? cv : kSentinel, fi = hi;
-          warp_best(ck, ci);
-          warp_best(fk, fi);
-          if (nFO && better(fo_k, fo_id, fk, fi)) fk = fo_k, fi = fo_id;
-          if (better(ck, ci, fk, fi)) fi = ci, ++c_fopop;  // (dbg: the next top is a child)
-          ++dseq;
-          if (lane == 0) *duo_req = (uint64_t(dseq) << 32) | fi;
+          next_top(cand && cx >= thr, cx, cv);
+          duo_issue(nid);
         } else {
           expand(tid, cv, cx, cand, cm);
         }
@@ -1067,10 +1195,17 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
         cv = cand ? pv : kSentinel;
         cx = cand ? px : 0;
         cm = cand && ((mb >> j) & 1u);
-        pre = false;  // other packets may have visited these since
         __syncwarp();
         if (lane == 0) st_release_cta(slotw + sl, slotword(kSentinel, sFREE));
         rot += cnt;
+        // other packets may have visited these since: the exact filter now
+        // (only this warp writes the visited bits), then the next top
+        cand = cand && !((vis[cv >> 5] >> (cv & 31)) & 1u);
+        pre = true;
+        if (a.flags & 262144u) {
+          next_top(cand && cx >= thr, cx, cv);
+          early_lookup();
+        }
       } else {
         ++c_miss;
 #ifdef RA_PIPE_MISSCLASS
@@ -1081,6 +1216,10 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
 #endif
         expand(tid, cv, cx, cand, cm);
         pre = true;
+        if (a.flags & 262144u) {
+          next_top(cand && cx >= thr, cx, cv);
+          early_lookup();
+        }
         if (!(a.flags & (8u | 32768u))) {
           // the likely next tops are this node's best children, which no
           // helper has seen: hint the best two so helpers start on them now
@@ -1100,8 +1239,8 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
     if constexpr (DUO) {  // stop the expansion warp; its tile is free after the barrier
       if (lane == 0) *duo_req = (uint64_t(dseq + 1) << 32) | kSentinel;
       pair_sync(qslot);
-      c_hit = duo_pk[0];  // its busy / adjacency / TMA-wait cycles (dbg)
-      c_fsp = duo_pk[1], c_usp = duo_pk[2], cy_dot = duo_pk[3];
+      c_hit = duo_pk[0];  // its busy / dot cycles (dbg); c_fsp / c_usp: this warp's issue / adjacency wait
+      cy_dot = duo_pk[3];
     }
     // ---- result (:402-410): the pool's top min(k, |pool|), best-first ----
     uint32_t p2 = 32;
@@ -1109,7 +1248,7 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
     bool fin_smem;
     uint8_t* fin_base = TP ? fo_base : smem + lay.tiles_off();
     if constexpr (TP) {
-      if (VS) {  // this warp's (dead) row tile
+      if (VS && !DUO) {  // this warp's (dead) row tile (DUO has none)
         fin_smem = PipeLayout::arr_bytes(p2) <= lay.tile_bytes();
         fin_base = wbase + lay.tp_tile_off();
       } else {
@@ -1255,13 +1394,17 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
       const uint32_t p = uint32_t(w);
       if (p == kSentinel) break;
       const uint64_t tb0 = clock64();
-      uint32_t v;
-      uint64_t sk;
-      bool isnew, msk;
-      expand(p, v, sk, isnew, msk);
+      __threadfence_block();
+      const uint32_t v = duo_rv[lane], nm = duo_rf[0];
+      const bool isnew = (nm >> lane) & 1u;
+      const uint32_t mm = __ballot_sync(kFull, isnew && masked_id(v));  // (W: not a pool entry)
+      const uint64_t td0 = clock64();
+      uint64_t sk = 0;
+      if (isnew) sk = okey(row_dot<D>(qd, keys + size_t(v) * D));  // (rows L2-prefetched)
+      __syncwarp();
+      cy_dot += clock64() - td0;
       duo_pk[lane] = sk;
       duo_pi[lane] = v;
-      const uint32_t nm = __ballot_sync(kFull, isnew), mm = __ballot_sync(kFull, msk);
       if (lane == 0) duo_flags[0] = nm, duo_flags[1] = mm;
       __syncwarp();
       if (lane == 0) {
@@ -1269,11 +1412,6 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
         *duo_rdy = hseq;
       }
       busy += clock64() - tb0;
-      // the new frontier nodes' adjacency rows go to L2 now
-      if constexpr (VS) {
-        if ((M * 4) % 16 == 0 && !(a.flags & 2u) && isnew && sk >= *duo_thr)
-          bulk_prefetch_l2(adj + size_t(v) * M, M * 4);
-      }
     }
     if (lane == 0) duo_pk[0] = busy, duo_pk[1] = cy_adj, duo_pk[2] = cy_tma, duo_pk[3] = cy_dot;
     pair_sync(qslot);
@@ -1588,7 +1726,8 @@ bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* sc
   //   bit 13     throughput mode: no L1 prefetch of key rows
   //   bit 14     chain regardless of the parent's rank
   //   bit 15     no hints from inline expansions   bit 16  no unchained-best hints
-  //   bit 17     also hint the third child
+  //   bit 17     also hint the third child         bit 18  early next top (latency)
+  //   bit 2      plain-loop row dot in the latency-mode expansions
   //   bits 19-21 helpers allowed to take W chunks during the search (default all)
   //   bit 22     the commit warp's scheduler partner pre-expands too
   //   bits 23-26 stop-test pivot slack / 8 (default 48)
@@ -1619,9 +1758,8 @@ bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* sc
     // DUO: TPS with a second warp per query that expands the next top while
     // the commit warp visits the previous packet; taken while the batch fits
     // one wave at <= kDuoPairs queries per SM (duo: 0 auto, 1 forced, -1 off)
-    if (duo >= 0) {
-      PipeLayout ls{uint32_t(D), std::min<uint32_t>(std::max<uint32_t>(a.max_M, 1), RA_TPS_ROWS),
-                    (max_n + 31) / 32, 1, 64};
+    if (!BF && duo >= 0) {  // (f32 rows: the commit warp issues f32 row copies)
+      PipeLayout ls{uint32_t(D), 0, (max_n + 31) / 32, 1, 64};  // (no row tile)
       ls.duo = 1;
       const uint32_t fit = uint32_t(std::min<size_t>((budget - ls.tp_base()) / ls.tp_warp_bytes(),
                                                      kDuoPairs));
@@ -1636,7 +1774,7 @@ bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* sc
           ls.capO = uint32_t(std::min<size_t>(per / 24 - 2, 4096)) & ~31u;
         }
         const size_t bytes = ls.tp_base() + wpc * ls.tp_warp_bytes();
-        auto kern = k_graph_search_pipe<D, true, true, BF, true>;
+        auto kern = k_graph_search_pipe<D, true, true, false, true>;
         static int set_bytes[64] = {};
         if (int(bytes) > set_bytes[ctx->device & 63]) {
           RA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

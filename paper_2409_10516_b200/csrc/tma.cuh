@@ -62,6 +62,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void prefetch_l1(const void* src) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(src));
 }
+// one line into L2, per thread (a vector instruction: no per-lane issue loop,
+// unlike the bulk forms)
+__device__ __forceinline__ void prefetch_l2(const void* src) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(src));
+}
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
