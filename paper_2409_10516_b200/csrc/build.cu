@@ -522,41 +522,112 @@ __global__ void k_any_covered(const uint32_t* deg, uint32_t n, uint32_t* flag) {
 }
 
 // ---- K5 helper: nearest anchor per pending node (:287-316) ------------------------
-__global__ void k_nearest_anchor(const float* __restrict__ keys, uint32_t d,
-                                 const double* __restrict__ norms,
-                                 const uint32_t* __restrict__ pending, uint32_t np,
-                                 const uint32_t* __restrict__ anchors, uint32_t na,
-                                 uint32_t* __restrict__ nearest) {
-  const uint32_t i = blockIdx.x;
+// The reference's a_norm - 2 * U.A^T + argmin as a tiled FP64 CUDA-core
+// GEMM: a block holds 64 pending rows and, chunk by chunk, 64 anchor rows
+// in shared memory widened to f64 (exact); each thread keeps a 4 x 4 block
+// of in-order dot chains (16 independent chains, operands reused 4x), then
+// the running (distance, anchor index) minimum per pending row, lower index
+// first on ties (the reference's strict < over ascending anchors).
+constexpr uint32_t NA_T = 64;  // pending rows and anchors per tile
+
+// wide rows (the tiles would not fit shared memory): one warp per pending
+// node, lanes stride the anchors
+__global__ void __launch_bounds__(256)
+    k_nearest_anchor_warp(const float* __restrict__ keys, uint32_t d,
+                          const double* __restrict__ norms, const uint32_t* __restrict__ pending,
+                          uint32_t np, const uint32_t* __restrict__ anchors, uint32_t na,
+                          uint32_t* __restrict__ nearest) {
+  const uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= np) return;
   const float* ku = keys + size_t(pending[i]) * d;
   double best = DBL_MAX;
   uint32_t bj = kSentinel;
-  for (uint32_t j = threadIdx.x; j < na; j += blockDim.x) {
-    const uint32_t a = anchors[j];
-    const double dist = norms[a] - 2.0 * dot_rows(ku, keys + size_t(a) * d, d);
-    if (dist < best || (dist == best && j < bj)) {
-      best = dist;
-      bj = j;
-    }
+  for (uint32_t j = lane; j < na; j += 32) {
+    const double dist = norms[anchors[j]] - 2.0 * dot_rows(ku, keys + size_t(anchors[j]) * d, d);
+    if (dist < best) best = dist, bj = j;
   }
-  __shared__ double sb[256];
-  __shared__ uint32_t sj[256];
-  sb[threadIdx.x] = best;
-  sj[threadIdx.x] = bj;
-  __syncthreads();
-  for (uint32_t s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) {
-      const double b2 = sb[threadIdx.x + s];
-      const uint32_t j2 = sj[threadIdx.x + s];
-      if (b2 < sb[threadIdx.x] || (b2 == sb[threadIdx.x] && j2 < sj[threadIdx.x])) {
-        sb[threadIdx.x] = b2;
-        sj[threadIdx.x] = j2;
-      }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double b2 = __shfl_xor_sync(kFull, best, o);
+    const uint32_t j2 = __shfl_xor_sync(kFull, bj, o);
+    if (b2 < best || (b2 == best && j2 < bj)) best = b2, bj = j2;
+  }
+  if (lane == 0) nearest[i] = anchors[bj];
+}
+
+__global__ void __launch_bounds__(256)
+    k_nearest_anchor(const float* __restrict__ keys, uint32_t d, const double* __restrict__ norms,
+                     const uint32_t* __restrict__ pending, uint32_t np,
+                     const uint32_t* __restrict__ anchors, uint32_t na,
+                     uint32_t* __restrict__ nearest) {
+  extern __shared__ double nsm[];
+  const uint32_t ld = d + 1;  // odd row stride: conflict-free column reads
+  double* P = nsm;            // [NA_T][ld]
+  double* A = nsm + size_t(NA_T) * ld;
+  double* red = A + size_t(NA_T) * ld;  // [NA_T][16] best distances
+  uint32_t* redj = reinterpret_cast<uint32_t*>(red + NA_T * 16);
+  const uint32_t tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const uint32_t p0 = blockIdx.x * NA_T;
+  for (uint32_t t = threadIdx.x; t < NA_T * d; t += blockDim.x) {
+    const uint32_t r = t / d, c = t % d;
+    P[r * ld + c] = p0 + r < np ? (double)keys[size_t(pending[p0 + r]) * d + c] : 0.0;
+  }
+  double best[4];
+  uint32_t bj[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) best[i] = DBL_MAX, bj[i] = kSentinel;
+  for (uint32_t a0 = 0; a0 < na; a0 += NA_T) {
+    __syncthreads();  // (previous chunk consumed; P staged on the first pass)
+    for (uint32_t t = threadIdx.x; t < NA_T * d; t += blockDim.x) {
+      const uint32_t r = t / d, c = t % d;
+      A[r * ld + c] = a0 + r < na ? (double)keys[size_t(anchors[a0 + r]) * d + c] : 0.0;
     }
     __syncthreads();
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (uint32_t c = 0; c < d; ++c) {  // k order (the reference's in-order dot)
+      double pv[4], av[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) pv[i] = P[(ty + 16 * i) * ld + c];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) av[j] = A[(tx + 16 * j) * ld + c];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(pv[i], av[j], acc[i][j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {  // ascending anchor index within this thread
+      const uint32_t aj = a0 + tx + 16 * j;
+      if (aj >= na) continue;
+      const double an = norms[anchors[aj]];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double dist = an - 2.0 * acc[i][j];
+        if (dist < best[i]) best[i] = dist, bj[i] = aj;
+      }
+    }
   }
-  if (threadIdx.x == 0) nearest[i] = anchors[sj[0]];
+  // argmin over the 16 threads sharing each pending row
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    red[(ty + 16 * i) * 16 + tx] = best[i];
+    redj[(ty + 16 * i) * 16 + tx] = bj[i];
+  }
+  __syncthreads();
+  if (threadIdx.x < NA_T && p0 + threadIdx.x < np) {
+    double b = DBL_MAX;
+    uint32_t j = kSentinel;
+    for (uint32_t k = 0; k < 16; ++k) {
+      const double b2 = red[threadIdx.x * 16 + k];
+      const uint32_t j2 = redj[threadIdx.x * 16 + k];
+      if (b2 < b || (b2 == b && j2 < j)) b = b2, j = j2;
+    }
+    nearest[p0 + threadIdx.x] = anchors[j];
+  }
 }
 
 // ---- K5: reachability (the reference's DFS sweep :240-253 and, for the
@@ -874,11 +945,34 @@ static void repair(ra_ctx* ctx, ra_kv* kv, const double* norms_dev, uint64_t ent
       k_deepest_drop<<<1, 1024, 0, s>>>(depth.p, n, M, adj, deg, anchors);
       na = 1;
     }
-    k_nearest_anchor<<<np, 256, 0, s>>>(kv->keys.p, d, norms_dev, pending, np, anchors, na,
-                                        nearest.p);
+    auto tlap = [&](const char* what) {
+      if (!trace) return;
+      RA_CUDA(cudaStreamSynchronize(s));
+      fprintf(stderr, "repair:   %s at %.2f ms\n", what,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                  .count());
+    };
+    tlap("lists");
+    {
+      const size_t sm = (2 * size_t(NA_T) * (d + 1) + NA_T * 16) * 8 + NA_T * 16 * 4;
+      const size_t budget = ctx->smem_optin ? ctx->smem_optin : 227 * 1024;
+      if (sm <= budget) {
+        RA_CUDA(cudaFuncSetAttribute(k_nearest_anchor,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        k_nearest_anchor<<<(np + NA_T - 1) / NA_T, 256, sm, s>>>(kv->keys.p, d, norms_dev,
+                                                                 pending, np, anchors, na,
+                                                                 nearest.p);
+      } else {
+        k_nearest_anchor_warp<<<(np + 7) / 8, 256, 0, s>>>(kv->keys.p, d, norms_dev, pending, np,
+                                                           anchors, na, nearest.p);
+      }
+      RA_LAUNCH_CHECK();
+    }
+    tlap("nearest");
     k_pair_keys<<<(np + 255) / 256, 256, 0, s>>>(nearest.p, pending, np, keys.p);
     tb = tmp.n;
     RA_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, keys.p, keys2.p, int64_t(np), 0, 64, s));
+    tlap("sort");
     RA_CUDA(cudaMemsetAsync(cnt.p, 0, 4, s));
     k_attach<<<np, 256, 0, s>>>(keys2.p, np, M, adj, deg, cnt.p);
     RA_LAUNCH_CHECK();
