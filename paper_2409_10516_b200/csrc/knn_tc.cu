@@ -22,6 +22,9 @@
 //      thr + delta < s_kt proves the (score desc, id asc) top-kt exact.
 //      Rows that fail (or overflow the buffer) go to the exact f64 kernel.
 #include <cfloat>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 
@@ -349,9 +352,63 @@ __device__ __forceinline__ uint64_t okey(double x) {  // order-preserving
   return (u >> 63) ? ~u : (u | (1ull << 63));
 }
 
+// the need-th largest of cnt u32 keys (key_at(i)), one warp, 8-bit radix
+// passes over a 256-bucket shared histogram
+template <class F>
+__device__ uint32_t warp_kth_largest_u32(F key_at, uint32_t cnt, uint32_t need, uint32_t* hist,
+                                         uint32_t lane) {
+  uint32_t prefix = 0, pmask = 0;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (uint32_t b = lane; b < 256; b += 32) hist[b] = 0;
+    __syncwarp();
+    for (uint32_t i = lane; i < cnt; i += 32) {
+      const uint32_t k = key_at(i);
+      if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    uint32_t local = 0;
+    for (int j = 0; j < 8; ++j) local += hist[255 - (lane * 8 + j)];
+    uint32_t incl = local;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= uint32_t(o)) incl += t;
+    }
+    const uint32_t excl = incl - local;
+    const uint32_t owner = __ffs(__ballot_sync(kFull, excl < need && incl >= need)) - 1;
+    uint32_t digit = 0, before = 0;
+    if (lane == owner) {
+      uint32_t acc = excl;
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t bkt = 255 - (lane * 8 + j);
+        if (acc + hist[bkt] >= need) {
+          digit = bkt;
+          before = acc;
+          break;
+        }
+        acc += hist[bkt];
+      }
+    }
+    digit = __shfl_sync(kFull, digit, owner);
+    before = __shfl_sync(kFull, before, owner);
+    need -= before;
+    prefix |= digit << shift;
+    pmask |= 255u << shift;
+    __syncwarp();
+  }
+  return prefix;
+}
+__device__ __forceinline__ uint32_t fkey(float f) {  // order-preserving
+  const uint32_t u = __float_as_uint(f);
+  return (u >> 31) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_inv(uint32_t k) {
+  return __uint_as_float((k >> 31) ? (k & 0x7FFFFFFFu) : ~k);
+}
+
 __global__ void __launch_bounds__(RS_WARPS * 32)
     k_rescore(const float* __restrict__ Q, const float* __restrict__ K, uint64_t nq, uint32_t d,
-              uint32_t kt, uint32_t cb, const uint32_t* __restrict__ bufI,
+              uint32_t kt, uint32_t cb, const float* __restrict__ bufS,
+              const uint32_t* __restrict__ bufI,
               const uint32_t* __restrict__ cnt_in, const float* __restrict__ thr_in,
               double delta_scale, double kmax_norm, uint32_t* __restrict__ knn,
               uint32_t* __restrict__ fail, uint32_t* __restrict__ fail_count) {
@@ -368,17 +425,38 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
   bool ok = cnt <= cb && cnt >= kt;
   if (ok) {
     const float* qr = Q + q * d;
-    // q staged as f64 in the (not yet used) histogram area's tail: d <= 128
+    double qn = 0.0;
+    for (uint32_t i = 0; i < d; ++i) qn = fma((double)qr[i], (double)qr[i], qn);
+    const double delta = delta_scale * sqrt(qn) * kmax_norm;
+    // Only survivors that can rank in the exact top-kt are rescored: at least
+    // kt survivors have S~ >= s~kt (the kt-th largest approximate score), so
+    // s_kt >= s~kt - delta, and one with S~ < s~kt - 2 delta has
+    // S <= S~ + delta < s_kt: strictly outside (ties included).
+    const float* sv = bufS + q * cb;
+    const uint32_t* sid = bufI + q * cb;
+    const float skt =
+        fkey_inv(warp_kth_largest_u32([&](uint32_t i) { return fkey(sv[i]); }, cnt, kt, hist, lane));
+    const double cut = (double)skt - 2.0 * delta;
+    uint32_t m = 0;
+    for (uint32_t c0 = 0; c0 < cnt; c0 += 32) {
+      const uint32_t i = c0 + lane;
+      const bool keep = i < cnt && (double)sv[i] >= cut;
+      const uint32_t bm = __ballot_sync(kFull, keep);
+      if (keep) ei[m + __popc(bm & ((1u << lane) - 1u))] = sid[i];
+      m += __popc(bm);
+    }
+    __syncwarp();
+    // q staged as f64 in the (now unused) histogram area's tail: d <= 128
     double* qd = reinterpret_cast<double*>(hist);
     for (uint32_t j = lane; j < d; j += 32) qd[j] = (double)qr[j];
     __syncwarp();
     // the reference's in-order f64 dot; each lane runs two independent
     // survivors' chains side by side (twice the loads in flight, DFMA
     // latency hidden by the other chain)
-    for (uint32_t i0 = 0; i0 < cnt; i0 += 64) {
+    for (uint32_t i0 = 0; i0 < m; i0 += 64) {
       const uint32_t ia = i0 + lane, ib = i0 + 32 + lane;
-      const bool va = ia < cnt, vb = ib < cnt;
-      const uint32_t ida = va ? bufI[q * cb + ia] : 0, idb = vb ? bufI[q * cb + ib] : 0;
+      const bool va = ia < m, vb = ib < m;
+      const uint32_t ida = va ? ei[ia] : 0, idb = vb ? ei[ib] : 0;
       const float4* ka = reinterpret_cast<const float4*>(K + size_t(ida) * d);
       const float4* kb = reinterpret_cast<const float4*>(K + size_t(idb) * d);
       double acc_a = 0.0, acc_b = 0.0;
@@ -413,7 +491,7 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
     for (int shift = 56; shift >= 0; shift -= 8) {
       for (uint32_t b = lane; b < 256; b += 32) hist[b] = 0;
       __syncwarp();
-      for (uint32_t i = lane; i < cnt; i += 32) {
+      for (uint32_t i = lane; i < m; i += 32) {
         const uint64_t k = okey(es[i]);
         if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
       }
@@ -449,18 +527,15 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
       __syncwarp();
     }
     // prefix = key of the kt-th largest; certificate tau + delta < s_kt
-    double qn = 0.0;
-    for (uint32_t i = 0; i < d; ++i) qn = fma((double)qr[i], (double)qr[i], qn);
     const uint64_t u = (prefix >> 63) ? (prefix & ~(1ull << 63)) : ~prefix;
     const double s_kt = __longlong_as_double(u);
-    const double delta = delta_scale * sqrt(qn) * kmax_norm;
     ok = thr == -FLT_MAX || (double)thr + delta < s_kt;
     if (ok) {
       // gather entries >= s_kt (kt + ties), sort (score desc, id asc), emit kt
       uint32_t base = 0;
-      for (uint32_t c0 = 0; c0 < cnt; c0 += 32) {
+      for (uint32_t c0 = 0; c0 < m; c0 += 32) {
         const uint32_t i = c0 + lane;
-        const bool take = i < cnt && es[i] >= s_kt;
+        const bool take = i < m && es[i] >= s_kt;
         const double sv = take ? es[i] : 0.0;
         const uint32_t iv = take ? ei[i] : 0;
         const uint32_t m = __ballot_sync(kFull, take);
@@ -513,6 +588,14 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
                 uint32_t kt, uint32_t* knn, DevBuf<uint32_t>& fail_rows, double* ms_gemm) {
   cudaStream_t s = ctx->stream;
   const uint32_t K3 = 3 * d;
+  static const bool trace = std::getenv("RA_KNN_TRACE") != nullptr;
+  const auto tk0 = std::chrono::steady_clock::now();
+  auto tlap = [&](const char* what) {
+    if (!trace) return;
+    RA_CUDA(cudaStreamSynchronize(s));
+    fprintf(stderr, "knn_tc: %-10s at %.2f ms\n", what,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tk0).count());
+  };
   const uint64_t mt = (nq + TM - 1) / TM, nt = (n + TN - 1) / TN;
   constexpr uint32_t cb = 2048;     // survivor buffer per row
   constexpr uint32_t msamp = 2048;  // strided key sample for the threshold
@@ -524,6 +607,7 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
     k_split<<<uint32_t((tb + 255) / 256), 256, 0, s>>>(K, n, d, TN, nt, 0, B.p);
     RA_LAUNCH_CHECK();
   }
+  tlap("split");
   DevBuf<float> bufS(nq * cb, s), thr(nq, s);
   DevBuf<uint32_t> bufI(nq * cb, s), cnt(nq, s);
   const size_t smem = size_t(TM) * K3 * 2 + NSTAGE * TN * KS * 2 + 256;
@@ -567,6 +651,7 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
       RA_LAUNCH_CHECK();
     }
   }
+  tlap("threshold");
   // pass 2: every key, keep S~ > threshold
   TcArgs t2{A.p, B.p, nq, n, K3, cb, sampled ? thr.p : nullptr, bufS.p, bufI.p, cnt.p};
   k_knn_tc<<<uint32_t(mt), KNN_THREADS, smem, s>>>(t2);
@@ -578,6 +663,7 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
   unsigned long long km_bits = 0;
   RA_CUDA(cudaMemcpyAsync(&km_bits, kmax.p, 8, cudaMemcpyDeviceToHost, s));
   RA_CUDA(cudaStreamSynchronize(s));
+  tlap("main+norm");
   float gms = 0;
   cudaEventElapsedTime(&gms, e0, e1);
   if (ms_gemm) *ms_gemm = gms;
@@ -593,12 +679,13 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
   const size_t rs_smem = RS_WARPS * (size_t(cb) * 12 + 256 * 4);
   RA_CUDA(cudaFuncSetAttribute(k_rescore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem));
   k_rescore<<<uint32_t((nq + RS_WARPS - 1) / RS_WARPS), RS_WARPS * 32, rs_smem, s>>>(
-      Q, K, nq, d, kt, cb, bufI.p, cnt.p, sampled ? thr.p : nullptr, delta_scale, kmax_norm, knn,
+      Q, K, nq, d, kt, cb, bufS.p, bufI.p, cnt.p, sampled ? thr.p : nullptr, delta_scale, kmax_norm, knn,
       fail_rows.p, fcount.p);
   RA_LAUNCH_CHECK();
   uint32_t nf = 0;
   RA_CUDA(cudaMemcpyAsync(&nf, fcount.p, 4, cudaMemcpyDeviceToHost, s));
   RA_CUDA(cudaStreamSynchronize(s));
+  tlap("rescore");
   return nf;
 }
 
