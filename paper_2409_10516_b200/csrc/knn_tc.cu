@@ -345,7 +345,6 @@ __global__ void k_select_thr(const float* __restrict__ bufS, const uint32_t* __r
 }
 
 // ---- exact rescoring of every survivor + certificate (warp per row) ----------
-constexpr uint32_t RS_WARPS = 2;
 
 __device__ __forceinline__ uint64_t okey(double x) {  // order-preserving
   const uint64_t u = __double_as_longlong(x);
@@ -405,45 +404,66 @@ __device__ __forceinline__ float fkey_inv(uint32_t k) {
   return __uint_as_float((k >> 31) ? (k & 0x7FFFFFFFu) : ~k);
 }
 
-__global__ void __launch_bounds__(RS_WARPS * 32)
+// WARPS rows per block, `cap` rescored survivors per row in shared memory;
+// rows with more (a wide certified band) go to `defer` for a pass with
+// cap = cb (or fail when defer is null). rows: the row ids (null = 0..nq).
+template <uint32_t WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
     k_rescore(const float* __restrict__ Q, const float* __restrict__ K, uint64_t nq, uint32_t d,
-              uint32_t kt, uint32_t cb, const float* __restrict__ bufS,
-              const uint32_t* __restrict__ bufI,
+              uint32_t kt, uint32_t cb, uint32_t cap, const uint32_t* __restrict__ rows,
+              uint32_t* __restrict__ defer, uint32_t* __restrict__ defer_count,
+              const float* __restrict__ bufS, const uint32_t* __restrict__ bufI,
               const uint32_t* __restrict__ cnt_in, const float* __restrict__ thr_in,
               double delta_scale, double kmax_norm, uint32_t* __restrict__ knn,
               uint32_t* __restrict__ fail, uint32_t* __restrict__ fail_count) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t q = blockIdx.x * uint64_t(RS_WARPS) + warp;
-  if (q >= nq) return;
-  const size_t per_warp = size_t(cb) * 12 + 256 * 4;
+  const uint64_t r = blockIdx.x * uint64_t(WARPS) + warp;
+  if (r >= nq) return;
+  const uint64_t q = rows ? rows[r] : r;
+  const size_t per_warp = size_t(cap) * 12 + 256 * 4;
   double* es = reinterpret_cast<double*>(smem + warp * per_warp);
-  uint32_t* ei = reinterpret_cast<uint32_t*>(es + cb);
-  uint32_t* hist = ei + cb;
+  uint32_t* ei = reinterpret_cast<uint32_t*>(es + cap);
+  uint32_t* hist = ei + cap;
   const uint32_t cnt = cnt_in[q];
   const float thr = thr_in ? thr_in[q] : -FLT_MAX;
   bool ok = cnt <= cb && cnt >= kt;
+  const float* qr = Q + q * d;
+  const float* sv = bufS + q * cb;
+  const uint32_t* sid = bufI + q * cb;
+  double delta = 0.0, cut = 0.0;
+  uint32_t m = 0;
   if (ok) {
-    const float* qr = Q + q * d;
     double qn = 0.0;
     for (uint32_t i = 0; i < d; ++i) qn = fma((double)qr[i], (double)qr[i], qn);
-    const double delta = delta_scale * sqrt(qn) * kmax_norm;
+    delta = delta_scale * sqrt(qn) * kmax_norm;
     // Only survivors that can rank in the exact top-kt are rescored: at least
     // kt survivors have S~ >= s~kt (the kt-th largest approximate score), so
     // s_kt >= s~kt - delta, and one with S~ < s~kt - 2 delta has
     // S <= S~ + delta < s_kt: strictly outside (ties included).
-    const float* sv = bufS + q * cb;
-    const uint32_t* sid = bufI + q * cb;
     const float skt =
         fkey_inv(warp_kth_largest_u32([&](uint32_t i) { return fkey(sv[i]); }, cnt, kt, hist, lane));
-    const double cut = (double)skt - 2.0 * delta;
-    uint32_t m = 0;
+    cut = (double)skt - 2.0 * delta;
+    for (uint32_t c0 = 0; c0 < cnt; c0 += 32) {
+      const uint32_t i = c0 + lane;
+      m += __popc(__ballot_sync(kFull, i < cnt && (double)sv[i] >= cut));
+    }
+    if (m > cap) {  // the band does not fit this pass
+      if (defer) {
+        if (lane == 0) defer[atomicAdd(defer_count, 1u)] = uint32_t(q);
+        return;
+      }
+      ok = false;
+    }
+  }
+  if (ok) {
+    uint32_t w = 0;
     for (uint32_t c0 = 0; c0 < cnt; c0 += 32) {
       const uint32_t i = c0 + lane;
       const bool keep = i < cnt && (double)sv[i] >= cut;
       const uint32_t bm = __ballot_sync(kFull, keep);
-      if (keep) ei[m + __popc(bm & ((1u << lane) - 1u))] = sid[i];
-      m += __popc(bm);
+      if (keep) ei[w + __popc(bm & ((1u << lane) - 1u))] = sid[i];
+      w += __popc(bm);
     }
     __syncwarp();
     // q staged as f64 in the (now unused) histogram area's tail: d <= 128
@@ -676,12 +696,31 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
   RA_CUDA(cudaMemsetAsync(fcount.p, 0, 4, s));
   // |S - S~| <= (3 * 2^-16 + K3 * 2^-23) * |q| |k|; 2^-10 is generous
   const double delta_scale = 1.0 / 1024.0;
-  const size_t rs_smem = RS_WARPS * (size_t(cb) * 12 + 256 * 4);
-  RA_CUDA(cudaFuncSetAttribute(k_rescore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem));
-  k_rescore<<<uint32_t((nq + RS_WARPS - 1) / RS_WARPS), RS_WARPS * 32, rs_smem, s>>>(
-      Q, K, nq, d, kt, cb, bufS.p, bufI.p, cnt.p, sampled ? thr.p : nullptr, delta_scale, kmax_norm, knn,
-      fail_rows.p, fcount.p);
-  RA_LAUNCH_CHECK();
+  // pass 1: 8 rows per block, 512 rescored survivors per row in shared
+  // memory (occupancy); rows whose certified band is wider go to pass 2
+  constexpr uint32_t kCap1 = 512;
+  DevBuf<uint32_t> defer(std::max<uint64_t>(nq, 1), s), dcount(1, s);
+  RA_CUDA(cudaMemsetAsync(dcount.p, 0, 4, s));
+  {
+    const size_t sm1 = 8 * (size_t(kCap1) * 12 + 256 * 4);
+    RA_CUDA(cudaFuncSetAttribute(k_rescore<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+    k_rescore<8><<<uint32_t((nq + 7) / 8), 8 * 32, sm1, s>>>(
+        Q, K, nq, d, kt, cb, kCap1, nullptr, defer.p, dcount.p, bufS.p, bufI.p, cnt.p,
+        sampled ? thr.p : nullptr, delta_scale, kmax_norm, knn, fail_rows.p, fcount.p);
+    RA_LAUNCH_CHECK();
+  }
+  uint32_t nd = 0;
+  RA_CUDA(cudaMemcpyAsync(&nd, dcount.p, 4, cudaMemcpyDeviceToHost, s));
+  RA_CUDA(cudaStreamSynchronize(s));
+  if (nd) {
+    const size_t sm2 = 2 * (size_t(cb) * 12 + 256 * 4);
+    RA_CUDA(cudaFuncSetAttribute(k_rescore<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+    k_rescore<2><<<(nd + 1) / 2, 2 * 32, sm2, s>>>(
+        Q, K, nd, d, kt, cb, cb, defer.p, nullptr, nullptr, bufS.p, bufI.p, cnt.p,
+        sampled ? thr.p : nullptr, delta_scale, kmax_norm, knn, fail_rows.p, fcount.p);
+    RA_LAUNCH_CHECK();
+  }
+  if (trace) fprintf(stderr, "knn_tc: %u rows in the wide-band rescoring pass\n", nd);
   uint32_t nf = 0;
   RA_CUDA(cudaMemcpyAsync(&nf, fcount.p, 4, cudaMemcpyDeviceToHost, s));
   RA_CUDA(cudaStreamSynchronize(s));
