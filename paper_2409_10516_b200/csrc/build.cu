@@ -356,28 +356,49 @@ __global__ void __launch_bounds__(PWARPS * 32)
     }
     double* bm = sm;
     uint32_t* bv = sv;
+    const float* ku = keys + size_t(u) * d;
+    auto score = [&](uint32_t i, uint32_t at) {  // candidate i's m_uv into slot `at`
+      const uint32_t v = uint32_t(edges[c0 + i]);
+      const double ip = dot_rows(ku, keys + size_t(v) * d, d);
+      bm[at] = euclid ? norms[u] + norms[v] - 2.0 * ip : -ip;
+      bv[at] = v;
+    };
+    auto sort_first = [&](uint32_t total) {  // ascending (m, v) over [0, total)
+      uint32_t p2 = 1;
+      while (p2 < total) p2 <<= 1;
+      for (uint32_t i = total + lane; i < p2; i += 32) {
+        bm[i] = DBL_MAX;
+        bv[i] = kSentinel;
+      }
+      __syncwarp();
+      warp_bitonic_asc(bm, bv, p2, lane);
+    };
     if (global_mode) {
       bm = gm + size_t(wid) * g_stride;
       bv = gv + size_t(wid) * g_stride;
     } else if (c > PCAP) {
-      if (lane == 0) big_nodes[atomicAdd(big_count, 1u)] = u;
-      continue;
+      if (2 * efc > PCAP) {  // (very large ef_construction: the HBM pass)
+        if (lane == 0) big_nodes[atomicAdd(big_count, 1u)] = u;
+        continue;
+      }
+      // hub node: only the best efc candidates are ever read (:179), so
+      // stream the candidates through shared memory in chunks, keeping the
+      // best efc so far sorted in front of each chunk
+      const uint32_t chunk = PCAP - efc;
+      uint32_t r = 0;
+      for (uint32_t s0 = 0; s0 < c; s0 += chunk) {
+        const uint32_t cn = min(chunk, c - s0);
+        for (uint32_t i = lane; i < cn; i += 32) score(s0 + i, r + i);
+        __syncwarp();
+        sort_first(r + cn);
+        r = min(r + cn, efc);
+        __syncwarp();
+      }
     }
-    const float* ku = keys + size_t(u) * d;
-    for (uint32_t i = lane; i < c; i += 32) {
-      const uint32_t v = uint32_t(edges[c0 + i]);
-      const double ip = dot_rows(ku, keys + size_t(v) * d, d);
-      bm[i] = euclid ? norms[u] + norms[v] - 2.0 * ip : -ip;
-      bv[i] = v;
+    if (global_mode || c <= PCAP) {
+      for (uint32_t i = lane; i < c; i += 32) score(i, i);
+      sort_first(c);
     }
-    uint32_t p2 = 1;
-    while (p2 < c) p2 <<= 1;
-    for (uint32_t i = c + lane; i < p2; i += 32) {
-      bm[i] = DBL_MAX;
-      bv[i] = kSentinel;
-    }
-    __syncwarp();
-    warp_bitonic_asc(bm, bv, p2, lane);
     const uint32_t no = c < efc ? c : efc;
     uint32_t kn = 0;
     for (uint32_t i = 0; i < no && kn < M; ++i) {

@@ -266,7 +266,8 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
     const float thr = (valid_row && a.thr_in) ? a.thr_in[q] : -FLT_MAX;
     uint32_t cnt = 0;
     float* bs = a.bufS + (valid_row ? q : 0) * size_t(a.cb);
-    uint32_t* bi = a.bufI + (valid_row ? q : 0) * size_t(a.cb);
+    // (threshold passes keep scores only: bufI == null)
+    uint32_t* bi = a.bufI ? a.bufI + (valid_row ? q : 0) * size_t(a.cb) : nullptr;
     for (uint32_t t = 0; t < ntiles; ++t) {
       const uint32_t buf = t & 1u, tph = (t >> 1) & 1u;
       mbar_wait_sleep(t_full + buf, tph);
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
                 if (key0 + j < a.n && v[j] > thr) {
                   if (cnt < a.cb) {
                     bs[cnt] = v[j];
-                    bi[cnt] = key0 + j;
+                    if (bi) bi[cnt] = key0 + j;
                   }
                   cnt = min(cnt + 1, a.cb + 1);
                 }
@@ -643,7 +644,7 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
     DevBuf<uint16_t> Bs(size_t(msamp) * K3, s);
     k_gather_sample<<<(msamp * d + 255) / 256, 256, 0, s>>>(K, n, d, msamp, ks.p);
     k_split<<<(msamp * d + 255) / 256, 256, 0, s>>>(ks.p, msamp, d, TN, msamp / TN, 0, Bs.p);
-    TcArgs t1{A.p, Bs.p, nq, msamp, K3, cb, nullptr, bufS.p, bufI.p, cnt.p};
+    TcArgs t1{A.p, Bs.p, nq, msamp, K3, cb, nullptr, bufS.p, nullptr, cnt.p};
     k_knn_tc<<<uint32_t(mt), KNN_THREADS, smem, s>>>(t1);
     const uint32_t r = std::max<uint32_t>(1, uint32_t((uint64_t(target) * msamp + n - 1) / n));
     if (r >= 8 || n <= 8u * msamp) {
@@ -663,7 +664,7 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
       k_gather_sample<<<uint32_t((uint64_t(m2) * d + 255) / 256), 256, 0, s>>>(K, n, d, m2, ks2.p);
       k_split<<<uint32_t((uint64_t(m2) * d + 255) / 256), 256, 0, s>>>(ks2.p, m2, d, TN, m2 / TN, 0,
                                                                       Bs2.p);
-      TcArgs t1b{A.p, Bs2.p, nq, m2, K3, cb, thr.p, bufS.p, bufI.p, cnt.p};
+      TcArgs t1b{A.p, Bs2.p, nq, m2, K3, cb, thr.p, bufS.p, nullptr, cnt.p};
       k_knn_tc<<<uint32_t(mt), KNN_THREADS, smem, s>>>(t1b);
       const uint32_t r2 = std::max<uint32_t>(1, uint32_t((uint64_t(target) * m2 + n - 1) / n));
       k_select_thr<<<uint32_t((nq + 7) / 8), 256, 0, s>>>(bufS.p, cnt.p, nq, cb, r2, thr2.p);
