@@ -61,6 +61,29 @@ __device__ __forceinline__ double dot_rows(const float* __restrict__ a,
   return acc;
 }
 
+// f32 dot with four partial sums (one per float4 lane component): a fast
+// estimate whose error is at most (d / 4 + 3) * 2^-24 * sum |a_i b_i| <=
+// (d / 4 + 3) * 2^-24 * |a| |b| (recursive fp32 FMA summation, Cauchy-Schwarz)
+__device__ __forceinline__ float dot_f32_est(const float* __restrict__ a, const float* __restrict__ b,
+                                             uint32_t d) {
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  if ((d & 3) == 0) {
+    const float4* a4 = reinterpret_cast<const float4*>(a);
+    const float4* b4 = reinterpret_cast<const float4*>(b);
+#pragma unroll 8
+    for (uint32_t c = 0; c < d / 4; ++c) {
+      const float4 x = __ldg(a4 + c), y = __ldg(b4 + c);
+      s0 = fmaf(x.x, y.x, s0);
+      s1 = fmaf(x.y, y.y, s1);
+      s2 = fmaf(x.z, y.z, s2);
+      s3 = fmaf(x.w, y.w, s3);
+    }
+  } else {
+    for (uint32_t i = 0; i < d; ++i) s0 = fmaf(__ldg(a + i), __ldg(b + i), s0);
+  }
+  return (s0 + s1) + (s2 + s3);
+}
+
 // ---- K0 -------------------------------------------------------------------------
 __global__ void k_norms(const float* __restrict__ keys, uint32_t n, uint32_t d, double* norms) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -409,10 +432,28 @@ __global__ void __launch_bounds__(PWARPS * 32)
         const uint32_t j = j0 + lane;
         bool o = false;
         if (j < kn) {
+          // decided by the fp32 estimate when it is clear of m_uv by more than
+          // its error bound; the exact in-order f64 test otherwise
           const uint32_t w = kept[j];
-          const double ip = dot_rows(keys + size_t(v) * d, keys + size_t(w) * d, d);
-          const double m_vw = euclid ? norms[v] + norms[w] - 2.0 * ip : -ip;
-          o = m_vw < m_uv;
+          const float* kv_ = keys + size_t(v) * d;
+          const float* kw_ = keys + size_t(w) * d;
+          const double nv = norms[v], nw = norms[w];
+          const float ipf = dot_f32_est(kv_, kw_, d);
+          bool decided = false;
+          if (isfinite(ipf)) {
+            const double ipa = ipf;
+            const double eps = double(d + 16) * 0x1p-24 * sqrt(nv * nw);
+            const double ma = euclid ? nv + nw - 2.0 * ipa : -ipa;
+            const double em = (euclid ? 2.0 * eps : eps) +
+                              0x1p-50 * (nv + nw + 2.0 * fabs(ipa) + fabs(m_uv));
+            if (ma + em < m_uv) o = true, decided = true;
+            else if (ma - em > m_uv) decided = true;
+          }
+          if (!decided) {
+            const double ip = dot_rows(kv_, kw_, d);
+            const double m_vw = euclid ? nv + nw - 2.0 * ip : -ip;
+            o = m_vw < m_uv;
+          }
         }
         if (__ballot_sync(kFull, o)) {
           occl = true;
@@ -1155,6 +1196,22 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
     const size_t psmem = PWARPS * (PCAP * 12 + size_t(M) * 4);
     RA_CUDA(cudaFuncSetAttribute(k_prune, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
     const uint32_t pgrid = std::min<uint32_t>((n + PWARPS - 1) / PWARPS, ctx->num_sms * 8);
+    static const bool ptrace = std::getenv("RA_PRUNE_TRACE") != nullptr;
+    if (ptrace) {  // candidate-count profile (profiling aid)
+      std::vector<uint64_t> h(size_t(n) + 1);
+      RA_CUDA(cudaMemcpyAsync(h.data(), off.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
+      RA_CUDA(cudaStreamSynchronize(s));
+      uint64_t mx = 0, big = 0, sum_big = 0;
+      for (uint32_t u = 0; u < n; ++u) {
+        const uint64_t c = h[u + 1] - h[u];
+        mx = std::max(mx, c);
+        if (c > PCAP) ++big, sum_big += c;
+      }
+      fprintf(stderr, "prune: candidates %llu, max per node %llu, nodes > %u: %llu (%llu candidates)\n",
+              (unsigned long long)h[n], (unsigned long long)mx, PCAP, (unsigned long long)big,
+              (unsigned long long)sum_big);
+    }
+    Timer ptm(s);
     k_prune<<<pgrid, PWARPS * 32, psmem, s>>>(K, n, d, norms.p, edges.p, off.p, nullptr, n, M,
                                              p->ef_construction, !p->prune_inner_product, nullptr,
                                              nullptr, 0, g->adj.p, deg.p, big.p, big_cnt.p);
@@ -1181,6 +1238,7 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
       RA_LAUNCH_CHECK();
     }
     edges.reset();
+    if (ptrace) fprintf(stderr, "prune: %.2f ms (second pass nodes %u)\n", ptm.lap(), nbig);
     st.ms_prune = tm.lap();
 
     // ---- entry point ----
