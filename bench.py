@@ -212,7 +212,7 @@ def ncu_summary(name="ncu_search_summary.json"):
 
 
 def ncu_traffic():
-    return ncu_summary().get("dram_bytes_per_launch")
+    return (ncu_summary("ncu_search_summary_r2.json") or ncu_summary()).get("dram_bytes_per_launch")
 
 
 def cpu_model():
