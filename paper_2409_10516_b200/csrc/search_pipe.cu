@@ -1397,11 +1397,12 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
       __threadfence_block();
       const uint32_t v = duo_rv[lane], nm = duo_rf[0];
       const bool isnew = (nm >> lane) & 1u;
-      const uint32_t mm = __ballot_sync(kFull, isnew && masked_id(v));  // (W: not a pool entry)
+      // the static-set bit is requested now and used after the chain
+      const uint32_t mw = (isnew && a.mask_bits) ? __ldg(a.mask_bits + (v >> 5)) : 0u;
       const uint64_t td0 = clock64();
       uint64_t sk = 0;
       if (isnew) sk = okey(row_dot<D>(qd, keys + size_t(v) * D));  // (rows L2-prefetched)
-      __syncwarp();
+      const uint32_t mm = __ballot_sync(kFull, isnew && ((mw >> (v & 31)) & 1u));  // (W: not a pool entry)
       cy_dot += clock64() - td0;
       duo_pk[lane] = sk;
       duo_pi[lane] = v;
