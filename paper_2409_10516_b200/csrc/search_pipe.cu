@@ -975,6 +975,7 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
     // - and posts it; the expansion warp runs the dot chains on those rows
     // and returns the packet while this warp visits the previous one.
     uint32_t dseq = 0;
+    uint32_t spec_v = kSentinel;  // DUO: this lane's neighbour of the speculated top
     auto duo_issue = [&](uint32_t p) {
       ++dseq;
       if (p != kSentinel) {
@@ -1056,6 +1057,14 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
     for (;;) {
       visit(cand, cx, cv, cm, pre);
       PIPE_TICK(3)
+      if constexpr (DUO) {  // the speculative prefetch (see below), after the visit
+        if (spec_v != kSentinel && !((vis[spec_v >> 5] >> (spec_v & 31)) & 1u)) {
+          const char* r = reinterpret_cast<const char*>(keys + size_t(spec_v) * D);
+#pragma unroll
+          for (int l = 0; l < D * 4 / 128; ++l) prefetch_l2(r + 128 * l);
+        }
+        spec_v = kSentinel;
+      }
       // frontier top (:387): lane heads vs the best overflow entry
       uint64_t tk;
       uint32_t tid;
@@ -1155,6 +1164,21 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
           // the expansion warp starts on it while this warp does the visit
           next_top(cand && cx >= thr, cx, cv);
           duo_issue(nid);
+          if (!(a.flags & (1u << 27))) {
+            // speculation two links ahead: the runner-up (the best of the
+            // frontier and these children other than nid) is the top after
+            // nid unless one of nid's children beats it; its adjacency row
+            // (an L2 hit: prefetched when it was found) is requested now and
+            // its new neighbours' key rows are prefetched after the visit
+            const bool inf2 = cand && cx >= thr && cv != nid;
+            uint64_t k2 = hi != nid ? hk : 0;
+            uint32_t i2 = hi != nid ? hi : kSentinel;
+            if (inf2 && better(cx, cv, k2, i2)) k2 = cx, i2 = cv;
+            warp_best(k2, i2);
+            if (nFO && fo_id != nid && better(fo_k, fo_id, k2, i2)) i2 = fo_id;
+            spec_v = (i2 != kSentinel && lane < M) ? __ldg(adj + size_t(i2) * M + lane)
+                                                   : 0xFFFFFFFFu;
+          }
         } else {
           expand(tid, cv, cx, cand, cm);
         }
@@ -1729,6 +1753,7 @@ bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* sc
   //   bit 15     no hints from inline expansions   bit 16  no unchained-best hints
   //   bit 17     also hint the third child         bit 18  early next top (latency)
   //   bit 2      plain-loop row dot in the latency-mode expansions
+  //   bit 27     DUO: no two-ahead row speculation
   //   bits 19-21 helpers allowed to take W chunks during the search (default all)
   //   bit 22     the commit warp's scheduler partner pre-expands too
   //   bits 23-26 stop-test pivot slack / 8 (default 48)
