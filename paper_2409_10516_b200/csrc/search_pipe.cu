@@ -1000,11 +1000,8 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
         }
         // (the best new neighbour is likely a top soon: its adjacency row,
         // the first load of its issue, to L2 now)
-        if (isnew && !(a.flags & 2u)) {
-          const char* ar = reinterpret_cast<const char*>(adj + size_t(v) * M);
-          prefetch_l2(ar);
-          prefetch_l2(ar + M * 4 - 1);
-        }
+        if (isnew && !(a.flags & 2u))  // (the row's first line; a straddling tail comes with the load)
+          prefetch_l2(adj + size_t(v) * M);
         c_fsp += clock64() - ti0;  // (dbg: the whole issue)
       } else if (lane == 0) {
         __threadfence_block();
