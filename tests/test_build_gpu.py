@@ -177,6 +177,10 @@ def test_tensor_core_knn_matches_exact_path(port):
         finally:
             del os.environ["RA_KNN_EXACT"]
         assert g_tc.serialize() == g_ex.serialize()
+        if n == 6000:  # and the oracle's phases 1-4 (the d = 64 case: seconds on one core)
+            from oracle.ffi import BuildParams
+            assert g_tc.serialize() == port.graph_build(w["keys"][0], w["prefill_q"][0],
+                                                        BuildParams(128, 24, 256, 8))
         # certificate failures are rare and recomputed exactly
         assert g_tc.build_stats.knn_rows == n
         assert g_tc.build_stats.knn_rows_widened < n // 10
