@@ -800,7 +800,8 @@ ra_status ra_engine_create(ra_ctx* ctx, ra_kv* const* groups, uint32_t n_groups,
         const char* v = std::getenv("RA_FUSED_ATTN");
         return v && v[0] == '0';
       }();
-      e->fused = !fa_off && e->fast_attn && !e->groups[0]->bf16 && !e->groups[0]->bf16_attn &&
+      e->fused = !fa_off && e->fast_attn &&
+                 !(e->groups[0]->bf16_attn && !e->groups[0]->bf16) &&  // (not attention-only bf16)
                  e->n_pool > 0 && search_fuses_attention(ctx, probe, e->max_n);
       if (e->fused) {
         const uint32_t rows = std::max<uint32_t>(e->max_M, 1);  // the kernel's tile rows

@@ -1102,7 +1102,7 @@ int search_variant(const ra_ctx* ctx) {
 
 bool search_fuses_attention(const ra_ctx* ctx, const SearchArgs& a, uint32_t max_n) {
   const int v = search_variant(ctx);
-  if (!(v == 0 || v == 4) || a.bf16 || a.B == 0) return false;
+  if (!(v == 0 || v == 4) || a.B == 0) return false;
   if (v == 0 && a.B > 2u * uint32_t(ctx->num_sms)) return false;  // throughput mode
   return pipe_latency_supported(ctx, a.d, a.max_M, max_n);
 }

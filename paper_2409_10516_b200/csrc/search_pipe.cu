@@ -1280,7 +1280,7 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
       __syncwarp();
       // (fused attention: leave room for >= 8 staged V rows behind the array)
       fin_smem = PipeLayout::arr_bytes(p2) + 16 +
-                     (a.fa.out && !BF ? (40 + 32 * (size_t(D) + 2)) * 8 + 8 * (size_t(D) * 4 + 8)
+                     (a.fa.out ? (40 + 32 * (size_t(D) + 2)) * 8 + 8 * (size_t(D) * 4 + 8)
                                       : 0) <=
                  size_t(kPW) * lay.tile_bytes();
       if (lane == 0) {
@@ -1480,7 +1480,9 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
     };
     // fused attention: one chunk of W (the tile's MT rows) -> its partial
     // (sum e*v, max, sum e) in the head's scratch row, in W order
-    const bool fused = !BF && a.fa.out != nullptr;
+    // (bf16 groups: the W rows come from the f32 copy, which holds the same
+    // rounded values)
+    const bool fused = a.fa.out != nullptr;
     auto wchunk = [&](uint32_t c) {
       const uint32_t r0 = c * a.fa.crows, rows = min(a.fa.crows, a.fa.nW - r0);
       const float* V = a.fa.values[b];
@@ -1728,9 +1730,8 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
     a.n_out[b] = take;
     a.truncated[b] = take < k;
   }
-  if constexpr (!BF) {
-    if (a.fa.out) fused_attention_tail<D>(a, lay, b, A, p2, fin_smem, take, smem);
-  }
+  if (a.fa.out) fused_attention_tail<D>(a, lay, b, A, p2, fin_smem, take, smem);
+
 }
 
 template <int D, bool BF>
@@ -1851,7 +1852,6 @@ bool launch_pipe_d(ra_ctx* ctx, const SearchArgs& a, uint32_t max_n, uint8_t* sc
     RA_LAUNCH_CHECK();
     return true;
   }
-  if (BF) s.fa.out = nullptr;  // fused attention reads f32 rows only
   PipeLayout lay{uint32_t(D), std::max<uint32_t>(a.max_M, 1), (max_n + 31) / 32, 1, 0};
   if (s.fa.out) {
     // the fused tail stages the W chunk partials and >= 8 V rows in the

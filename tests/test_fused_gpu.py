@@ -34,6 +34,8 @@ def test_kernels_per_step():
     assert eng.kernels_per_step() == 1
     eng16, _ = _engine("bf16_attn")
     assert eng16.kernels_per_step() == 3
+    engb, _ = _engine("bf16")  # full bf16: the tail reads the f32 copy (same rounded values)
+    assert engb.kernels_per_step() == 1
 
 
 def test_fused_and_three_kernel_steps_agree(tmp_path):
