@@ -12,10 +12,10 @@
 //   K3 k_prune        phase 3 occlusion prune, one warp per node (:162-202)
 //   K4 entry point    medoid / max-norm argmin-argmax (:207-233)
 //   K5 repair         phase 4 (:235-348) on the GPU: reachability by a
-//                     cooperative level-synchronous BFS, pending / anchor
-//                     lists by stream compaction, nearest anchor, (anchor,
-//                     node) sort, one thread per anchor group for the chained
-//                     attachments; the host only reads the round's counts
+//                     work-queue sweep, pending / anchor lists by stream
+//                     compaction, the nearest anchor as a tiled FP64 GEMM,
+//                     (anchor, node) sort, one block per anchor group for the
+//                     chained attachments; the host only reads the counts
 // Every f64 reduction runs in the reference's order (through the
 // sequential-order Eigen contract of oracle/shim), so adjacency, entry point
 // and OODG blob are bit-identical to the oracle build.
@@ -290,9 +290,18 @@ __host__ __device__ inline uint32_t prop_count(uint32_t b, uint32_t w) {
   return (lo > 0 ? 1u : 0u) + (b - lo);
 }
 
+// bits of an id in [0, n) (>= 1)
+__host__ __device__ __forceinline__ uint32_t edge_bits(uint32_t n) {
+  uint32_t b = 1;
+  while (b < 32 && (uint64_t(n - 1) >> b) != 0) ++b;
+  return b;
+}
+
+// proposals packed as (src << eb) | dst with eb = bits of n - 1, so the
+// radix sort runs over 2 * eb key bits only
 __global__ void k_proposals(const uint32_t* __restrict__ knn, uint64_t nq, uint32_t kt,
                             uint32_t w, const uint32_t* __restrict__ b_off, uint32_t per_row,
-                            uint64_t* __restrict__ out) {
+                            uint32_t eb, uint64_t* __restrict__ out) {
   const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (t >= nq * (kt - 1)) return;
   const uint64_t qi = t / (kt - 1);
@@ -301,15 +310,15 @@ __global__ void k_proposals(const uint32_t* __restrict__ knn, uint64_t nq, uint3
   const uint64_t u = row[b];
   uint64_t* o = out + qi * per_row + b_off[b];
   const uint32_t lo = prop_lo(b, w);
-  if (lo > 0) *o++ = u << 32 | row[0];
-  for (uint32_t a = lo; a < b; ++a) *o++ = u << 32 | row[a];
+  if (lo > 0) *o++ = u << eb | row[0];
+  for (uint32_t a = lo; a < b; ++a) *o++ = u << eb | row[a];
 }
 
 __global__ void k_src_offsets(const uint64_t* __restrict__ edges, uint64_t ne, uint32_t n,
-                              uint64_t* __restrict__ off) {
+                              uint32_t eb, uint64_t* __restrict__ off) {
   const uint64_t u = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (u > n) return;
-  const uint64_t key = u << 32;
+  const uint64_t key = u << eb;
   uint64_t lo = 0, hi = ne;
   while (lo < hi) {
     const uint64_t mid = (lo + hi) >> 1;
@@ -362,6 +371,7 @@ __global__ void __launch_bounds__(PWARPS * 32)
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t wid = blockIdx.x * PWARPS + warp;
+  const uint64_t dst_mask = (1ull << edge_bits(n)) - 1;  // (edges: src << eb | dst)
   const bool global_mode = gm != nullptr;
   double* sm = reinterpret_cast<double*>(smem) + size_t(warp) * PCAP;
   uint32_t* sv = reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(smem) + PWARPS * PCAP) +
@@ -381,7 +391,7 @@ __global__ void __launch_bounds__(PWARPS * 32)
     uint32_t* bv = sv;
     const float* ku = keys + size_t(u) * d;
     auto score = [&](uint32_t i, uint32_t at) {  // candidate i's m_uv into slot `at`
-      const uint32_t v = uint32_t(edges[c0 + i]);
+      const uint32_t v = uint32_t(edges[c0 + i] & dst_mask);
       const double ip = dot_rows(ku, keys + size_t(v) * d, d);
       bm[at] = euclid ? norms[u] + norms[v] - 2.0 * ip : -ip;
       bv[at] = v;
@@ -1160,11 +1170,10 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
       DevBuf<uint32_t> d_boff(b_off.size(), s);
       RA_CUDA(cudaMemcpyAsync(d_boff.p, b_off.data(), b_off.size() * 4, cudaMemcpyHostToDevice, s));
       const uint64_t threads = uint64_t(nq) * (kt - 1);
-      k_proposals<<<uint32_t((threads + 255) / 256), 256, 0, s>>>(knn.p, nq, kt, p->edge_window,
-                                                                 d_boff.p, per_row, edges.p);
+      k_proposals<<<uint32_t((threads + 255) / 256), 256, 0, s>>>(
+          knn.p, nq, kt, p->edge_window, d_boff.p, per_row, edge_bits(n), edges.p);
       RA_LAUNCH_CHECK();
-      int end_bit = 32;
-      while (end_bit < 64 && (uint64_t(n - 1) >> (end_bit - 32)) != 0) ++end_bit;
+      const int end_bit = int(2 * edge_bits(n));
       size_t tb = 0;
       cub::DeviceRadixSort::SortKeys(nullptr, tb, edges.p, edges2.p, (int64_t)total, 0, end_bit, s);
       DevBuf<uint8_t> tmp(tb, s);
@@ -1181,7 +1190,7 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
     edges2.reset();
     st.candidate_edges = ne;
     DevBuf<uint64_t> off(size_t(n) + 1, s);
-    k_src_offsets<<<(n + 1 + 255) / 256, 256, 0, s>>>(edges.p, ne, n, off.p);
+    k_src_offsets<<<(n + 1 + 255) / 256, 256, 0, s>>>(edges.p, ne, n, edge_bits(n), off.p);
     RA_LAUNCH_CHECK();
     st.ms_edges = tm.lap();
 
@@ -1190,8 +1199,11 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
     g->n = n;
     g->max_degree = M;
     g->default_ef = p->default_ef;
-    g->adj.alloc(size_t(n) * M);
+    const auto ta0 = std::chrono::steady_clock::now();
+    g->adj.alloc_lived(size_t(n) * M, s);
     DevBuf<uint32_t> deg(n, s), big(n, s), big_cnt(1, s);
+    const double alloc_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ta0).count();
     RA_CUDA(cudaMemsetAsync(big_cnt.p, 0, 4, s));
     const size_t psmem = PWARPS * (PCAP * 12 + size_t(M) * 4);
     RA_CUDA(cudaFuncSetAttribute(k_prune, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
@@ -1238,7 +1250,9 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
       RA_LAUNCH_CHECK();
     }
     edges.reset();
-    if (ptrace) fprintf(stderr, "prune: %.2f ms (second pass nodes %u)\n", ptm.lap(), nbig);
+    if (ptrace)
+      fprintf(stderr, "prune: %.2f ms (second pass nodes %u), allocations %.2f ms\n", ptm.lap(), nbig,
+              alloc_ms);
     st.ms_prune = tm.lap();
 
     // ---- entry point ----

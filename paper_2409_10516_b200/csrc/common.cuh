@@ -93,6 +93,14 @@ struct DevBuf {
     if (count) RA_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
     n = count, st = s, pooled = true;
   }
+  // a long-lived buffer taken from the stream-ordered pool (no synchronous
+  // cudaMalloc on the build path: those measured up to 135 ms at times),
+  // released with cudaFree (valid for pool memory; it synchronizes)
+  void alloc_lived(size_t count, cudaStream_t s) {
+    reset();
+    if (count) RA_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
+    n = count;
+  }
   // grow-only reallocation (contents not preserved)
   void ensure(size_t count) {
     if (count > n) alloc(count);
