@@ -1090,6 +1090,21 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
     DevBuf<double> norms(n, s);
     k_norms<<<(n + 255) / 256, 256, 0, s>>>(K, n, d, norms.p);
     RA_LAUNCH_CHECK();
+    // the medoid's column mean (a long dependent add chain per column, on 4
+    // SMs) runs on the side stream beside phases 1-3; joined at the entry
+    DevBuf<double> mean(d, s);
+    if (!p->entry_maxnorm) {
+      if (!ctx->side) {
+        RA_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        RA_CUDA(cudaEventCreateWithFlags(&ctx->side_fork, cudaEventDisableTiming));
+        RA_CUDA(cudaEventCreateWithFlags(&ctx->side_join, cudaEventDisableTiming));
+      }
+      RA_CUDA(cudaEventRecord(ctx->side_fork, s));
+      RA_CUDA(cudaStreamWaitEvent(ctx->side, ctx->side_fork, 0));
+      k_colmean<<<(d + 31) / 32, 256, 0, ctx->side>>>(K, n, d, mean.p);
+      RA_LAUNCH_CHECK();
+      RA_CUDA(cudaEventRecord(ctx->side_join, ctx->side));
+    }
 
     // ---- phase 1 ----
     const uint32_t kt = std::min<uint64_t>(p->k_train, n);
@@ -1259,8 +1274,7 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
     DevBuf<uint32_t> covered(1, s);
     RA_CUDA(cudaMemsetAsync(covered.p, 0, 4, s));
     k_any_covered<<<(n + 255) / 256, 256, 0, s>>>(deg.p, n, covered.p);
-    DevBuf<double> mean(d, s);
-    if (!p->entry_maxnorm) k_colmean<<<(d + 31) / 32, 256, 0, s>>>(K, n, d, mean.p);
+    if (!p->entry_maxnorm) RA_CUDA(cudaStreamWaitEvent(s, ctx->side_join, 0));
     uint32_t any = 0;
     RA_CUDA(cudaMemcpyAsync(&any, covered.p, 4, cudaMemcpyDeviceToHost, s));
     RA_CUDA(cudaStreamSynchronize(s));

@@ -96,6 +96,9 @@ void ra_ctx_destroy(ra_ctx* ctx) {
   if (!ctx) return;
   DeviceGuard dg(ctx->device, true);
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->side) cudaStreamSynchronize(ctx->side), cudaStreamDestroy(ctx->side);
+  if (ctx->side_fork) cudaEventDestroy(ctx->side_fork);
+  if (ctx->side_join) cudaEventDestroy(ctx->side_join);
   delete ctx;
 }
 

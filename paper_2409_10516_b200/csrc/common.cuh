@@ -141,6 +141,10 @@ struct ra_ctx {
   ra::DevBuf<uint8_t> scratch_a;
   ra::DevBuf<uint8_t> scratch_b;
   ra::DevBuf<uint8_t> scratch_c;
+  // a side stream + fork / join events (created on first use): the build's
+  // column mean runs there beside phases 1-3
+  cudaStream_t side = nullptr;
+  cudaEvent_t side_fork = nullptr, side_join = nullptr;
 };
 
 struct ra_kv {
