@@ -269,6 +269,34 @@ __global__ void k_knn_merge(const uint32_t* __restrict__ pid, const double* __re
   for (uint32_t r = lane; r < kt; r += 32) knn[size_t(row) * kt + r] = bi[r];
 }
 
+// exact fallback rows (few): every key's in-order f64 score for each row,
+// as (order-preserving key, id) pairs for a segmented radix sort (stable:
+// equal scores keep ascending ids, the TopKCollector order)
+__device__ __forceinline__ uint64_t okey64(double x) {
+  const uint64_t u = __double_as_longlong(x + 0.0);
+  return (u >> 63) ? ~u : (u | (1ull << 63));
+}
+__global__ void k_exact_scores(const float* __restrict__ Q, const uint32_t* __restrict__ rows,
+                               uint32_t nr, const float* __restrict__ K, uint32_t n, uint32_t d,
+                               uint64_t* __restrict__ sk, uint32_t* __restrict__ sv) {
+  const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (t >= uint64_t(nr) * n) return;
+  const uint32_t r = uint32_t(t / n), j = uint32_t(t % n);
+  sk[t] = okey64(dot_rows(Q + size_t(rows[r]) * d, K + size_t(j) * d, d));
+  sv[t] = j;
+}
+__global__ void k_take_top(const uint32_t* __restrict__ sv, uint32_t nr, uint32_t n, uint32_t kt,
+                           const uint32_t* __restrict__ rows, uint32_t* __restrict__ knn) {
+  const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (t >= uint64_t(nr) * kt) return;
+  const uint32_t r = uint32_t(t / kt), i = uint32_t(t % kt);
+  knn[uint64_t(rows[r]) * kt + i] = sv[uint64_t(r) * n + i];
+}
+__global__ void k_seg_offsets(uint32_t nr, uint32_t n, int* off) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i <= nr) off[i] = int(i * n);
+}
+
 __global__ void k_gather_rows(const float* __restrict__ Q, uint32_t d,
                               const uint32_t* __restrict__ rows, uint32_t nr, float* out) {
   const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
@@ -919,6 +947,16 @@ struct Timer {
     cudaEventCreate(&b);
     cudaEventRecord(a, s);
   }
+  double peek() {  // ms since the last lap, without resetting
+    cudaEvent_t c;
+    cudaEventCreate(&c);
+    cudaEventRecord(c, s);
+    cudaEventSynchronize(c);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, c);
+    cudaEventDestroy(c);
+    return ms;
+  }
   double lap() {
     cudaEventRecord(b, s);
     cudaEventSynchronize(b);
@@ -1128,29 +1166,35 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
       st.knn_rows = nq;
       st.knn_rows_widened = nf;
       if (nf) {
-        DevBuf<float> qf(size_t(nf) * d, s);
-        DevBuf<uint32_t> kf(size_t(nf) * kt, s);
-        k_gather_rows<<<(nf * d + 255) / 256, 256, 0, s>>>(TQ, d, fail.p, nf, qf.p);
-        // few rows: split the keys over C blocks per row tile so the exact
-        // pass fills the GPU, then merge the C partial top-kt lists per row
-        const uint32_t tiles = (nf + KQ - 1) / KQ;
-        uint32_t C = std::max<uint32_t>(1, std::min<uint32_t>(64, 2 * ctx->num_sms / tiles));
-        uint32_t kchunk = (n + C - 1) / C;
-        kchunk = std::max<uint32_t>((kchunk + KK - 1) / KK * KK, (kt + KK - 1) / KK * KK);
-        C = (n + kchunk - 1) / kchunk;
-        uint32_t cb = 1;
-        while (cb < std::max<uint32_t>(2 * kt + KK, C * kt)) cb <<= 1;
-        const size_t rows_pad = size_t(tiles) * KQ;
-        DevBuf<double> bs(size_t(C) * rows_pad * cb, s);
-        DevBuf<uint32_t> bi(size_t(C) * rows_pad * cb, s);
-        DevBuf<uint32_t> pid(size_t(C) * nf * kt, s);
-        DevBuf<double> pscore(size_t(C) * nf * kt, s);
-        k_knn<<<dim3(tiles, C), KTHREADS, 0, s>>>(qf.p, nf, K, n, d, kt, cb, bs.p, bi.p, pid.p,
-                                                   nullptr, pscore.p, C > 1 ? kchunk : 0);
-        k_knn_merge<<<(nf + 7) / 8, 256, 0, s>>>(pid.p, pscore.p, nf, C, kt, cb, bs.p, bi.p,
-                                                 kf.p);
-        k_scatter_knn<<<(nf * kt + 255) / 256, 256, 0, s>>>(kf.p, fail.p, nf, kt, knn.p);
-        RA_LAUNCH_CHECK();
+        // rows the certificate could not vouch for: exact in-order scores of
+        // every key, a stable segmented sort (score desc, id asc) per row, the
+        // first kt kept. Batched so the pair buffers stay bounded.
+        const uint32_t per = std::max<uint32_t>(1, uint32_t((256ull << 20) / (24ull * n)));
+        for (uint32_t r0 = 0; r0 < nf; r0 += per) {
+          const uint32_t nr = std::min(per, nf - r0);
+          const uint64_t tot = uint64_t(nr) * n;
+          DevBuf<uint64_t> k1(tot, s), k2(tot, s);
+          DevBuf<uint32_t> v1(tot, s), v2(tot, s);
+          DevBuf<int> off(nr + 1, s);
+          k_exact_scores<<<uint32_t((tot + 255) / 256), 256, 0, s>>>(TQ, fail.p + r0, nr, K, n, d,
+                                                                     k1.p, v1.p);
+          k_seg_offsets<<<(nr + 1 + 255) / 256, 256, 0, s>>>(nr, n, off.p);
+          size_t tb = 0;
+          cub::DeviceSegmentedRadixSort::SortPairsDescending(nullptr, tb, k1.p, k2.p, v1.p, v2.p,
+                                                             int64_t(tot), int64_t(nr), off.p,
+                                                             off.p + 1, 0, 64, s);
+          DevBuf<uint8_t> tmp(tb, s);
+          RA_CUDA(cub::DeviceSegmentedRadixSort::SortPairsDescending(
+              tmp.p, tb, k1.p, k2.p, v1.p, v2.p, int64_t(tot), int64_t(nr), off.p, off.p + 1, 0, 64,
+              s));
+          k_take_top<<<uint32_t((uint64_t(nr) * kt + 255) / 256), 256, 0, s>>>(v2.p, nr, n, kt,
+                                                                               fail.p + r0, knn.p);
+          RA_LAUNCH_CHECK();
+        }
+        if (std::getenv("RA_KNN_TRACE")) {
+          RA_CUDA(cudaStreamSynchronize(s));
+          fprintf(stderr, "knn: exact fallback for %u rows done at %.2f ms\n", nf, tm.peek());
+        }
       }
     } else if (nq) {
       uint32_t cb = 1;
