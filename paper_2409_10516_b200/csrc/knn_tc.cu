@@ -619,7 +619,7 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
   };
   const uint64_t mt = (nq + TM - 1) / TM, nt = (n + TN - 1) / TN;
   constexpr uint32_t cb = 2048;     // survivor buffer per row
-  constexpr uint32_t msamp = 2048;  // strided key sample for the threshold
+  constexpr uint32_t msamp = 1024;  // strided key sample for the threshold
   constexpr uint32_t target = 640;  // expected survivors per row (>= kt w.h.p.)
   DevBuf<uint16_t> A(mt * TM * K3, s), B(nt * TN * K3, s);
   {
