@@ -88,9 +88,11 @@ ra_status ra_ctx_synchronize(ra_ctx* ctx);
 ra_status ra_host_alloc(size_t bytes, void** out);
 void ra_host_free(void* p);
 /* Graph-search kernel variant for this ctx (overrides RA_SEARCH_KERNEL):
- * "auto" (latency mode up to 2 x SMs queries, then throughput mode),
- * "lat", "tp", "tps" (throughput, shared-memory visited bits + TMA row
- * tiles), "tpr" (throughput, register rows), "cta", "warp"; NULL = default.
+ * "auto" (latency mode up to 2 x SMs queries, then throughput mode: DUO
+ * while the batch fits one wave, else TPS, else TP), "lat", "duo"
+ * (throughput, a commit warp + an expansion warp per query), "tp", "tps"
+ * (throughput, shared-memory visited bits + TMA row tiles), "tpr"
+ * (throughput, register rows), "cta", "warp"; NULL = default.
  * Every variant returns identical results. Engines read it at creation. */
 ra_status ra_ctx_set_search_kernel(ra_ctx* ctx, const char* name);
 

@@ -37,6 +37,14 @@
 // adjacency row, TMA the unvisited neighbours' key rows into their tile,
 // run the exact chains, publish the packet; then chain greedily into the
 // best new neighbour (the likely next top) while it ranks among the heads.
+//
+// Throughput modes reuse the commit code with one query per warp (TP / TPS:
+// inline expansions) or per warp PAIR (DUO): the commit warp learns the next
+// top right after reading a packet (the best of the packet's new children
+// >= thr and the frontier after the pop - the visit only inserts those
+// children, a compaction can only end the search), starts that expansion
+// (adjacency row, filter, L2 prefetch of the new rows) and posts it, then
+// visits; the expansion warp runs the exact chains and returns the packet.
 #include <cfloat>
 #include <cstdlib>
 
