@@ -97,6 +97,33 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_c, uint64_t da, uint64_t 
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(tmem_c),
       "l"(da), "l"(db), "r"(idesc), "r"(accum));
 }
+// arrive on `bar` at the same shared offset in every CTA of `mask` (cluster)
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+// bulk copy into the same shared offset of every CTA of `mask`, completing
+// bytes on each one's barrier at `bar`'s offset
+__device__ __forceinline__ void bulk_g2s_mc(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -166,12 +193,19 @@ struct TcArgs {
   uint32_t* cnt_out;     // [nq]; cb + 1 = overflow
 };
 
+// MC: launched in clusters of 2 (two query tiles): each CTA's producer loads
+// half of every B stage and multicasts it to both, so B crosses L2 once per
+// pair; a stage is refilled only after BOTH CTAs' MMAs released it (the
+// commits multicast to both empty barriers, which count 2 arrivals)
+template <bool MC>
 __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t K3 = a.K3, nstages_k = K3 / KS;
   const uint32_t ntiles = (a.n + TN - 1) / TN;
   const uint64_t m0 = uint64_t(blockIdx.x) * TM;
+  const uint32_t mt_real = uint32_t((a.nq + TM - 1) / TM);  // (MC pads the grid to even)
+  const uint32_t a_tile = min(blockIdx.x, mt_real - 1);
   // layout: A tile | B stages | barriers | tmem slot
   uint8_t* sA = smem;
   const uint32_t a_bytes = TM * K3 * 2;
@@ -188,7 +222,7 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < NSTAGE; ++s) {
       mbar_init_n(full + s, 1);
-      mbar_init_n(empty + s, 1);
+      mbar_init_n(empty + s, MC ? 2 : 1);
     }
     mbar_init_n(a_full, 1);
     for (int b = 0; b < 2; ++b) {
@@ -205,6 +239,7 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
   }
   fence_before();
   __syncthreads();
+  if constexpr (MC) cluster_sync_all();  // the peer's barriers exist before any multicast
   fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -212,7 +247,7 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
     // ---- TMA producer ----
     if (lane == 0) {
       mbar_arrive_expect_tx(a_full, a_bytes);
-      const uint8_t* gA = reinterpret_cast<const uint8_t*>(a.A) + size_t(blockIdx.x) * a_bytes;
+      const uint8_t* gA = reinterpret_cast<const uint8_t*>(a.A) + size_t(a_tile) * a_bytes;
       for (uint32_t off = 0; off < a_bytes; off += 32768)
         bulk_g2s(sA + off, gA + off, min(32768u, a_bytes - off), a_full);
       uint32_t it = 0;
@@ -223,7 +258,12 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
           mbar_arrive_expect_tx(full + slot, b_stage);
           const uint8_t* gB = reinterpret_cast<const uint8_t*>(a.B) +
                               (size_t(t) * nstages_k + s) * b_stage;
-          bulk_g2s(sB + slot * b_stage, gB, b_stage, full + slot);
+          if constexpr (MC) {
+            const uint32_t h = b_stage / 2, off = cluster_rank() * h;
+            bulk_g2s_mc(sB + slot * b_stage + off, gB + off, h, full + slot, 0x3);
+          } else {
+            bulk_g2s(sB + slot * b_stage, gB, b_stage, full + slot);
+          }
         }
     }
   } else if (warp == EPI_WARPS + 1) {
@@ -253,7 +293,8 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
             const uint64_t db = smem_desc(b_base + 2 * kk * b_lbo, b_lbo, sbo);
             mma_bf16(tc, da, db, idesc, (s | kk) ? 1u : 0u);
           }
-          mma_commit(empty + slot);  // frees the stage when these MMAs finish
+          if constexpr (MC) mma_commit_mc(empty + slot, 0x3);  // (both CTAs' producers)
+          else mma_commit(empty + slot);  // frees the stage when these MMAs finish
         }
         mma_commit(t_full + buf);    // accumulator ready for the epilogue
       }
@@ -311,9 +352,43 @@ __global__ void __launch_bounds__(KNN_THREADS, 1) k_knn_tc(TcArgs a) {
   }
   fence_before();
   __syncthreads();
+  if constexpr (MC) cluster_sync_all();  // no multicast or remote arrive still in flight
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem)
                  : "memory");
+}
+
+// launch k_knn_tc: clusters of two query tiles with B multicast unless
+// RA_KNN_MC=0 (the grid padded to even; the pad CTA's rows are past nq)
+void launch_knn_tc(const TcArgs& t, uint64_t mt, size_t smem, cudaStream_t s) {
+  static const bool mc = [] {
+    const char* v = std::getenv("RA_KNN_MC");
+    return !(v && v[0] == '0');
+  }();
+  if (!mc) {
+    k_knn_tc<false><<<uint32_t(mt), KNN_THREADS, smem, s>>>(t);
+    RA_LAUNCH_CHECK();
+    return;
+  }
+  static bool attr = false;
+  if (!attr) {
+    RA_CUDA(cudaFuncSetAttribute(k_knn_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(uint32_t((mt + 1) / 2 * 2));
+  cfg.blockDim = dim3(KNN_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  RA_CUDA(cudaLaunchKernelEx(&cfg, k_knn_tc<true>, t));
 }
 
 // ---- per-row threshold from the sample pass: r-th largest S~ ------------------
@@ -632,7 +707,8 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
   DevBuf<float> bufS(nq * cb, s), thr(nq, s);
   DevBuf<uint32_t> bufI(nq * cb, s), cnt(nq, s);
   const size_t smem = size_t(TM) * K3 * 2 + NSTAGE * TN * KS * 2 + 256;
-  RA_CUDA(cudaFuncSetAttribute(k_knn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  RA_CUDA(cudaFuncSetAttribute(k_knn_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -645,7 +721,7 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
     k_gather_sample<<<(msamp * d + 255) / 256, 256, 0, s>>>(K, n, d, msamp, ks.p);
     k_split<<<(msamp * d + 255) / 256, 256, 0, s>>>(ks.p, msamp, d, TN, msamp / TN, 0, Bs.p);
     TcArgs t1{A.p, Bs.p, nq, msamp, K3, cb, nullptr, bufS.p, nullptr, cnt.p};
-    k_knn_tc<<<uint32_t(mt), KNN_THREADS, smem, s>>>(t1);
+    launch_knn_tc(t1, mt, smem, s);
     const uint32_t r = std::max<uint32_t>(1, uint32_t((uint64_t(target) * msamp + n - 1) / n));
     if (r >= 8 || n <= 8u * msamp) {
       k_select_thr<<<uint32_t((nq + 7) / 8), 256, 0, s>>>(bufS.p, cnt.p, nq, cb, r, thr.p);
@@ -665,7 +741,7 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
       k_split<<<uint32_t((uint64_t(m2) * d + 255) / 256), 256, 0, s>>>(ks2.p, m2, d, TN, m2 / TN, 0,
                                                                       Bs2.p);
       TcArgs t1b{A.p, Bs2.p, nq, m2, K3, cb, thr.p, bufS.p, nullptr, cnt.p};
-      k_knn_tc<<<uint32_t(mt), KNN_THREADS, smem, s>>>(t1b);
+      launch_knn_tc(t1b, mt, smem, s);
       const uint32_t r2 = std::max<uint32_t>(1, uint32_t((uint64_t(target) * m2 + n - 1) / n));
       k_select_thr<<<uint32_t((nq + 7) / 8), 256, 0, s>>>(bufS.p, cnt.p, nq, cb, r2, thr2.p);
       RA_CUDA(cudaMemcpyAsync(thr.p, thr2.p, nq * 4, cudaMemcpyDeviceToDevice, s));
@@ -675,7 +751,7 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
   tlap("threshold");
   // pass 2: every key, keep S~ > threshold
   TcArgs t2{A.p, B.p, nq, n, K3, cb, sampled ? thr.p : nullptr, bufS.p, bufI.p, cnt.p};
-  k_knn_tc<<<uint32_t(mt), KNN_THREADS, smem, s>>>(t2);
+  launch_knn_tc(t2, mt, smem, s);
   RA_LAUNCH_CHECK();
   cudaEventRecord(e1, s);
   DevBuf<unsigned long long> kmax(1, s);
