@@ -370,12 +370,9 @@ void launch_knn_tc(const TcArgs& t, uint64_t mt, size_t smem, cudaStream_t s) {
     RA_LAUNCH_CHECK();
     return;
   }
-  static bool attr = false;
-  if (!attr) {
-    RA_CUDA(cudaFuncSetAttribute(k_knn_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    attr = true;
-  }
+  // (per device, like the single-CTA path's attribute)
+  RA_CUDA(cudaFuncSetAttribute(k_knn_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(uint32_t((mt + 1) / 2 * 2));
   cfg.blockDim = dim3(KNN_THREADS);
