@@ -984,11 +984,14 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
     // and returns the packet while this warp visits the previous one.
     uint32_t dseq = 0;
     uint32_t spec_v = kSentinel;  // DUO: this lane's neighbour of the speculated top
+    uint32_t spec_node = kSentinel, spec_row = kSentinel;  // (its id and adjacency entry)
     auto duo_issue = [&](uint32_t p) {
       ++dseq;
       if (p != kSentinel) {
         const uint64_t ti0 = clock64();
-        const uint32_t v = lane < M ? __ldg(adj + size_t(p) * M + lane) : kSentinel;
+        // the speculated runner-up's adjacency row is already in registers
+        const uint32_t v = p == spec_node ? spec_row
+                                          : lane < M ? __ldg(adj + size_t(p) * M + lane) : kSentinel;
         const uint32_t grp = __match_any_sync(kFull, v);
         c_usp += clock64() - ti0;  // (dbg: the adjacency-row wait)
         const bool isnew = v != kSentinel && uint32_t(__ffs(grp) - 1) == lane &&
@@ -1183,6 +1186,7 @@ __global__ void __launch_bounds__(TP ? (DUO ? kDuoPairs * 64 : kTW * 32) : kPW *
             if (nFO && fo_id != nid && better(fo_k, fo_id, k2, i2)) i2 = fo_id;
             spec_v = (i2 != kSentinel && lane < M) ? __ldg(adj + size_t(i2) * M + lane)
                                                    : 0xFFFFFFFFu;
+            spec_node = i2, spec_row = spec_v;
           }
         } else {
           expand(tid, cv, cx, cand, cm);
