@@ -389,13 +389,41 @@ __device__ void warp_bitonic_asc(double* m, uint32_t* v, uint32_t n_pow2, uint32
   }
 }
 
+// prune work order: candidate count per node (keys for a descending sort);
+// nodes without candidates get their empty row here and are counted out
+__global__ void k_prune_order(const uint64_t* __restrict__ off, uint32_t n, uint32_t M,
+                              uint32_t* key, uint32_t* val, uint32_t* adj, uint32_t* deg,
+                              uint32_t* n_active) {
+  const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  const uint64_t c = off[u + 1] - off[u];
+  key[u] = c > 0xFFFFFFFFull ? 0xFFFFFFFFu : uint32_t(c);
+  val[u] = u;
+  if (c) {
+    atomicAdd(n_active, 1u);
+  } else {
+    deg[u] = 0;
+    for (uint32_t j = 0; j < M; ++j) adj[size_t(u) * M + j] = 0xFFFFFFFFu;
+  }
+}
+
+#ifdef RA_PRUNE_PROF
+// (profiling aid) score+sort / occlusion / fill cycles, candidates tested,
+// ballot rounds, pair tests, nodes that filled M, kept sum, exact tests
+__device__ unsigned long long g_prune_prof[9];
+#define PPROF(i, v) \
+  do { if (lane == 0) atomicAdd(&g_prune_prof[i], (unsigned long long)(v)); } while (0)
+#else
+#define PPROF(i, v) do {} while (0)
+#endif
+
 __global__ void __launch_bounds__(PWARPS * 32)
     k_prune(const float* __restrict__ keys, uint32_t n, uint32_t d,
             const double* __restrict__ norms, const uint64_t* __restrict__ edges,
             const uint64_t* __restrict__ off, const uint32_t* __restrict__ nodes,
             uint32_t n_nodes, uint32_t M, uint32_t efc, int euclid, double* gm, uint32_t* gv,
             uint64_t g_stride, uint32_t* __restrict__ adj, uint32_t* __restrict__ deg,
-            uint32_t* big_nodes, uint32_t* big_count) {
+            uint32_t* big_nodes, uint32_t* big_count, uint32_t* queue) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t wid = blockIdx.x * PWARPS + warp;
@@ -406,7 +434,17 @@ __global__ void __launch_bounds__(PWARPS * 32)
                  size_t(warp) * PCAP;
   uint32_t* kept = reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(smem) + PWARPS * PCAP) +
                    PWARPS * PCAP + size_t(warp) * M;
-  for (uint32_t idx = wid; idx < n_nodes; idx += gridDim.x * PWARPS) {
+  // queue != null: `nodes` is ordered by candidate count, descending, and
+  // warps take the next node from queue[0] until queue[1] (largest first:
+  // the hubs start at once and the small nodes fill in behind them)
+  const uint32_t n_work = queue ? queue[1] : n_nodes;
+  for (uint32_t it = 0;; ++it) {
+    uint32_t idx = wid + it * gridDim.x * PWARPS;
+    if (queue) {
+      if (lane == 0) idx = atomicAdd(queue, 1u);
+      idx = __shfl_sync(kFull, idx, 0);
+    }
+    if (idx >= n_work) break;
     const uint32_t u = nodes ? nodes[idx] : idx;
     const uint64_t c0 = off[u], c1 = off[u + 1];
     const uint32_t c = uint32_t(c1 - c0);
@@ -417,6 +455,10 @@ __global__ void __launch_bounds__(PWARPS * 32)
     }
     double* bm = sm;
     uint32_t* bv = sv;
+#ifdef RA_PRUNE_PROF
+    long long t0 = clock64();
+    uint64_t n_tests = 0, n_rounds = 0, n_cand = 0;
+#endif
     const float* ku = keys + size_t(u) * d;
     auto score = [&](uint32_t i, uint32_t at) {  // candidate i's m_uv into slot `at`
       const uint32_t v = uint32_t(edges[c0 + i] & dst_mask);
@@ -462,10 +504,19 @@ __global__ void __launch_bounds__(PWARPS * 32)
     }
     const uint32_t no = c < efc ? c : efc;
     uint32_t kn = 0;
+#ifdef RA_PRUNE_PROF
+    long long t1 = clock64();
+    PPROF(0, t1 - t0);
+#endif
     for (uint32_t i = 0; i < no && kn < M; ++i) {
       const uint32_t v = bv[i];
       const double m_uv = bm[i];
       bool occl = false;
+#ifdef RA_PRUNE_PROF
+      ++n_cand;
+      n_tests += kn;
+      n_rounds += kn ? 1 : 0;
+#endif
       for (uint32_t j0 = 0; j0 < kn; j0 += 32) {
         const uint32_t j = j0 + lane;
         bool o = false;
@@ -488,6 +539,9 @@ __global__ void __launch_bounds__(PWARPS * 32)
             else if (ma - em > m_uv) decided = true;
           }
           if (!decided) {
+#ifdef RA_PRUNE_PROF
+            atomicAdd(&g_prune_prof[8], 1ull);
+#endif
             const double ip = dot_rows(kv_, kw_, d);
             const double m_vw = euclid ? nv + nw - 2.0 * ip : -ip;
             o = m_vw < m_uv;
@@ -504,6 +558,15 @@ __global__ void __launch_bounds__(PWARPS * 32)
         __syncwarp();
       }
     }
+#ifdef RA_PRUNE_PROF
+    long long t2 = clock64();
+    PPROF(1, t2 - t1);
+    PPROF(3, n_cand);
+    PPROF(4, n_rounds);
+    PPROF(5, n_tests);
+    PPROF(6, kn == M ? 1 : 0);
+    PPROF(7, kn);
+#endif
     // fill from the ordered list (:196-201)
     for (uint32_t i = 0; i < no && kn < M; ++i) {
       const uint32_t v = bv[i];
@@ -524,6 +587,9 @@ __global__ void __launch_bounds__(PWARPS * 32)
     for (uint32_t j = lane; j < M; j += 32) adj[size_t(u) * M + j] = j < kn ? kept[j] : kSentinel;
     if (lane == 0) deg[u] = kn;
     __syncwarp();
+#ifdef RA_PRUNE_PROF
+    PPROF(2, clock64() - t2);
+#endif
   }
 }
 
@@ -1283,10 +1349,30 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
               (unsigned long long)sum_big);
     }
     Timer ptm(s);
-    k_prune<<<pgrid, PWARPS * 32, psmem, s>>>(K, n, d, norms.p, edges.p, off.p, nullptr, n, M,
-                                             p->ef_construction, !p->prune_inner_product, nullptr,
-                                             nullptr, 0, g->adj.p, deg.p, big.p, big_cnt.p);
-    RA_LAUNCH_CHECK();
+    {
+      // largest-first dynamic schedule: nodes sorted by candidate count
+      // (descending), one resident wave of warps pulling from a counter
+      DevBuf<uint32_t> k1(n, s), k2(n, s), v1(n, s), order(n, s), queue(2, s);
+      RA_CUDA(cudaMemsetAsync(queue.p, 0, 8, s));
+      k_prune_order<<<(n + 255) / 256, 256, 0, s>>>(off.p, n, M, k1.p, v1.p, g->adj.p, deg.p,
+                                                    queue.p + 1);
+      RA_LAUNCH_CHECK();
+      size_t tb = 0;
+      cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, k1.p, k2.p, v1.p, order.p, int64_t(n), 0,
+                                                32, s);
+      DevBuf<uint8_t> tmp(tb, s);
+      RA_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp.p, tb, k1.p, k2.p, v1.p, order.p,
+                                                        int64_t(n), 0, 32, s));
+      int per_sm = 0;
+      RA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_prune, PWARPS * 32, psmem));
+      const uint32_t qgrid = std::max<uint32_t>(1, std::min<uint32_t>(
+                                                       pgrid, uint32_t(std::max(per_sm, 1)) * ctx->num_sms));
+      k_prune<<<qgrid, PWARPS * 32, psmem, s>>>(K, n, d, norms.p, edges.p, off.p, order.p, n, M,
+                                               p->ef_construction, !p->prune_inner_product, nullptr,
+                                               nullptr, 0, g->adj.p, deg.p, big.p, big_cnt.p,
+                                               queue.p);
+      RA_LAUNCH_CHECK();
+    }
     uint32_t nbig = 0;
     RA_CUDA(cudaMemcpyAsync(&nbig, big_cnt.p, 4, cudaMemcpyDeviceToHost, s));
     RA_CUDA(cudaStreamSynchronize(s));
@@ -1305,13 +1391,27 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
       DevBuf<uint32_t> gv(size_t(ggrid) * PWARPS * p2, s);
       k_prune<<<ggrid, PWARPS * 32, psmem, s>>>(K, n, d, norms.p, edges.p, off.p, big.p, nbig, M,
                                                p->ef_construction, !p->prune_inner_product, gm.p,
-                                               gv.p, p2, g->adj.p, deg.p, nullptr, nullptr);
+                                               gv.p, p2, g->adj.p, deg.p, nullptr, nullptr, nullptr);
       RA_LAUNCH_CHECK();
     }
     edges.reset();
     if (ptrace)
       fprintf(stderr, "prune: %.2f ms (second pass nodes %u), allocations %.2f ms\n", ptm.lap(), nbig,
               alloc_ms);
+#ifdef RA_PRUNE_PROF
+    {
+      unsigned long long pp[9];
+      RA_CUDA(cudaMemcpyFromSymbol(pp, g_prune_prof, sizeof(pp)));
+      fprintf(stderr,
+              "prune prof (per node): score+sort %.0f occl %.0f fill %.0f cycles; tested %.1f rounds "
+              "%.1f pairs %.1f; filled M %.3f kept %.1f exact %.2f\n",
+              pp[0] / double(n), pp[1] / double(n), pp[2] / double(n), pp[3] / double(n),
+              pp[4] / double(n), pp[5] / double(n), pp[6] / double(n), pp[7] / double(n),
+              pp[8] / double(n));
+      const unsigned long long z[9] = {};
+      RA_CUDA(cudaMemcpyToSymbol(g_prune_prof, z, sizeof(z)));
+    }
+#endif
     st.ms_prune = tm.lap();
 
     // ---- entry point ----
