@@ -110,6 +110,32 @@ def test_build_on_ood_workload_hubs(port):
     assert g.build_stats.candidate_edges > 0
 
 
+def test_edge_dedup_set_matches_sort_path():
+    """Phase 2's proposal dedup (open-addressing set + compaction + sort of
+    the survivors) gives the same graph as the global sort + unique, and a
+    set too small for the proposals falls back to that sort path."""
+    ra = _ra()
+    import torch
+    from paper_2409_10516_b200.workload import WorkloadSpec, generate_group
+    w = generate_group(WorkloadSpec(n_ctx=32768, d_model=256, d_head=128, n_heads=4,
+                                    n_kv_groups=1, seed=29, n_decode=1), 0, "cuda")
+    kv = ra.KVGroup(w["keys"], w["values"])
+    bp = ra.OODGraphBuildParams(128, 24, 256, 8)
+    blobs, cand = [], []
+    for env in ({}, {"RA_EDGES_SORT": "1"}, {"RA_EDGES_HASH_LG": "10"}):
+        os.environ.update(env)
+        try:
+            g = ra.ood_build(kv, w["prefill_q"][0], bp)
+        finally:
+            for k in env:
+                del os.environ[k]
+        blobs.append(g.serialize())
+        cand.append(g.build_stats.candidate_edges)
+    torch.cuda.synchronize()
+    assert cand[0] > 1024 and cand[0] == cand[1] == cand[2]
+    assert blobs[0] == blobs[1] == blobs[2]
+
+
 def test_hand_built_line_graph():
     # test_index_oodgraph.cpp:71-111, 207-216
     ra = _ra()
