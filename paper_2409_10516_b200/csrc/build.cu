@@ -1333,45 +1333,55 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
     const int end_bit = int(2 * edge_bits(n));
     bool hashed = false;
     if (total && !std::getenv("RA_EDGES_SORT")) {
-      // dedup set sized for ~64 unique proposals per key (load <= ~0.5 at
-      // the bench shape), capped by the proposal count
+      // dedup set sized for ~128 distinct proposals per key (the bench
+      // shape's heads have 2-7M distinct pairs at 128K: load <= ~0.4), capped
+      // by the proposal count; on overflow it is rebuilt 4x larger once
       uint32_t lg = 10;
-      while (lg < 40 && (1ull << lg) < std::min<uint64_t>(2 * total, uint64_t(n) * 64)) ++lg;
+      while (lg < 40 && (1ull << lg) < std::min<uint64_t>(2 * total, uint64_t(n) * 128)) ++lg;
       if (const char* e = std::getenv("RA_EDGES_HASH_LG"))  // (tests: force the overflow path)
         lg = std::max(4, std::min(40, std::atoi(e)));
-      DevBuf<unsigned long long> tab(1ull << lg, s);
-      DevBuf<uint32_t> ovf(1, s);
-      RA_CUDA(cudaMemsetAsync(tab.p, 0xFF, (1ull << lg) * 8, s));
-      RA_CUDA(cudaMemsetAsync(ovf.p, 0, 4, s));
-      const uint64_t threads = uint64_t(nq) * (kt - 1);
-      k_proposals_hash<<<uint32_t((threads + 255) / 256), 256, 0, s>>>(
-          knn.p, nq, kt, p->edge_window, edge_bits(n), tab.p, lg, ovf.p);
-      RA_LAUNCH_CHECK();
-      edges2.alloc(1ull << lg, s);
-      DevBuf<uint64_t> nsel(1, s);
-      size_t tb = 0;
-      cub::DeviceSelect::If(nullptr, tb, reinterpret_cast<uint64_t*>(tab.p), edges2.p, nsel.p,
-                            int64_t(1ull << lg), HNotEmpty(), s);
-      DevBuf<uint8_t> tmp(tb, s);
-      RA_CUDA(cub::DeviceSelect::If(tmp.p, tb, reinterpret_cast<uint64_t*>(tab.p), edges2.p, nsel.p,
-                                    int64_t(1ull << lg), HNotEmpty(), s));
-      uint32_t h_ovf = 0;
-      RA_CUDA(cudaMemcpyAsync(&ne, nsel.p, 8, cudaMemcpyDeviceToHost, s));
-      RA_CUDA(cudaMemcpyAsync(&h_ovf, ovf.p, 4, cudaMemcpyDeviceToHost, s));
-      RA_CUDA(cudaStreamSynchronize(s));
-      if (!h_ovf) {
-        hashed = true;
-        tab.reset();
-        edges.alloc(std::max<uint64_t>(ne, 1), s);
-        if (ne) {
-          size_t tb2 = 0;
-          cub::DeviceRadixSort::SortKeys(nullptr, tb2, edges2.p, edges.p, (int64_t)ne, 0, end_bit, s);
-          DevBuf<uint8_t> tmp2(tb2, s);
-          RA_CUDA(cub::DeviceRadixSort::SortKeys(tmp2.p, tb2, edges2.p, edges.p, (int64_t)ne, 0,
-                                                 end_bit, s));
+      for (int attempt = 0; !hashed; ++attempt) {
+        DevBuf<unsigned long long> tab(1ull << lg, s);
+        DevBuf<uint32_t> ovf(1, s);
+        RA_CUDA(cudaMemsetAsync(tab.p, 0xFF, (1ull << lg) * 8, s));
+        RA_CUDA(cudaMemsetAsync(ovf.p, 0, 4, s));
+        const uint64_t threads = uint64_t(nq) * (kt - 1);
+        k_proposals_hash<<<uint32_t((threads + 255) / 256), 256, 0, s>>>(
+            knn.p, nq, kt, p->edge_window, edge_bits(n), tab.p, lg, ovf.p);
+        RA_LAUNCH_CHECK();
+        edges2.alloc(1ull << lg, s);
+        DevBuf<uint64_t> nsel(1, s);
+        size_t tb = 0;
+        cub::DeviceSelect::If(nullptr, tb, reinterpret_cast<uint64_t*>(tab.p), edges2.p, nsel.p,
+                              int64_t(1ull << lg), HNotEmpty(), s);
+        DevBuf<uint8_t> tmp(tb, s);
+        RA_CUDA(cub::DeviceSelect::If(tmp.p, tb, reinterpret_cast<uint64_t*>(tab.p), edges2.p,
+                                      nsel.p, int64_t(1ull << lg), HNotEmpty(), s));
+        uint32_t h_ovf = 0;
+        RA_CUDA(cudaMemcpyAsync(&ne, nsel.p, 8, cudaMemcpyDeviceToHost, s));
+        RA_CUDA(cudaMemcpyAsync(&h_ovf, ovf.p, 4, cudaMemcpyDeviceToHost, s));
+        RA_CUDA(cudaStreamSynchronize(s));
+        if (std::getenv("RA_PRUNE_TRACE"))
+          fprintf(stderr, "edges: %llu proposals, set 2^%u slots, %llu distinct%s\n",
+                  (unsigned long long)total, lg, (unsigned long long)ne, h_ovf ? " (overflow)" : "");
+        if (!h_ovf) {
+          hashed = true;
+          tab.reset();
+          edges.alloc(std::max<uint64_t>(ne, 1), s);
+          if (ne) {
+            size_t tb2 = 0;
+            cub::DeviceRadixSort::SortKeys(nullptr, tb2, edges2.p, edges.p, (int64_t)ne, 0, end_bit,
+                                           s);
+            DevBuf<uint8_t> tmp2(tb2, s);
+            RA_CUDA(cub::DeviceRadixSort::SortKeys(tmp2.p, tb2, edges2.p, edges.p, (int64_t)ne, 0,
+                                                   end_bit, s));
+          }
+        } else {
+          ne = 0;
+          edges2.reset();
+          if (attempt >= 1 || (1ull << (lg + 2)) > 2 * total || lg + 2 > 36) break;
+          lg += 2;
         }
-      } else {
-        ne = 0;
       }
     }
     if (total && !hashed) {

@@ -11,12 +11,13 @@ def main():
     ap.add_argument("--n", type=int, default=32768)
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--heads", type=int, default=1, help="distinct prefill-query sets (of 4)")
+    ap.add_argument("--group", type=int, default=0, help="KV group of the 8-group workload")
     a = ap.parse_args()
     import torch
     import paper_2409_10516_b200 as ra
     from paper_2409_10516_b200.workload import WorkloadSpec, generate_group
-    w = generate_group(WorkloadSpec(n_ctx=a.n, d_model=256, d_head=128, n_heads=4, n_kv_groups=1,
-                                    seed=7, n_decode=1), 0, "cuda")
+    w = generate_group(WorkloadSpec(n_ctx=a.n, d_model=256, d_head=128, n_heads=32, n_kv_groups=8,
+                                    seed=7, n_decode=1), a.group, "cuda")
     kv = ra.KVGroup(w["keys"], w["values"])
     torch.cuda.synchronize()
     for r in range(a.reps):
