@@ -283,7 +283,95 @@ __global__ void k_exact_scores(const float* __restrict__ Q, const uint32_t* __re
   if (t >= uint64_t(nr) * n) return;
   const uint32_t r = uint32_t(t / n), j = uint32_t(t % n);
   sk[t] = okey64(dot_rows(Q + size_t(rows[r]) * d, K + size_t(j) * d, d));
-  sv[t] = j;
+  if (sv) sv[t] = j;
+}
+
+// Block per exact-fallback row: radix-select the kt-th largest key of the
+// row's n keys (8 bits per pass, warp-aggregated histogram), gather the keys
+// >= it and bitonic-sort them by (key desc, id asc) in shared memory: the
+// first kt are exactly the stable segmented sort's first kt. Rows with more
+// than XCAP keys >= the kt-th (mass ties) are listed in ovf_rows (query ids)
+// for the segmented sort.
+constexpr uint32_t XT = 1024, XCAP = 2048;
+__global__ void __launch_bounds__(XT)
+    k_exact_topk(const uint64_t* __restrict__ sk, uint32_t n, uint32_t kt,
+                 const uint32_t* __restrict__ rows, uint32_t* __restrict__ knn,
+                 uint32_t* __restrict__ ovf_rows, uint32_t* __restrict__ n_ovf, uint32_t cap) {
+  __shared__ uint32_t hist[256];
+  __shared__ uint64_t ck[XCAP];
+  __shared__ uint32_t ci[XCAP];
+  __shared__ uint32_t s_digit, s_need, s_cnt;
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
+  const uint64_t* kr = sk + uint64_t(blockIdx.x) * n;
+  uint64_t prefix = 0, pmask = 0;
+  uint32_t need = kt;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (uint32_t b = tid; b < 256; b += XT) hist[b] = 0;
+    __syncthreads();
+    for (uint32_t i0 = 0; i0 < n; i0 += XT) {
+      const uint32_t i = i0 + tid;
+      const uint64_t k = i < n ? kr[i] : 0;
+      const bool in = i < n && (k & pmask) == prefix;
+      const uint32_t dg = in ? uint32_t(k >> shift) & 255u : 256u;
+      const uint32_t peers = __match_any_sync(kFull, dg);
+      if (in && lane == uint32_t(__ffs(peers) - 1)) atomicAdd(&hist[dg], uint32_t(__popc(peers)));
+    }
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t acc = 0;
+      for (int b = 255; b >= 0; --b) {
+        if (acc + hist[b] >= need) {
+          s_digit = uint32_t(b);
+          s_need = need - acc;
+          break;
+        }
+        acc += hist[b];
+      }
+    }
+    __syncthreads();
+    prefix |= uint64_t(s_digit) << shift;
+    pmask |= 0xFFull << shift;
+    need = s_need;
+    __syncthreads();
+  }
+  if (tid == 0) s_cnt = 0;
+  __syncthreads();
+  for (uint32_t i = tid; i < n; i += XT) {
+    const uint64_t k = kr[i];
+    if (k >= prefix) {
+      const uint32_t at = atomicAdd(&s_cnt, 1u);
+      if (at < XCAP) ck[at] = k, ci[at] = i;
+    }
+  }
+  __syncthreads();
+  const uint32_t cnt = s_cnt;
+  if (cnt > cap) {
+    if (tid == 0) ovf_rows[atomicAdd(n_ovf, 1u)] = rows[blockIdx.x];
+    return;
+  }
+  uint32_t p2 = 1;
+  while (p2 < cnt) p2 <<= 1;
+  for (uint32_t i = cnt + tid; i < p2; i += XT) ck[i] = 0, ci[i] = 0xFFFFFFFFu;
+  __syncthreads();
+  for (uint32_t k = 2; k <= p2; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = tid; i < p2; i += XT) {
+        const uint32_t l = i ^ j;
+        if (l > i) {
+          const uint64_t ki = ck[i], kl = ck[l];
+          const uint32_t ii = ci[i], il = ci[l];
+          const bool l_first = kl > ki || (kl == ki && il < ii);
+          const bool i_first = ki > kl || (ki == kl && ii < il);
+          if ((i & k) == 0 ? l_first : i_first) {
+            ck[i] = kl, ck[l] = ki;
+            ci[i] = il, ci[l] = ii;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (uint32_t j = tid; j < kt; j += XT) knn[uint64_t(rows[blockIdx.x]) * kt + j] = ci[j];
 }
 __global__ void k_take_top(const uint32_t* __restrict__ sv, uint32_t nr, uint32_t n, uint32_t kt,
                            const uint32_t* __restrict__ rows, uint32_t* __restrict__ knn) {
@@ -1272,29 +1360,56 @@ extern "C" ra_status ra_graph_build(ra_ctx* ctx, ra_kv* kv, const float* train_q
       st.knn_rows_widened = nf;
       if (nf) {
         // rows the certificate could not vouch for: exact in-order scores of
-        // every key, a stable segmented sort (score desc, id asc) per row, the
-        // first kt kept. Batched so the pair buffers stay bounded.
+        // every key, then the row's top kt by a block radix select +
+        // shared-memory sort (k_exact_topk); rows with mass ties past its
+        // capacity take a stable segmented sort (score desc, id asc). Batched
+        // so the score buffers stay bounded.
         const uint32_t per = std::max<uint32_t>(1, uint32_t((256ull << 20) / (24ull * n)));
-        for (uint32_t r0 = 0; r0 < nf; r0 += per) {
-          const uint32_t nr = std::min(per, nf - r0);
-          const uint64_t tot = uint64_t(nr) * n;
-          DevBuf<uint64_t> k1(tot, s), k2(tot, s);
-          DevBuf<uint32_t> v1(tot, s), v2(tot, s);
-          DevBuf<int> off(nr + 1, s);
-          k_exact_scores<<<uint32_t((tot + 255) / 256), 256, 0, s>>>(TQ, fail.p + r0, nr, K, n, d,
-                                                                     k1.p, v1.p);
-          k_seg_offsets<<<(nr + 1 + 255) / 256, 256, 0, s>>>(nr, n, off.p);
-          size_t tb = 0;
-          cub::DeviceSegmentedRadixSort::SortPairsDescending(nullptr, tb, k1.p, k2.p, v1.p, v2.p,
-                                                             int64_t(tot), int64_t(nr), off.p,
-                                                             off.p + 1, 0, 64, s);
-          DevBuf<uint8_t> tmp(tb, s);
-          RA_CUDA(cub::DeviceSegmentedRadixSort::SortPairsDescending(
-              tmp.p, tb, k1.p, k2.p, v1.p, v2.p, int64_t(tot), int64_t(nr), off.p, off.p + 1, 0, 64,
-              s));
-          k_take_top<<<uint32_t((uint64_t(nr) * kt + 255) / 256), 256, 0, s>>>(v2.p, nr, n, kt,
-                                                                               fail.p + r0, knn.p);
-          RA_LAUNCH_CHECK();
+        auto segmented = [&](const uint32_t* ids, uint32_t cnt_rows) {
+          for (uint32_t r0 = 0; r0 < cnt_rows; r0 += per) {
+            const uint32_t nr = std::min(per, cnt_rows - r0);
+            const uint64_t tot = uint64_t(nr) * n;
+            DevBuf<uint64_t> k1(tot, s), k2(tot, s);
+            DevBuf<uint32_t> v1(tot, s), v2(tot, s);
+            DevBuf<int> off(nr + 1, s);
+            k_exact_scores<<<uint32_t((tot + 255) / 256), 256, 0, s>>>(TQ, ids + r0, nr, K, n, d,
+                                                                       k1.p, v1.p);
+            k_seg_offsets<<<(nr + 1 + 255) / 256, 256, 0, s>>>(nr, n, off.p);
+            size_t tb = 0;
+            cub::DeviceSegmentedRadixSort::SortPairsDescending(nullptr, tb, k1.p, k2.p, v1.p, v2.p,
+                                                               int64_t(tot), int64_t(nr), off.p,
+                                                               off.p + 1, 0, 64, s);
+            DevBuf<uint8_t> tmp(tb, s);
+            RA_CUDA(cub::DeviceSegmentedRadixSort::SortPairsDescending(
+                tmp.p, tb, k1.p, k2.p, v1.p, v2.p, int64_t(tot), int64_t(nr), off.p, off.p + 1, 0,
+                64, s));
+            k_take_top<<<uint32_t((uint64_t(nr) * kt + 255) / 256), 256, 0, s>>>(v2.p, nr, n, kt,
+                                                                                 ids + r0, knn.p);
+            RA_LAUNCH_CHECK();
+          }
+        };
+        if (std::getenv("RA_KNN_SEGSORT")) {
+          segmented(fail.p, nf);
+        } else {
+          DevBuf<uint32_t> ovf(nf, s), novf(1, s);
+          RA_CUDA(cudaMemsetAsync(novf.p, 0, 4, s));
+          const uint32_t per_x = std::max<uint32_t>(1, uint32_t((512ull << 20) / (8ull * n)));
+          uint32_t xcap = XCAP;
+          if (const char* e = std::getenv("RA_KNN_TOPK_CAP"))  // (tests: force the sort path)
+            xcap = std::min<uint32_t>(XCAP, uint32_t(std::atoi(e)));
+          for (uint32_t r0 = 0; r0 < nf; r0 += per_x) {
+            const uint32_t nr = std::min(per_x, nf - r0);
+            const uint64_t tot = uint64_t(nr) * n;
+            DevBuf<uint64_t> k1(tot, s);
+            k_exact_scores<<<uint32_t((tot + 255) / 256), 256, 0, s>>>(TQ, fail.p + r0, nr, K, n, d,
+                                                                       k1.p, nullptr);
+            k_exact_topk<<<nr, XT, 0, s>>>(k1.p, n, kt, fail.p + r0, knn.p, ovf.p, novf.p, xcap);
+            RA_LAUNCH_CHECK();
+          }
+          uint32_t h_novf = 0;
+          RA_CUDA(cudaMemcpyAsync(&h_novf, novf.p, 4, cudaMemcpyDeviceToHost, s));
+          RA_CUDA(cudaStreamSynchronize(s));
+          if (h_novf) segmented(ovf.p, h_novf);
         }
         if (std::getenv("RA_KNN_TRACE")) {
           RA_CUDA(cudaStreamSynchronize(s));

@@ -769,7 +769,9 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
   DevBuf<uint32_t> fcount(1, s);
   RA_CUDA(cudaMemsetAsync(fcount.p, 0, 4, s));
   // |S - S~| <= (3 * 2^-16 + K3 * 2^-23) * |q| |k|; 2^-10 is generous
-  const double delta_scale = 1.0 / 1024.0;
+  double delta_scale = 1.0 / 1024.0;
+  if (const char* e = std::getenv("RA_KNN_DELTA_SCALE"))  // (tests: certificate failures)
+    delta_scale = std::max(delta_scale, std::atof(e));
   // pass 1: 8 rows per block, 512 rescored survivors per row in shared
   // memory (occupancy); rows whose certified band is wider go to pass 2
   constexpr uint32_t kCap1 = 512;

@@ -136,6 +136,37 @@ def test_edge_dedup_set_matches_sort_path():
     assert blobs[0] == blobs[1] == blobs[2]
 
 
+def test_knn_fallback_rows_topk_select_matches_sort():
+    """Rows the kNN certificate cannot vouch for are scored exactly against
+    every key; their top kt comes from a block radix select + shared-memory
+    sort. Widening the certificate forces most rows down that path: the
+    graph must equal the segmented-sort path's, the forced-overflow path's
+    (every row to the sort) and the exact f64 kernel's."""
+    ra = _ra()
+    import torch
+    from paper_2409_10516_b200.workload import WorkloadSpec, generate_group
+    w = generate_group(WorkloadSpec(n_ctx=8192, d_model=256, d_head=128, n_heads=4,
+                                    n_kv_groups=1, seed=31, n_decode=1), 0, "cuda")
+    kv = ra.KVGroup(w["keys"], w["values"])
+    bp = ra.OODGraphBuildParams(128, 24, 256, 8)
+    blobs, fb = [], []
+    for env in ({"RA_KNN_DELTA_SCALE": "0.05"},
+                {"RA_KNN_DELTA_SCALE": "0.05", "RA_KNN_SEGSORT": "1"},
+                {"RA_KNN_DELTA_SCALE": "0.05", "RA_KNN_TOPK_CAP": "64"},
+                {"RA_KNN_EXACT": "1"}, {}):
+        os.environ.update(env)
+        try:
+            g = ra.ood_build(kv, w["prefill_q"][0], bp)
+        finally:
+            for k in env:
+                del os.environ[k]
+        blobs.append(g.serialize())
+        fb.append(g.build_stats.knn_rows_widened)
+    torch.cuda.synchronize()
+    assert fb[0] > 500, fb
+    assert all(b == blobs[0] for b in blobs), fb
+
+
 def test_hand_built_line_graph():
     # test_index_oodgraph.cpp:71-111, 207-216
     ra = _ra()
