@@ -562,15 +562,17 @@ __global__ void __launch_bounds__(WARPS * 32)
         }
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const double* qq = qd + 4 * (c0 + c);
-          acc_a = fma(qq[0], (double)xa[c].x, acc_a);
-          acc_b = fma(qq[0], (double)xb[c].x, acc_b);
-          acc_a = fma(qq[1], (double)xa[c].y, acc_a);
-          acc_b = fma(qq[1], (double)xb[c].y, acc_b);
-          acc_a = fma(qq[2], (double)xa[c].z, acc_a);
-          acc_b = fma(qq[2], (double)xb[c].z, acc_b);
-          acc_a = fma(qq[3], (double)xa[c].w, acc_a);
-          acc_b = fma(qq[3], (double)xb[c].w, acc_b);
+          // (qd is 16-byte aligned: two 128-bit broadcasts per float4 column)
+          const double2 q01 = reinterpret_cast<const double2*>(qd)[2 * (c0 + c)];
+          const double2 q23 = reinterpret_cast<const double2*>(qd)[2 * (c0 + c) + 1];
+          acc_a = fma(q01.x, (double)xa[c].x, acc_a);
+          acc_b = fma(q01.x, (double)xb[c].x, acc_b);
+          acc_a = fma(q01.y, (double)xa[c].y, acc_a);
+          acc_b = fma(q01.y, (double)xb[c].y, acc_b);
+          acc_a = fma(q23.x, (double)xa[c].z, acc_a);
+          acc_b = fma(q23.x, (double)xb[c].z, acc_b);
+          acc_a = fma(q23.y, (double)xa[c].w, acc_a);
+          acc_b = fma(q23.y, (double)xb[c].w, acc_b);
         }
       }
       if (va) es[ia] = acc_a, ei[ia] = ida;
