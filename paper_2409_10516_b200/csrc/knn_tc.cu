@@ -480,6 +480,13 @@ __device__ __forceinline__ float fkey_inv(uint32_t k) {
 // WARPS rows per block, `cap` rescored survivors per row in shared memory;
 // rows with more (a wide certified band) go to `defer` for a pass with
 // cap = cb (or fail when defer is null). rows: the row ids (null = 0..nq).
+// one 32-byte read-only load (LDG.E.ENL2.256 on sm_100a); p 32-byte aligned
+__device__ __forceinline__ void ldg256(const float4* p, float4& lo, float4& hi) {
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z), "=f"(hi.w)
+      : "l"(p));
+}
+
 template <uint32_t WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
     k_rescore(const float* __restrict__ Q, const float* __restrict__ K, uint64_t nq, uint32_t d,
@@ -555,10 +562,14 @@ __global__ void __launch_bounds__(WARPS * 32)
       double acc_a = 0.0, acc_b = 0.0;
       for (uint32_t c0 = 0; c0 < d / 4; c0 += 8) {
         float4 xa[8], xb[8];
+        // 256-bit loads: each lane takes a whole 32-byte sector at once (with
+        // 16-byte loads every sector was requested twice from L2)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          xa[c] = va ? __ldg(ka + c0 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-          xb[c] = vb ? __ldg(kb + c0 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c = 0; c < 8; c += 2) {
+          const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+          xa[c] = xa[c + 1] = xb[c] = xb[c + 1] = z;
+          if (va) ldg256(ka + c0 + c, xa[c], xa[c + 1]);
+          if (vb) ldg256(kb + c0 + c, xb[c], xb[c + 1]);
         }
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
@@ -807,3 +818,4 @@ uint32_t knn_tc(ra_ctx* ctx, const float* Q, uint64_t nq, const float* K, uint32
 }
 
 }  // namespace ra
+
